@@ -1,0 +1,245 @@
+/*
+ * lbmg.h — C ABI of the B200-native ACM-MRT + immersed-boundary LBM step.
+ *
+ * This is the drop-in boundary for the reference solver path
+ * (/root/reference/proj/include/lbm).  Every entry point names the reference
+ * interface it replaces.  Plain C types only: pointers, sizes, POD structs.
+ * Host-side I/O is FP64 in the reference's canonical AoS order; device state
+ * is fp32 (DDF-shifted populations) on sm_100a.
+ *
+ * Error convention: every function returning int returns LBMG_OK (0) or one
+ * of the LBMG_ERR_* codes; lbmg_last_error() then holds the message.  The
+ * C++ mirror (include/lbm_b200.hpp) turns LBMG_ERR_CONFIG into
+ * lbm::ConfigError and LBMG_ERR_IO into lbm::IoError, like the reference
+ * (core.hpp:50-58).  Divergence is NOT an error: it is reported through
+ * lbmg_status, exactly like lbm::StepStatus (solver.hpp:47-52).
+ */
+#ifndef LBMG_H
+#define LBMG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LBMG_ABI_VERSION 1
+
+/* ---- status codes ------------------------------------------------------ */
+#define LBMG_OK 0
+#define LBMG_ERR_CONFIG 1 /* lbm::ConfigError */
+#define LBMG_ERR_CUDA 2   /* CUDA runtime failure / no device */
+#define LBMG_ERR_OOM 3    /* device allocation failed */
+#define LBMG_ERR_IO 4     /* lbm::IoError */
+#define LBMG_ERR_STATE 5  /* call not valid in the current state */
+
+/* ---- enums (values match the reference's enum order) ------------------- */
+/* collision.hpp:23 CollisionKind */
+enum { LBMG_BGK = 0, LBMG_RAW_MRT = 1, LBMG_CENTRAL_MRT = 2 };
+/* collision.hpp:25 RatePolicy */
+enum { LBMG_POLICY_CONSTANT = 0, LBMG_POLICY_RELAX_TOWARD_ONE = 1 };
+/* boundary.hpp:22 FaceCondition */
+enum { LBMG_NOSLIP = 0, LBMG_INLET = 1, LBMG_OUTFLOW = 2, LBMG_PERIODIC = 3 };
+/* scene.hpp:23 MeshConfig::Type (File is not supported: host asset I/O) */
+enum { LBMG_MESH_SPHERE = 0, LBMG_MESH_BOX = 1, LBMG_MESH_FIN_COMB = 2, LBMG_MESH_QUAD = 3 };
+/* ib.hpp:35 SamplingMethod */
+enum { LBMG_SAMPLING_DART = 0, LBMG_SAMPLING_ELIMINATION = 1 };
+/* scene.hpp:43 InitKind */
+enum { LBMG_INIT_UNIFORM = 0, LBMG_INIT_TAYLOR_GREEN = 1 };
+/* ib.hpp:33 AccumulationMode */
+enum { LBMG_IB_ATOMIC = 0, LBMG_IB_DETERMINISTIC = 1 };
+
+/* ---- scene description (mirrors SceneConfig, scene.hpp:49-78) ---------- */
+typedef struct {
+    int condition;      /* LBMG_NOSLIP..LBMG_PERIODIC */
+    double velocity[3]; /* inlet velocity (inlet density is 1) */
+} lbmg_face;
+
+typedef struct { /* MeshConfig, scene.hpp:22-33 */
+    int type;
+    double center[3], lo[3], hi[3], origin[3];
+    double radius;
+    int subdivisions;
+    int fins;
+    double fin_length, fin_height, fin_spacing;
+    double size, plane_z;
+} lbmg_mesh;
+
+typedef struct { /* SolidConfig, scene.hpp:35-40 + RigidMotion ib.hpp:111-115 */
+    lbmg_mesh mesh;
+    double poisson_radius;
+    int sampling;   /* LBMG_SAMPLING_* */
+    int has_motion; /* std::optional<RigidMotion> engaged */
+    double linear_velocity[3], angular_velocity[3], center[3];
+} lbmg_solid_config;
+
+typedef struct {
+    int nx, ny, nz;
+    double viscosity;
+    int kind;               /* LBMG_BGK.. */
+    double high_order_rate; /* rate of degree>=3 moment rows */
+    int policy;             /* LBMG_POLICY_* */
+    double policy_eps0;
+    int has_explicit_rates;
+    double rates[27]; /* canonical moment-row order (collision.cpp:24-30) */
+    lbmg_face faces[6]; /* order -x,+x,-y,+y,-z,+z (boundary.hpp:37) */
+    double body_force[3];
+    int n_solids;
+    const lbmg_solid_config* solids;
+    int init; /* LBMG_INIT_* */
+    double init_density;
+    double init_velocity[3];
+    double tg_u_max;
+    int regions;
+    unsigned threads_per_region; /* CPU-only knob; ignored by the GPU */
+    size_t alpha;                /* CSoA group size (Eq. 9) */
+    int block_edge;              /* ell: solid-sample block edge */
+    int ib_mode;                 /* LBMG_IB_* */
+    uint64_t seed;
+} lbmg_scene_config;
+
+/* StepStatus, solver.hpp:47-52 */
+typedef struct {
+    int ok;
+    int mach_warning;
+    long step;
+    char reason[120];
+} lbmg_status;
+
+/* TimingRow, io.hpp:50-54 (phase name, step, seconds) */
+typedef struct {
+    char phase[24];
+    long step;
+    double seconds;
+} lbmg_timing_row;
+
+typedef struct lbmg_scene lbmg_scene;   /* Scene, scene.hpp:92-96 */
+typedef struct lbmg_runner lbmg_runner; /* Runner, runner.hpp:25-83 */
+
+/* ---- library ----------------------------------------------------------- */
+int lbmg_abi_version(void);
+/* Thread-local message of the last failing call. */
+const char* lbmg_last_error(void);
+/* Number of visible CUDA devices (0 on a CPU-only host). */
+int lbmg_device_count(void);
+
+/* ---- scene setup (host C++) -------------------------------------------- */
+/* SceneConfig defaults, scene.hpp:49-78. */
+void lbmg_scene_config_default(lbmg_scene_config* cfg);
+/* SceneConfig::make_model + CollisionModel::validate (scene.cpp:28-45,
+ * collision.cpp:109-146) + BoundarySet::validate (boundary.cpp:7-15).
+ * Writes the 27 effective rates (canonical row order) when rates != NULL. */
+int lbmg_validate_config(const lbmg_scene_config* cfg, double* rates);
+/* build_scene, scene.cpp:341-366: samples every solid (seeded Poisson-disk),
+ * sets reference positions, orders by block_edge. */
+int lbmg_scene_build(const lbmg_scene_config* cfg, lbmg_scene** out);
+void lbmg_scene_destroy(lbmg_scene* s);
+int lbmg_scene_solid_count(const lbmg_scene* s);
+size_t lbmg_scene_sample_count(const lbmg_scene* s, int solid);
+/* SolidSampleSet arrays (ib.hpp:47-60) in stored order; any pointer may be
+ * NULL.  Vec3 arrays are n*3 doubles. */
+int lbmg_scene_samples(const lbmg_scene* s, int solid, double* positions,
+                       double* reference_positions, uint32_t* source_id, uint8_t* flagged,
+                       double* bbox_lo_hi /* 6 */, int* block_edge);
+/* Replaces a solid's sample set (positions, reference positions, source ids),
+ * e.g. with a set produced elsewhere.  bbox is recomputed. */
+int lbmg_scene_set_samples(lbmg_scene* s, int solid, size_t n, const double* positions,
+                           const double* reference_positions, const uint32_t* source_id);
+
+/* ---- host-side reference algorithms exposed for parity ------------------ */
+/* morton3, ib.cpp:13-25 */
+uint64_t lbmg_morton3(uint32_t x, uint32_t y, uint32_t z);
+/* reorder_samples, ib.cpp:231-292: permutation perm[new] = old. */
+int lbmg_reorder_permutation(size_t n, const double* positions, const uint32_t* source_id,
+                             int ell, uint32_t* perm);
+/* split_domain, decomp.cpp:5-18: z0z1[2*r], z0z1[2*r+1]. */
+int lbmg_split_domain(int nz, int m, int* z0z1);
+
+/* ---- runner (device engine) -------------------------------------------- */
+/* Runner(const Scene&, int regions, unsigned threads), runner.cpp:22-58.
+ * regions > 1 places every z-slab region on `device` (in-process halo
+ * exchange through device memory); world/rank mode is lbmg_runner_create_rank. */
+int lbmg_runner_create(const lbmg_scene* scene, int regions, int device, lbmg_runner** out);
+/* One region (z-slab `rank` of `world`) of a multi-process run: halos are
+ * exchanged by the caller through lbmg_runner_halo_* (NCCL send/recv). */
+int lbmg_runner_create_rank(const lbmg_scene* scene, int world, int rank, int device,
+                            lbmg_runner** out);
+void lbmg_runner_destroy(lbmg_runner* r);
+/* Runner::clone, runner.cpp:297-317 (deep copy of the device state). */
+int lbmg_runner_clone(const lbmg_runner* r, lbmg_runner** out);
+/* Run the engine's kernels on this stream (cudaStream_t as void*; NULL =
+ * the runner's own stream). */
+int lbmg_runner_set_stream(lbmg_runner* r, void* stream);
+
+/* Runner::advance, runner.cpp:121-230.  Synchronous on return.  When
+ * timings != NULL, up to timings_cap rows are appended (per-phase CUDA-event
+ * times) and *n_timings receives the count written. */
+int lbmg_runner_advance(lbmg_runner* r, long steps, lbmg_status* status,
+                        lbmg_timing_row* timings, size_t timings_cap, size_t* n_timings);
+long lbmg_runner_step_count(const lbmg_runner* r);
+int lbmg_runner_status(const lbmg_runner* r, lbmg_status* status);
+int lbmg_runner_dims(const lbmg_runner* r, int* nx, int* ny, int* nz);
+int lbmg_runner_region_count(const lbmg_runner* r);
+/* Runner::set_layout, runner.cpp:252-258. */
+int lbmg_runner_set_layout(lbmg_runner* r, int block_edge, size_t alpha);
+size_t lbmg_runner_alpha(const lbmg_runner* r);
+int lbmg_runner_block_edge(const lbmg_runner* r);
+
+/* Runner::gather_rho/u/f, runner.cpp:260-295: canonical AoS FP64 over the
+ * global grid (n_nodes*{1,3,27} doubles).  In rank mode: this rank's owned
+ * planes only, z-offset by the slab start (see lbmg_runner_slab). */
+int lbmg_runner_gather_rho(const lbmg_runner* r, double* out);
+int lbmg_runner_gather_u(const lbmg_runner* r, double* out);
+int lbmg_runner_gather_f(const lbmg_runner* r, double* out);
+int lbmg_runner_slab(const lbmg_runner* r, int* z0, int* z1);
+
+/* Runner::totals_log, runner.hpp:52: 6 doubles (force, torque) per step. */
+size_t lbmg_runner_totals_count(const lbmg_runner* r);
+int lbmg_runner_totals(const lbmg_runner* r, double* out, size_t cap_steps);
+
+/* Runner::region_solids, runner.hpp:56: per-region sample replica. */
+size_t lbmg_runner_sample_count(const lbmg_runner* r, int region, int solid);
+int lbmg_runner_samples(const lbmg_runner* r, int region, int solid, double* positions,
+                        double* boundary_velocity, double* penalty_force,
+                        double* sampled_velocity, uint32_t* source_id, uint8_t* flagged);
+
+/* Cell flags: owner face of every (node, direction) pull, as decided by
+ * face_owns_direction (boundary.cpp:28-40) on the device: out[k*27+i] is the
+ * face 0..5 that reconstructs f*_i at node k, or 255 when the pull streams. */
+int lbmg_runner_cell_flags(const lbmg_runner* r, uint8_t* out);
+
+/* ---- multi-process halo exchange (rank mode) ---------------------------- */
+/* Device pointers of this rank's outgoing / incoming population halos of
+ * buffer `parity`: the fluid phase of step t fills send[(t+1)&1] and step t+1
+ * reads recv[(t+1)&1]; after creation send[0] must be moved to the
+ * neighbours' recv[0].  send_lo carries the c_z=-1 populations of the bottom
+ * owned plane (to rank-1), send_hi the c_z=+1 populations of the top plane
+ * (to rank+1); each is 9*nx*ny floats.  NULL where the slab has no such
+ * neighbour (periodic z wraps rank 0 <-> rank world-1). */
+int lbmg_runner_halo_f(lbmg_runner* r, int parity, void** send_lo, void** send_hi, void** recv_lo,
+                       void** recv_hi, size_t* bytes);
+/* Same for the (rho,u) plane exchange the IB phase needs (4*nx*ny floats). */
+int lbmg_runner_halo_macro(lbmg_runner* r, void** send_lo, void** send_hi, void** recv_lo,
+                           void** recv_hi, size_t* bytes);
+/* Split step for rank mode: PRE = IB band moments (+ pack macro halo);
+ * MID = IB interpolate/penalty/spread + totals + motion; FLUID_EDGE = the
+ * fused update of the two boundary planes (+ pack f halo); FLUID_BULK = the
+ * rest; END = step bookkeeping.  The caller exchanges halos between phases. */
+enum { LBMG_PHASE_PRE = 0, LBMG_PHASE_MID = 1, LBMG_PHASE_FLUID_EDGE = 2,
+       LBMG_PHASE_FLUID_BULK = 3, LBMG_PHASE_END = 4 };
+int lbmg_runner_phase(lbmg_runner* r, int phase, int write_macro);
+/* After an externally driven run: synchronise and fold device status/totals
+ * into the host-side Runner state (like the tail of lbmg_runner_advance). */
+int lbmg_runner_sync(lbmg_runner* r, lbmg_status* status);
+
+/* ---- kernel-level entry points (unit parity, GPU) ----------------------- */
+/* collide (collision.cpp:207-212) of n nodes on the device, fp32 arithmetic:
+ * f (n*27), rho (n), u (n*3) host FP64 in, omega (n*27) host FP64 out. */
+int lbmg_collide_batch(const lbmg_scene_config* model_cfg, size_t n, const double* f,
+                       const double* rho, const double* u, double* omega);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LBMG_H */

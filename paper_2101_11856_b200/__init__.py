@@ -1,0 +1,21 @@
+"""B200-native ACM-MRT + immersed-boundary lattice-Boltzmann step
+(arXiv 2101.11856) behind the reference solver's API.
+
+    from paper_2101_11856_b200 import SceneConfig, build_scene, Runner
+    scene = build_scene(cfg)          # host setup (sampling, ordering)
+    r = Runner(scene)                 # device state on cuda:0
+    r.advance(100)                    # fused sm_100a step kernels
+    rho = r.gather_rho()              # canonical AoS FP64 readback
+"""
+from .scene import (ConfigError, FaceSpec, MeshConfig, RigidMotion, SceneConfig, SolidConfig,
+                    load_scene_config, parse_scene_config)
+from .runner import (CudaError, Runner, Scene, StateError, StepStatus, TimingRow, build_scene,
+                     collide_batch, device_count, lib, model_rates, morton3, reorder_permutation,
+                     split_domain)
+
+__all__ = [
+    "ConfigError", "FaceSpec", "MeshConfig", "RigidMotion", "SceneConfig", "SolidConfig",
+    "load_scene_config", "parse_scene_config", "CudaError", "Runner", "Scene", "StateError",
+    "StepStatus", "TimingRow", "build_scene", "collide_batch", "device_count", "lib", "model_rates",
+    "morton3", "reorder_permutation", "split_domain",
+]

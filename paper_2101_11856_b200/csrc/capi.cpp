@@ -1,0 +1,396 @@
+// extern "C" surface (include/lbmg.h).  Exceptions never cross the ABI:
+// each entry point maps them to an LBMG_ERR_* code + lbmg_last_error().
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "lbmg.h"
+#include "runner.hpp"
+#include "scene.hpp"
+
+using namespace lbmg;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return LBMG_OK;
+    } catch (const lbmg::ConfigError& e) {
+        g_err = e.what();
+        return LBMG_ERR_CONFIG;
+    } catch (const OomError& e) {
+        g_err = e.what();
+        return LBMG_ERR_OOM;
+    } catch (const CudaError& e) {
+        g_err = e.what();
+        return LBMG_ERR_CUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return LBMG_ERR_STATE;
+    }
+}
+
+void put_status(const Status& s, lbmg_status* o) {
+    if (!o) return;
+    o->ok = s.ok ? 1 : 0;
+    o->mach_warning = s.mach_warning ? 1 : 0;
+    o->step = s.step;
+    std::snprintf(o->reason, sizeof o->reason, "%s", s.reason.c_str());
+}
+
+Runner& R(lbmg_runner* r) {
+    if (!r || !r->impl) throw StateError("null runner");
+    return *r->impl;
+}
+const Runner& R(const lbmg_runner* r) {
+    if (!r || !r->impl) throw StateError("null runner");
+    return *r->impl;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lbmg_abi_version(void) { return LBMG_ABI_VERSION; }
+const char* lbmg_last_error(void) { return g_err.c_str(); }
+
+int lbmg_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+void lbmg_scene_config_default(lbmg_scene_config* c) {
+    std::memset(c, 0, sizeof *c);
+    c->viscosity = 0.05;
+    c->kind = LBMG_BGK;
+    c->high_order_rate = 1.0;
+    c->policy = LBMG_POLICY_CONSTANT;
+    c->policy_eps0 = 0.01;
+    for (int f = 0; f < 6; ++f) c->faces[f].condition = LBMG_NOSLIP;
+    c->init = LBMG_INIT_UNIFORM;
+    c->init_density = 1.0;
+    c->tg_u_max = 0.02;
+    c->regions = 1;
+    c->alpha = 1;
+    c->block_edge = 1;
+    c->ib_mode = LBMG_IB_ATOMIC;
+    c->seed = 1;
+}
+
+int lbmg_validate_config(const lbmg_scene_config* cfg, double* rates) {
+    return guarded([&] {
+        validate_config(*cfg);
+        if (rates) {
+            auto r = make_rates(*cfg);
+            for (int i = 0; i < 27; ++i) rates[i] = r[i];
+        }
+    });
+}
+
+// build_scene, scene.cpp:341-366.
+int lbmg_scene_build(const lbmg_scene_config* cfg, lbmg_scene** out) {
+    return guarded([&] {
+        validate_config(*cfg);
+        auto* s = new lbmg_scene;
+        try {
+            s->cfg = *cfg;
+            s->solid_cfgs.assign(cfg->solids, cfg->solids + cfg->n_solids);
+            s->cfg.solids = s->solid_cfgs.empty() ? nullptr : s->solid_cfgs.data();
+            uint64_t seed = cfg->seed;
+            for (const auto& sc : s->solid_cfgs) {
+                SolidInstance inst;
+                inst.cfg = sc;
+                const TriMesh mesh = build_mesh(sc.mesh);
+                inst.samples = sample_surface(mesh, sc.poisson_radius, seed++, sc.sampling, &inst.report);
+                if (sc.has_motion) {
+                    inst.moving = true;
+                    inst.linear_velocity = v3(sc.linear_velocity);
+                    inst.angular_velocity = v3(sc.angular_velocity);
+                    inst.center = v3(sc.center);
+                    for (size_t k = 0; k < inst.samples.size(); ++k)
+                        inst.samples.reference_positions[k] = inst.samples.positions[k] - inst.center;
+                } else {
+                    inst.samples.reference_positions = inst.samples.positions;
+                }
+                reorder_samples(inst.samples, cfg->block_edge);
+                s->solids.push_back(std::move(inst));
+            }
+        } catch (...) {
+            delete s;
+            throw;
+        }
+        *out = s;
+    });
+}
+
+void lbmg_scene_destroy(lbmg_scene* s) { delete s; }
+
+int lbmg_scene_solid_count(const lbmg_scene* s) { return s ? int(s->solids.size()) : 0; }
+
+size_t lbmg_scene_sample_count(const lbmg_scene* s, int solid) {
+    if (!s || solid < 0 || solid >= int(s->solids.size())) return 0;
+    return s->solids[solid].samples.size();
+}
+
+int lbmg_scene_samples(const lbmg_scene* s, int solid, double* pos, double* refpos, uint32_t* src,
+                       uint8_t* flagged, double* bbox, int* ell) {
+    return guarded([&] {
+        if (!s || solid < 0 || solid >= int(s->solids.size())) throw StateError("solid index out of range");
+        const SampleSet& set = s->solids[solid].samples;
+        for (size_t k = 0; k < set.size(); ++k) {
+            for (int a = 0; a < 3; ++a) {
+                if (pos) pos[3 * k + a] = set.positions[k][a];
+                if (refpos) refpos[3 * k + a] = set.reference_positions[k][a];
+            }
+            if (src) src[k] = set.source_id[k];
+            if (flagged) flagged[k] = 0;
+        }
+        if (bbox)
+            for (int a = 0; a < 3; ++a) {
+                bbox[a] = set.bbox_lo[a];
+                bbox[3 + a] = set.bbox_hi[a];
+            }
+        if (ell) *ell = set.block_edge;
+    });
+}
+
+int lbmg_scene_set_samples(lbmg_scene* s, int solid, size_t n, const double* pos, const double* refpos,
+                           const uint32_t* src) {
+    return guarded([&] {
+        if (!s || solid < 0 || solid >= int(s->solids.size())) throw StateError("solid index out of range");
+        SampleSet& set = s->solids[solid].samples;
+        set.positions.resize(n);
+        set.reference_positions.resize(n);
+        set.source_id.resize(n);
+        set.bbox_lo = {1e300, 1e300, 1e300};
+        set.bbox_hi = {-1e300, -1e300, -1e300};
+        for (size_t k = 0; k < n; ++k) {
+            set.positions[k] = v3(pos + 3 * k);
+            set.reference_positions[k] = v3(refpos + 3 * k);
+            set.source_id[k] = src[k];
+            for (int a = 0; a < 3; ++a) {
+                set.bbox_lo[a] = std::min(set.bbox_lo[a], set.positions[k][a]);
+                set.bbox_hi[a] = std::max(set.bbox_hi[a], set.positions[k][a]);
+            }
+        }
+    });
+}
+
+uint64_t lbmg_morton3(uint32_t x, uint32_t y, uint32_t z) { return morton3(x, y, z); }
+
+int lbmg_reorder_permutation(size_t n, const double* positions, const uint32_t* source_id, int ell,
+                             uint32_t* perm) {
+    return guarded([&] {
+        std::vector<V3> p(n);
+        for (size_t k = 0; k < n; ++k) p[k] = v3(positions + 3 * k);
+        auto out = reorder_permutation(p, std::vector<uint32_t>(source_id, source_id + n), ell);
+        std::memcpy(perm, out.data(), n * sizeof(uint32_t));
+    });
+}
+
+int lbmg_split_domain(int nz, int m, int* z0z1) {
+    return guarded([&] {
+        auto s = split_domain(nz, m);
+        for (int r = 0; r < m; ++r) {
+            z0z1[2 * r] = s[r][0];
+            z0z1[2 * r + 1] = s[r][1];
+        }
+    });
+}
+
+int lbmg_runner_create(const lbmg_scene* scene, int regions, int device, lbmg_runner** out) {
+    return guarded([&] {
+        if (!scene) throw StateError("null scene");
+        auto* r = new lbmg_runner;
+        try {
+            r->impl = std::make_unique<Runner>(*scene, regions, device, 0, 0);
+        } catch (...) {
+            delete r;
+            throw;
+        }
+        *out = r;
+    });
+}
+
+int lbmg_runner_create_rank(const lbmg_scene* scene, int world, int rank, int device, lbmg_runner** out) {
+    return guarded([&] {
+        if (!scene) throw StateError("null scene");
+        if (world < 1) throw lbmg::ConfigError("world must be >= 1");
+        auto* r = new lbmg_runner;
+        try {
+            r->impl = std::make_unique<Runner>(*scene, 1, device, world, rank);
+        } catch (...) {
+            delete r;
+            throw;
+        }
+        *out = r;
+    });
+}
+
+void lbmg_runner_destroy(lbmg_runner* r) { delete r; }
+
+int lbmg_runner_clone(const lbmg_runner* r, lbmg_runner** out) {
+    return guarded([&] {
+        auto* c = new lbmg_runner;
+        try {
+            c->impl = R(r).clone();
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+int lbmg_runner_set_stream(lbmg_runner* r, void* stream) {
+    return guarded([&] { R(r).set_stream(static_cast<cudaStream_t>(stream)); });
+}
+
+int lbmg_runner_advance(lbmg_runner* r, long steps, lbmg_status* status, lbmg_timing_row* rows, size_t cap,
+                        size_t* n_rows) {
+    return guarded([&] {
+        std::vector<Timing> t;
+        Status st = R(r).advance(steps, rows ? &t : nullptr);
+        put_status(st, status);
+        if (rows) {
+            size_t k = 0;
+            for (; k < t.size() && k < cap; ++k) {
+                std::snprintf(rows[k].phase, sizeof rows[k].phase, "%s", t[k].phase.c_str());
+                rows[k].step = t[k].step;
+                rows[k].seconds = t[k].seconds;
+            }
+            if (n_rows) *n_rows = k;
+        }
+    });
+}
+
+long lbmg_runner_step_count(const lbmg_runner* r) { return r && r->impl ? r->impl->step_count() : -1; }
+
+int lbmg_runner_status(const lbmg_runner* r, lbmg_status* status) {
+    return guarded([&] { put_status(R(r).status(), status); });
+}
+
+int lbmg_runner_dims(const lbmg_runner* r, int* nx, int* ny, int* nz) {
+    return guarded([&] {
+        *nx = R(r).nx();
+        *ny = R(r).ny();
+        *nz = R(r).nz();
+    });
+}
+
+int lbmg_runner_region_count(const lbmg_runner* r) { return r && r->impl ? r->impl->region_count() : 0; }
+
+int lbmg_runner_set_layout(lbmg_runner* r, int block_edge, size_t alpha) {
+    return guarded([&] { R(r).set_layout(block_edge, alpha); });
+}
+
+size_t lbmg_runner_alpha(const lbmg_runner* r) { return r && r->impl ? r->impl->alpha() : 0; }
+int lbmg_runner_block_edge(const lbmg_runner* r) { return r && r->impl ? r->impl->block_edge() : 0; }
+
+int lbmg_runner_gather_rho(const lbmg_runner* r, double* out) {
+    return guarded([&] { R(r).gather(0, out); });
+}
+int lbmg_runner_gather_u(const lbmg_runner* r, double* out) {
+    return guarded([&] { R(r).gather(1, out); });
+}
+int lbmg_runner_gather_f(const lbmg_runner* r, double* out) {
+    return guarded([&] { R(r).gather(2, out); });
+}
+int lbmg_runner_slab(const lbmg_runner* r, int* z0, int* z1) {
+    return guarded([&] { R(r).slab(z0, z1); });
+}
+
+size_t lbmg_runner_totals_count(const lbmg_runner* r) {
+    return r && r->impl ? r->impl->totals_log().size() : 0;
+}
+
+int lbmg_runner_totals(const lbmg_runner* r, double* out, size_t cap) {
+    return guarded([&] {
+        const auto& log = R(r).totals_log();
+        for (size_t s = 0; s < log.size() && s < cap; ++s)
+            for (int a = 0; a < 6; ++a) out[6 * s + a] = log[s][a];
+    });
+}
+
+size_t lbmg_runner_sample_count(const lbmg_runner* r, int region, int solid) {
+    try {
+        return R(r).sample_count(region, solid);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 0;
+    }
+}
+
+int lbmg_runner_samples(const lbmg_runner* r, int region, int solid, double* pos, double* ub, double* force,
+                        double* sampled, uint32_t* src, uint8_t* flagged) {
+    return guarded([&] { R(r).samples(region, solid, pos, ub, force, sampled, src, flagged); });
+}
+
+int lbmg_runner_cell_flags(const lbmg_runner* r, uint8_t* out) {
+    return guarded([&] { R(r).cell_flags(out); });
+}
+
+int lbmg_runner_halo_f(lbmg_runner* r, int parity, void** sl, void** sh, void** rl, void** rh, size_t* b) {
+    return guarded([&] { R(r).halo_f(parity, sl, sh, rl, rh, b); });
+}
+
+int lbmg_runner_halo_macro(lbmg_runner* r, void** sl, void** sh, void** rl, void** rh, size_t* b) {
+    return guarded([&] { R(r).halo_macro(sl, sh, rl, rh, b); });
+}
+
+int lbmg_runner_phase(lbmg_runner* r, int phase, int write_macro) {
+    return guarded([&] { R(r).phase(phase, write_macro); });
+}
+
+int lbmg_runner_sync(lbmg_runner* r, lbmg_status* status) {
+    return guarded([&] { put_status(R(r).sync_external(), status); });
+}
+
+int lbmg_collide_batch(const lbmg_scene_config* cfg, size_t n, const double* f, const double* rho,
+                       const double* u, double* omega) {
+    return guarded([&] {
+        const auto rates = make_rates(*cfg);
+        const auto& T = model_tables();
+        ModelConst m{};
+        m.kind = cfg->kind;
+        m.policy = cfg->kind == LBMG_CENTRAL_MRT ? cfg->policy : LBMG_POLICY_CONSTANT;
+        m.omega = float(1.0 / (3.0 * cfg->viscosity + 0.5));
+        m.eps0 = float(cfg->policy_eps0);
+        for (int mu = 0; mu < 27; ++mu) m.rate[mu] = float(rates[T.mu_to_row[mu]]);
+        double *df = nullptr, *dr = nullptr, *du = nullptr, *dom = nullptr;
+        auto cleanup = [&] {
+            cudaFree(df);
+            cudaFree(dr);
+            cudaFree(du);
+            cudaFree(dom);
+        };
+        try {
+            cuda_check(cudaMalloc(&df, n * 27 * 8 + 8), "cudaMalloc");
+            cuda_check(cudaMalloc(&dr, n * 8 + 8), "cudaMalloc");
+            cuda_check(cudaMalloc(&du, n * 24 + 8), "cudaMalloc");
+            cuda_check(cudaMalloc(&dom, n * 27 * 8 + 8), "cudaMalloc");
+            cuda_check(cudaMemcpy(df, f, n * 27 * 8, cudaMemcpyHostToDevice), "H2D f");
+            cuda_check(cudaMemcpy(dr, rho, n * 8, cudaMemcpyHostToDevice), "H2D rho");
+            cuda_check(cudaMemcpy(du, u, n * 24, cudaMemcpyHostToDevice), "H2D u");
+            launch_collide_batch(m, unsigned(n), df, dr, du, dom, nullptr);
+            cuda_check(cudaGetLastError(), "collide_batch launch");
+            cuda_check(cudaMemcpy(omega, dom, n * 27 * 8, cudaMemcpyDeviceToHost), "D2H omega");
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        cleanup();
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,182 @@
+// Device-side region description, kernel parameter blocks and the
+// boundary-ownership logic shared by the fused fluid kernel and the IB band
+// pre-pass.
+//
+// HBM layout of one region (a z-slab of owned planes):
+//   f[2]        27 fp32 populations per node, DDF-shifted (f_i - w_i), in the
+//               paper's CSoA layout (Eq. 9, layout.hpp:41-52) with group
+//               alpha = 2^la; alpha >= n_pad is plain SoA.  A/B by step parity.
+//   rho, u      fp32 rho* and u* (u as 3 SoA planes of stride ns)
+//   gib, tflag  fp32 IB force density (3 SoA planes) + one byte per 32 nodes
+//   slot[2][6]  per-face persistent f* of the 9 populations each face
+//               reconstructs (needed for the stale outflow-edge read,
+//               SURVEY App. A.3), A/B by parity
+//   halo        9 crossing populations of the neighbour's boundary plane
+//               (c_z=+1 from below, c_z=-1 from above), A/B by parity
+#pragma once
+
+#include <cstdint>
+
+#include "lattice.cuh"
+
+namespace lbmg {
+
+enum : int { kNoSlip = 0, kInlet = 1, kOutflow = 2, kPeriodic = 3 };
+enum : int { kBGK = 0, kRawMRT = 1, kCentralMRT = 2 };
+enum : int { kPolicyConstant = 0, kPolicyRelax = 1 };
+constexpr unsigned char kNoOwner = 255;
+
+// n / d for n < 2^31 with a precomputed magic number (round-up method).
+struct FastDiv {
+    unsigned d = 1, mul = 0, shift = 0;
+    FastDiv() = default;
+    explicit FastDiv(unsigned dv) : d(dv) {
+        shift = 0;
+        while ((1u << shift) < d) ++shift;
+        unsigned long long m = ((1ull << 32) * ((1ull << shift) - d)) / d + 1;
+        mul = static_cast<unsigned>(m);
+    }
+    LBMG_HD unsigned div(unsigned n) const {
+#ifdef __CUDA_ARCH__
+        return (__umulhi(n, mul) + n) >> shift;
+#else
+        return static_cast<unsigned>(((static_cast<unsigned long long>(n) * mul >> 32) + n) >> shift);
+#endif
+    }
+};
+
+struct RegionGeo {
+    int nx, ny, nzl;      // owned local dims
+    int NZ;               // global nz
+    int gz0;              // global z of local plane 0
+    int per[3];           // periodic axes
+    unsigned plane;       // nx*ny
+    unsigned n;           // owned nodes
+    unsigned n_pad;       // padded node count (multiple of alpha, or of 32 for SoA)
+    int la;               // log2(alpha); 31 for SoA
+    unsigned amask;       // alpha-1; 0x7fffffff for SoA
+    unsigned A;           // per-direction stride inside a group: alpha, or n_pad for SoA
+    unsigned ns;          // stride of the per-node SoA fields (rho, u, gib): n rounded to 32
+    FastDiv div_nx, div_ny;
+
+    // Eq. 9 (layout.hpp:41-52): beta*alpha*floor(k/alpha) + alpha*i + k mod alpha
+    LBMG_HD unsigned long long idx(unsigned k, int i) const {
+        return static_cast<unsigned long long>(k >> la) * (27ull * A) +
+               static_cast<unsigned long long>(static_cast<unsigned>(i)) * A + (k & amask);
+    }
+    LBMG_HD unsigned node(int x, int y, int lz) const {
+        return (static_cast<unsigned>(lz) * static_cast<unsigned>(ny) + static_cast<unsigned>(y)) *
+                   static_cast<unsigned>(nx) +
+               static_cast<unsigned>(x);
+    }
+    LBMG_HD int extent(int a) const { return a == 0 ? nx : (a == 1 ? ny : NZ); }
+    // Face-plane (slot) extents: x faces (y, lz), y faces (x, lz), z faces (x, y).
+    LBMG_HD unsigned slot_plane(int face) const {
+        int a = face_axis(face);
+        return a == 0 ? unsigned(ny) * nzl : (a == 1 ? unsigned(nx) * nzl : plane);
+    }
+    LBMG_HD unsigned slot_index(int face, int x, int y, int lz, int i) const {
+        int a = face_axis(face);
+        unsigned u = a == 0 ? y : x;
+        unsigned v = a == 2 ? y : lz;
+        unsigned U = a == 0 ? ny : nx;
+        return cross9(i, a) * slot_plane(face) + v * U + u;
+    }
+};
+
+struct FaceTable {
+    int cond[6];
+    float inlet[6][27];  // feq(1, u_in)_i - w_i per inlet face
+};
+
+struct ModelConst {
+    int kind;
+    int policy;
+    float omega;     // BGK rate omega_nu
+    float eps0;      // policy epsilon_0
+    float rate[27];  // by moment tensor index mu
+    float body[3];   // body force
+};
+
+// Pointers of one region; the [2] arrays are selected by step parity p=t&1:
+// f[p] = f(t) in, f[p^1] = f(t+1) out; slot[p] = f* slots of step t-1 (read
+// for stale outflow), slot[p^1] written; recv[p] = f(t) neighbour halo in;
+// send[p^1] = f(t+1) halo out.
+struct RegionPtrs {
+    float* f[2];
+    float* slot[2][6];
+    const float* recv_lo[2];
+    const float* recv_hi[2];
+    float* send_lo[2];
+    float* send_hi[2];
+    float* rho;
+    float* u;    // 3 planes of ns
+    float* gib;  // 3 planes of ns, or null without solids
+    unsigned char* tflag;
+    const float* mrecv_lo;  // (rho,u) of the ghost planes, 4*plane
+    const float* mrecv_hi;
+    float* msend_lo;
+    float* msend_hi;
+    unsigned* band_count;  // IB band nodes this step
+};
+
+struct DevCounters {
+    long long t;               // step counter
+    unsigned diverged;         // sticky divergence flag
+    unsigned mach;             // sticky Mach warning
+    long long diverged_step;   // step at which divergence was detected
+    long long chunk_t0;        // first step of the current advance chunk
+};
+
+struct FluidParams {
+    RegionGeo g;
+    FaceTable faces;
+    ModelConst m;
+    RegionPtrs p;
+    DevCounters* ctr;
+};
+
+// Owner face of the pull of direction i at global (gx, gy, gz): the first
+// non-periodic face in pass order whose side the source x - c_i lies beyond,
+// or kNoOwner when the pull streams (boundary.cpp:28-40).
+template <int I>
+LBMG_HD int owner_face_c(const RegionGeo& g, int gx, int gy, int gz) {
+    constexpr int c0 = cx(I), c1 = cy(I), c2 = cz(I);
+    if constexpr (c0 != 0) {
+        if (!g.per[0]) {
+            int s = gx - c0;
+            if (s < 0) return 0;
+            if (s >= g.nx) return 1;
+        }
+    }
+    if constexpr (c1 != 0) {
+        if (!g.per[1]) {
+            int s = gy - c1;
+            if (s < 0) return 2;
+            if (s >= g.ny) return 3;
+        }
+    }
+    if constexpr (c2 != 0) {
+        if (!g.per[2]) {
+            int s = gz - c2;
+            if (s < 0) return 4;
+            if (s >= g.NZ) return 5;
+        }
+    }
+    return kNoOwner;
+}
+
+// Runtime-direction variant (used on the rare reconstruction chains).
+LBMG_HD int owner_face(const RegionGeo& g, int gx, int gy, int gz, int i) {
+    const int c[3] = {cx(i), cy(i), cz(i)};
+    const int coord[3] = {gx, gy, gz};
+    for (int f = 0; f < 6; ++f) {
+        int a = face_axis(f);
+        if (g.per[a] || c[a] == 0) continue;
+        int s = coord[a] - c[a];
+        if (face_side(f) < 0 ? s < 0 : s >= g.extent(a)) return f;
+    }
+    return kNoOwner;
+}
+
+}  // namespace lbmg

@@ -1,0 +1,61 @@
+// Host-visible declarations of the device engine (kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "device_common.cuh"
+
+namespace lbmg {
+
+// Device replica of one SolidSampleSet (ib.hpp:47-60), SoA of FP64 Vec3.
+struct IbSolidDev {
+    unsigned n;
+    double* pos;      // n*3
+    double* ref;      // n*3
+    double* ub;       // n*3
+    double* force;    // n*3
+    double* sampled;  // n*3
+    unsigned* source;
+    unsigned char* flagged;
+};
+
+// Motion table row per step: center(t)[3], R(t)[9], v[3], omega[3].
+constexpr int kMotionRow = 18;
+
+struct InitParams {
+    int kind;  // 0 uniform, 1 Taylor-Green
+    double rho0;
+    double u0[3];
+    double tg_u;
+    int NX, NY;
+};
+
+void launch_fluid(const FluidParams& P, unsigned k0, unsigned k1, int write_macro, cudaStream_t st);
+void launch_macro(const FluidParams& P, int parity, cudaStream_t st);
+void launch_ib_mark(const FluidParams& P, const IbSolidDev& S, unsigned* stamp, unsigned* band,
+                    cudaStream_t st);
+void launch_ib_band(const FluidParams& P, const unsigned* band, int sm_count, cudaStream_t st);
+void launch_macro_pack(const FluidParams& P, cudaStream_t st);
+void launch_ib_spread(const FluidParams& P, const IbSolidDev& S, cudaStream_t st);
+int totals_blocks(size_t n);
+// table: motion rows per step from DevCounters::chunk_t0; stride in doubles per step
+void launch_ib_totals(const FluidParams& P, const IbSolidDev& S, const double* table, double* partial,
+                      double* out_base, int stride, cudaStream_t st);
+void launch_ib_motion(const DevCounters* ctr, const IbSolidDev& S, const double* table, int nx, int ny,
+                      int nz, cudaStream_t st);
+void launch_ib_motion_once(const IbSolidDev& S, const double* row, int nx, int ny, int nz,
+                           cudaStream_t st);
+void launch_step_end(DevCounters* ctr, cudaStream_t st);
+void launch_init(const FluidParams& P, const InitParams& ip, cudaStream_t st);
+void launch_read_f(const FluidParams& P, int parity, unsigned k0, unsigned k1, double* out,
+                   cudaStream_t st);
+void launch_read_macro(const FluidParams& P, unsigned k0, unsigned k1, double* rho, double* u,
+                       cudaStream_t st);
+void launch_cell_flags(const FluidParams& P, unsigned k0, unsigned k1, unsigned char* out,
+                       cudaStream_t st);
+void launch_relayout(const float* src, float* dst, const RegionGeo& gs, const RegionGeo& gd,
+                     cudaStream_t st);
+void launch_collide_batch(const ModelConst& m, unsigned n, const double* f, const double* rho,
+                          const double* u, double* omega, cudaStream_t st);
+
+}  // namespace lbmg

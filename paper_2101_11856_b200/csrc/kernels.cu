@@ -1,0 +1,770 @@
+// sm_100a kernels of the ACM-MRT + IB step.  Every kernel reads the step
+// counter from device memory (parity selects the A/B buffers), so one step is
+// a fixed launch sequence that replays unchanged inside a CUDA graph.
+//
+// Step (runner.cpp:121-230, fused):
+//   ib_mark      per sample: kernel support, flag, band-node dedup (stamp)
+//   ib_band      per band node: pull + face passes + moments -> rho*, u*
+//   (macro halo) rho/u of the boundary planes to the neighbour slabs
+//   ib_spread    per sample: interpolate, penalty, scatter into g (smem hash)
+//   ib_totals    per solid FP64 reaction force/torque (deterministic order)
+//   ib_motion    per sample: rigid motion to t+1 (moving solids)
+//   fluid        per node: pull-stream + six face passes + moments + CM-MRT
+//                (+ adaptive rates) + forcing; writes f(t+1), the crossing
+//                populations of the boundary planes into the neighbours' halo,
+//                and the face slots
+//   step_end     t += 1 unless diverged
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "collision.cuh"
+#include "device_common.cuh"
+#include "engine.hpp"
+
+namespace lbmg {
+
+namespace {
+
+struct StepView {
+    const float* fin;
+    const float* halo_lo;
+    const float* halo_hi;
+    const float* slot_prev[6];
+};
+
+__device__ __forceinline__ StepView make_view(const FluidParams& P, int p) {
+    StepView v;
+    v.fin = P.p.f[p];
+    v.halo_lo = P.p.recv_lo[p];
+    v.halo_hi = P.p.recv_hi[p];
+#pragma unroll
+    for (int f = 0; f < 6; ++f) v.slot_prev[f] = P.p.slot[p][f];
+    return v;
+}
+
+// Streamed value f_i(x - c_i) for a pull that is not missing (stream,
+// solver.cpp:46-87): periodic wrap in x/y, ghost planes from the halo.
+__device__ __forceinline__ float pull_rt(const RegionGeo& g, const StepView& v, int x, int y,
+                                         int lz, int i) {
+    int sx = x - cx(i), sy = y - cy(i);
+    if (sx < 0) sx += g.nx; else if (sx >= g.nx) sx -= g.nx;
+    if (sy < 0) sy += g.ny; else if (sy >= g.ny) sy -= g.ny;
+    const int lzs = lz - cz(i);
+    const unsigned hp = cross9(i, 2) * g.plane + unsigned(sy) * g.nx + unsigned(sx);
+    if (lzs < 0) return v.halo_lo[hp];
+    if (lzs >= g.nzl) return v.halo_hi[hp];
+    return v.fin[g.idx(g.node(sx, sy, lzs), i)];
+}
+
+// f*_i at (x,y,lz) after the face pass `owner` has run this step
+// (apply_face, boundary.cpp:42-118).  Outflow copies f*_i of the interior
+// neighbour as it stands at that point of the pass sequence: the streamed
+// value, an earlier face's fresh reconstruction (followed here), or — when a
+// later face owns it — the previous step's slot value (stale read).
+__device__ float reconstruct(const RegionGeo& g, const FaceTable& ft, const StepView& v, int x,
+                             int y, int lz, int i, int owner) {
+    int f = owner;
+    for (int guard = 0; guard < 7; ++guard) {
+        const int cond = ft.cond[f];
+        if (cond == kNoSlip) return v.fin[g.idx(g.node(x, y, lz), opposite(i))];
+        if (cond == kInlet) return ft.inlet[f][i];
+        // outflow: step one cell inward along the face normal
+        const int a = face_axis(f), s = face_side(f);
+        if (a == 0) x -= s;
+        else if (a == 1) y -= s;
+        else lz -= s;
+        const int fn = owner_face(g, x, y, g.gz0 + lz, i);
+        if (fn == kNoOwner) return pull_rt(g, v, x, y, lz, i);
+        if (fn > f) return v.slot_prev[fn][g.slot_index(fn, x, y, lz, i)];
+        f = fn;
+    }
+    return 0.0f;  // unreachable: the owner strictly decreases along the chain
+}
+
+// Gathers f~* (post-stream, post-face-pass) of one node into fs.
+// Interior nodes take the direct path; others resolve each direction.
+template <bool WRITE_SLOTS>
+__device__ __forceinline__ void gather_node(const FluidParams& P, const StepView& v, float* const* slot_cur,
+                                            unsigned k, int x, int y, int lz, float (&fs)[27]) {
+    const RegionGeo& g = P.g;
+    const bool interior = x >= 1 && x <= g.nx - 2 && y >= 1 && y <= g.ny - 2 && lz >= 1 &&
+                          lz <= g.nzl - 2;
+    if (interior) {
+        static_for<0, 27>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            const unsigned ks = k - unsigned(cx(i) + g.nx * cy(i) + int(g.plane) * cz(i));
+            fs[i] = __ldg(&v.fin[g.idx(ks, i)]);
+        });
+        return;
+    }
+    const int gz = g.gz0 + lz;
+    static_for<0, 27>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        const int own = owner_face_c<i>(g, x, y, gz);
+        if (own == kNoOwner) {
+            fs[i] = pull_rt(g, v, x, y, lz, i);
+        } else {
+            const float val = reconstruct(g, P.faces, v, x, y, lz, i, own);
+            fs[i] = val;
+            if constexpr (WRITE_SLOTS) slot_cur[own][g.slot_index(own, x, y, lz, i)] = val;
+        }
+    });
+}
+
+struct Macro {
+    float rho, drho, ux, uy, uz;
+    bool bad;
+};
+
+// compute_moments (solver.cpp:89-137) on DDF-shifted populations.
+__device__ __forceinline__ Macro moments(const float (&fs)[27]) {
+    Macro mc;
+    float dr = 0.f, jx = 0.f, jy = 0.f, jz = 0.f;
+    static_for<0, 27>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        dr += fs[i];
+        if constexpr (cx(i) == 1) jx += fs[i];
+        if constexpr (cx(i) == -1) jx -= fs[i];
+        if constexpr (cy(i) == 1) jy += fs[i];
+        if constexpr (cy(i) == -1) jy -= fs[i];
+        if constexpr (cz(i) == 1) jz += fs[i];
+        if constexpr (cz(i) == -1) jz -= fs[i];
+    });
+    mc.drho = dr;
+    mc.rho = 1.0f + dr;
+    mc.bad = !(mc.rho > 0.0f) || !isfinite(mc.rho) || !isfinite(jx) || !isfinite(jy) ||
+             !isfinite(jz);
+    const float inv = 1.0f / mc.rho;
+    mc.ux = jx * inv;
+    mc.uy = jy * inv;
+    mc.uz = jz * inv;
+    return mc;
+}
+
+__device__ __forceinline__ void decode(const RegionGeo& g, unsigned k, int& x, int& y, int& lz) {
+    const unsigned q = g.div_nx.div(k);
+    x = int(k - q * unsigned(g.nx));
+    const unsigned q2 = g.div_ny.div(q);
+    y = int(q - q2 * unsigned(g.ny));
+    lz = int(q2);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Fused fluid step over local nodes [k0, k1).
+template <int KIND, int POLICY>
+__global__ void __launch_bounds__(256) fluid_kernel(const FluidParams P, unsigned k0, unsigned k1,
+                                                    int write_macro) {
+    DevCounters* ctr = P.ctr;
+    if (ctr->diverged) return;
+    const unsigned k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= k1) return;
+    const RegionGeo& g = P.g;
+    const int p = int(ctr->t & 1);
+    const StepView v = make_view(P, p);
+    int x, y, lz;
+    decode(g, k, x, y, lz);
+
+    float fs[27];
+    gather_node<true>(P, v, P.p.slot[p ^ 1], k, x, y, lz, fs);
+    const Macro mc = moments(fs);
+    if (mc.bad) {
+        // divergence: stop before IB/collision of this step (runner.cpp:154-161)
+        if (atomicExch(&ctr->diverged, 1u) == 0u) ctr->diverged_step = ctr->t;
+        if (write_macro) P.p.rho[k] = mc.rho;
+        return;
+    }
+    if (mc.ux * mc.ux + mc.uy * mc.uy + mc.uz * mc.uz >= 0.16f) atomicOr(&ctr->mach, 1u);
+    if (write_macro) {
+        P.p.rho[k] = mc.rho;
+        P.p.u[k] = mc.ux;
+        P.p.u[k + g.ns] = mc.uy;
+        P.p.u[k + 2u * g.ns] = mc.uz;
+    }
+    float gx = P.m.body[0], gy = P.m.body[1], gz = P.m.body[2];
+    if (P.p.tflag != nullptr && P.p.tflag[k >> 5]) {
+        float* gib = P.p.gib;
+        gx += gib[k];
+        gy += gib[k + g.ns];
+        gz += gib[k + 2u * g.ns];
+        gib[k] = 0.f;
+        gib[k + g.ns] = 0.f;
+        gib[k + 2u * g.ns] = 0.f;
+    }
+    const bool has_force = (gx != 0.f) || (gy != 0.f) || (gz != 0.f);
+    collide_node<KIND, POLICY>(fs, mc.rho, mc.drho, mc.ux, mc.uy, mc.uz, gx, gy, gz, has_force, P.m);
+
+    float* fout = P.p.f[p ^ 1];
+    static_for<0, 27>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        fout[g.idx(k, i)] = fs[i];
+    });
+    // crossing populations of the boundary planes -> neighbour halos
+    if (lz == 0) {
+        float* s = P.p.send_lo[p ^ 1];
+        if (s) {
+            const unsigned hp = unsigned(y) * g.nx + x;
+            static_for<1, 10>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                s[cross9(i, 2) * g.plane + hp] = fs[i];
+            });
+        }
+    }
+    if (lz == g.nzl - 1) {
+        float* s = P.p.send_hi[p ^ 1];
+        if (s) {
+            const unsigned hp = unsigned(y) * g.nx + x;
+            static_for<18, 27>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                s[cross9(i, 2) * g.plane + hp] = fs[i];
+            });
+        }
+    }
+}
+
+// Recompute rho*/u* of the current step from f(t) (used after divergence so
+// readback matches the reference's partially-written moments, solver.cpp:113).
+__global__ void macro_kernel(const FluidParams P, int parity) {
+    const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+    const RegionGeo& g = P.g;
+    if (k >= g.n) return;
+    const StepView v = make_view(P, parity);
+    int x, y, lz;
+    decode(g, k, x, y, lz);
+    float fs[27];
+    gather_node<false>(P, v, nullptr, k, x, y, lz, fs);
+    const Macro mc = moments(fs);
+    P.p.rho[k] = mc.rho;
+    if (!mc.bad) {
+        P.p.u[k] = mc.ux;
+        P.p.u[k + g.ns] = mc.uy;
+        P.p.u[k + 2u * g.ns] = mc.uz;
+    }
+}
+
+// IB band pre-pass: rho*, u* at the band nodes only.
+__global__ void ib_band_kernel(const FluidParams P, const unsigned* band) {
+    DevCounters* ctr = P.ctr;
+    if (ctr->diverged) return;
+    const unsigned count = *P.p.band_count;
+    const RegionGeo& g = P.g;
+    const int p = int(ctr->t & 1);
+    const StepView v = make_view(P, p);
+    for (unsigned j = blockIdx.x * blockDim.x + threadIdx.x; j < count; j += gridDim.x * blockDim.x) {
+        const unsigned k = band[j];
+        int x, y, lz;
+        decode(g, k, x, y, lz);
+        float fs[27];
+        gather_node<false>(P, v, nullptr, k, x, y, lz, fs);
+        const Macro mc = moments(fs);
+        P.p.rho[k] = mc.rho;
+        P.p.u[k] = mc.ux;
+        P.p.u[k + g.ns] = mc.uy;
+        P.p.u[k + 2u * g.ns] = mc.uz;
+    }
+}
+
+// (rho,u) of the two boundary planes into the macro halo of the neighbours.
+__global__ void macro_pack_kernel(const FluidParams P) {
+    if (P.ctr->diverged) return;
+    const RegionGeo& g = P.g;
+    const unsigned j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= g.plane) return;
+    if (P.p.msend_lo) {
+        const unsigned k = j;
+        P.p.msend_lo[j] = P.p.rho[k];
+        P.p.msend_lo[j + g.plane] = P.p.u[k];
+        P.p.msend_lo[j + 2u * g.plane] = P.p.u[k + g.ns];
+        P.p.msend_lo[j + 3u * g.plane] = P.p.u[k + 2u * g.ns];
+    }
+    if (P.p.msend_hi) {
+        const unsigned k = unsigned(g.nzl - 1) * g.plane + j;
+        P.p.msend_hi[j] = P.p.rho[k];
+        P.p.msend_hi[j + g.plane] = P.p.u[k];
+        P.p.msend_hi[j + 2u * g.plane] = P.p.u[k + g.ns];
+        P.p.msend_hi[j + 3u * g.plane] = P.p.u[k + 2u * g.ns];
+    }
+}
+
+__global__ void step_end_kernel(DevCounters* ctr) {
+    if (!ctr->diverged) ctr->t += 1;
+}
+
+// ---------------------------------------------------------------------------
+// Immersed boundary (ib.cpp:294-501).
+
+namespace {
+
+struct Support {
+    int base[3];
+    double w[3][2];
+    bool inside;
+};
+
+// kernel_support (ib.cpp:294-308), FP64, bit-exact flags.
+__device__ __forceinline__ Support kernel_support(const double p[3], int nx, int ny, int nz) {
+    Support ks;
+    ks.inside = true;
+    const int n[3] = {nx, ny, nz};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (p[a] < 0.0 || p[a] > double(n[a] - 1)) ks.inside = false;
+        int b = int(floor(p[a]));
+        b = max(0, min(b, n[a] - 2));
+        ks.base[a] = b;
+        const double t = __dsub_rn(p[a], double(b));
+        ks.w[a][0] = __dsub_rn(1.0, t);
+        ks.w[a][1] = t;
+    }
+    return ks;
+}
+
+// sample_active (ib.cpp:313-317)
+__device__ __forceinline__ bool sample_active(double pz, int NZ, int z0, int z1) {
+    int bz = int(floor(pz));
+    bz = max(0, min(bz, NZ - 2));
+    return bz + 1 >= z0 && bz < z1;
+}
+
+}  // namespace
+
+__global__ void ib_mark_kernel(const FluidParams P, IbSolidDev S, unsigned* stamp, unsigned* band) {
+    DevCounters* ctr = P.ctr;
+    if (ctr->diverged) return;
+    const RegionGeo& g = P.g;
+    const unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S.n) return;
+    const double pos[3] = {S.pos[3 * s], S.pos[3 * s + 1], S.pos[3 * s + 2]};
+    const Support ks = kernel_support(pos, g.nx, g.ny, g.NZ);
+    S.flagged[s] = ks.inside ? 0 : 1;
+    const int z0 = g.gz0, z1 = g.gz0 + g.nzl;
+    if (!ks.inside || !sample_active(pos[2], g.NZ, z0, z1)) return;
+    const unsigned mark = unsigned(ctr->t) + 1u;
+#pragma unroll
+    for (int oz = 0; oz < 2; ++oz) {
+        const int gz = ks.base[2] + oz;
+        if (gz < z0 || gz >= z1) continue;
+#pragma unroll
+        for (int oy = 0; oy < 2; ++oy)
+#pragma unroll
+            for (int ox = 0; ox < 2; ++ox) {
+                const unsigned k = g.node(ks.base[0] + ox, ks.base[1] + oy, gz - g.gz0);
+                if (atomicExch(&stamp[k], mark) != mark) band[atomicAdd(P.p.band_count, 1u)] = k;
+            }
+    }
+}
+
+// Interpolate (ib.cpp:321-343), penalty (ib.cpp:345-365) and scatter
+// (ib.cpp:369-454, atomic mode) per sample.  Scatter contributions are
+// combined in a per-CTA shared-memory hash table (samples are block/Morton
+// sorted, so a CTA touches few distinct nodes) and flushed with one global
+// atomic per (node, component).
+constexpr int kSpreadThreads = 128;
+constexpr int kHashSlots = 2048;  // >= 2 * 8 * kSpreadThreads (load <= 0.5), power of two
+
+__global__ void __launch_bounds__(kSpreadThreads) ib_spread_kernel(const FluidParams P, IbSolidDev S) {
+    __shared__ unsigned hkey[kHashSlots];
+    __shared__ float hval[3][kHashSlots];
+    DevCounters* ctr = P.ctr;
+    if (ctr->diverged) return;
+    const RegionGeo& g = P.g;
+    for (int j = threadIdx.x; j < kHashSlots; j += blockDim.x) {
+        hkey[j] = 0xffffffffu;
+        hval[0][j] = hval[1][j] = hval[2][j] = 0.f;
+    }
+    __syncthreads();
+
+    const unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
+    const int z0 = g.gz0, z1 = g.gz0 + g.nzl;
+    if (s < S.n) {
+        const double pos[3] = {S.pos[3 * s], S.pos[3 * s + 1], S.pos[3 * s + 2]};
+        const Support ks = kernel_support(pos, g.nx, g.ny, g.NZ);
+        const bool active = ks.inside && sample_active(pos[2], g.NZ, z0, z1);
+        double us[3] = {0.0, 0.0, 0.0};
+        double fg[3] = {0.0, 0.0, 0.0};
+        if (active) {
+            double rs = 0.0;
+            for (int oz = 0; oz < 2; ++oz)
+                for (int oy = 0; oy < 2; ++oy)
+                    for (int ox = 0; ox < 2; ++ox) {
+                        const double w = __dmul_rn(__dmul_rn(ks.w[0][ox], ks.w[1][oy]), ks.w[2][oz]);
+                        const int x = ks.base[0] + ox, y = ks.base[1] + oy, gz = ks.base[2] + oz;
+                        float r, ux, uy, uz;
+                        if (gz >= z0 && gz < z1) {
+                            const unsigned k = g.node(x, y, gz - g.gz0);
+                            r = P.p.rho[k];
+                            ux = P.p.u[k];
+                            uy = P.p.u[k + g.ns];
+                            uz = P.p.u[k + 2u * g.ns];
+                        } else {
+                            const float* h = gz < z0 ? P.p.mrecv_lo : P.p.mrecv_hi;
+                            const unsigned j = unsigned(y) * g.nx + x;
+                            r = h[j];
+                            ux = h[j + g.plane];
+                            uy = h[j + 2u * g.plane];
+                            uz = h[j + 3u * g.plane];
+                        }
+                        us[0] += w * ux;
+                        us[1] += w * uy;
+                        us[2] += w * uz;
+                        rs += w * r;
+                    }
+            for (int a = 0; a < 3; ++a) fg[a] = rs * (S.ub[3 * s + a] - us[a]);
+        }
+        for (int a = 0; a < 3; ++a) {
+            S.sampled[3 * s + a] = us[a];
+            S.force[3 * s + a] = fg[a];
+        }
+        if (active) {
+            for (int oz = 0; oz < 2; ++oz) {
+                const int gz = ks.base[2] + oz;
+                if (gz < z0 || gz >= z1) continue;
+                for (int oy = 0; oy < 2; ++oy)
+                    for (int ox = 0; ox < 2; ++ox) {
+                        const double w = __dmul_rn(__dmul_rn(ks.w[0][ox], ks.w[1][oy]), ks.w[2][oz]);
+                        const unsigned key = g.node(ks.base[0] + ox, ks.base[1] + oy, gz - g.gz0);
+                        unsigned h = (key * 2654435761u) & (kHashSlots - 1);
+                        for (;;) {
+                            const unsigned prev = atomicCAS(&hkey[h], 0xffffffffu, key);
+                            if (prev == 0xffffffffu || prev == key) break;
+                            h = (h + 1) & (kHashSlots - 1);
+                        }
+                        atomicAdd(&hval[0][h], float(w * fg[0]));
+                        atomicAdd(&hval[1][h], float(w * fg[1]));
+                        atomicAdd(&hval[2][h], float(w * fg[2]));
+                    }
+            }
+        }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < kHashSlots; j += blockDim.x) {
+        const unsigned key = hkey[j];
+        if (key == 0xffffffffu) continue;
+        atomicAdd(&P.p.gib[key], hval[0][j]);
+        atomicAdd(&P.p.gib[key + g.ns], hval[1][j]);
+        atomicAdd(&P.p.gib[key + 2u * g.ns], hval[2][j]);
+        P.p.tflag[key >> 5] = 1;
+    }
+}
+
+// Reaction totals (ib.cpp:491-501) over samples with z in [z0, z1):
+// per-block FP64 partials, then a fixed-order final sum -> deterministic.
+constexpr int kTotThreads = 256;
+__global__ void __launch_bounds__(kTotThreads) ib_totals_partial_kernel(const FluidParams P, IbSolidDev S,
+                                                                       const double* table,
+                                                                       double* partial) {
+    if (P.ctr->diverged) return;
+    __shared__ double sh[6][kTotThreads];
+    const double* motion_row = table + (P.ctr->t - P.ctr->chunk_t0) * kMotionRow;
+    const double c[3] = {motion_row[0], motion_row[1], motion_row[2]};
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    const double z0 = P.g.gz0, z1 = P.g.gz0 + P.g.nzl;
+    for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < S.n; s += gridDim.x * blockDim.x) {
+        const double pz = S.pos[3 * s + 2];
+        if (pz < z0 || pz >= z1) continue;
+        const double F[3] = {S.force[3 * s], S.force[3 * s + 1], S.force[3 * s + 2]};
+        const double r[3] = {S.pos[3 * s] - c[0], S.pos[3 * s + 1] - c[1], pz - c[2]};
+        acc[0] -= F[0];
+        acc[1] -= F[1];
+        acc[2] -= F[2];
+        acc[3] -= r[1] * F[2] - r[2] * F[1];
+        acc[4] -= r[2] * F[0] - r[0] * F[2];
+        acc[5] -= r[0] * F[1] - r[1] * F[0];
+    }
+    for (int a = 0; a < 6; ++a) sh[a][threadIdx.x] = acc[a];
+    __syncthreads();
+    for (int off = kTotThreads / 2; off > 0; off >>= 1) {
+        if (threadIdx.x < off)
+            for (int a = 0; a < 6; ++a) sh[a][threadIdx.x] += sh[a][threadIdx.x + off];
+        __syncthreads();
+    }
+    if (threadIdx.x < 6) partial[blockIdx.x * 6 + threadIdx.x] = sh[threadIdx.x][0];
+}
+
+__global__ void ib_totals_final_kernel(const DevCounters* ctr, const double* partial, int nblocks,
+                                       double* out_base, int stride) {
+    if (ctr->diverged) return;
+    const int a = threadIdx.x;
+    if (a >= 6) return;
+    double acc = 0.0;
+    for (int b = 0; b < nblocks; ++b) acc += partial[b * 6 + a];
+    out_base[(ctr->t - ctr->chunk_t0) * stride + a] = acc;
+}
+
+__device__ void motion_apply(const double* row, IbSolidDev S, unsigned s, int nx, int ny, int nz) {
+    const double* c = row;
+    const double* R = row + 3;
+    const double* v = row + 12;
+    const double* w = row + 15;
+    const double r0 = S.ref[3 * s], r1 = S.ref[3 * s + 1], r2 = S.ref[3 * s + 2];
+    // p = R r, then center + p: same operation order, no contraction
+    double p[3];
+    for (int a = 0; a < 3; ++a)
+        p[a] = __dadd_rn(__dadd_rn(__dmul_rn(R[3 * a], r0), __dmul_rn(R[3 * a + 1], r1)),
+                         __dmul_rn(R[3 * a + 2], r2));
+    double x[3];
+    for (int a = 0; a < 3; ++a) x[a] = __dadd_rn(c[a], p[a]);
+    const double d[3] = {__dsub_rn(x[0], c[0]), __dsub_rn(x[1], c[1]), __dsub_rn(x[2], c[2])};
+    // omega x d (core.hpp:27-29)
+    const double cr[3] = {__dsub_rn(__dmul_rn(w[1], d[2]), __dmul_rn(w[2], d[1])),
+                          __dsub_rn(__dmul_rn(w[2], d[0]), __dmul_rn(w[0], d[2])),
+                          __dsub_rn(__dmul_rn(w[0], d[1]), __dmul_rn(w[1], d[0]))};
+    for (int a = 0; a < 3; ++a) {
+        S.pos[3 * s + a] = x[a];
+        S.ub[3 * s + a] = __dadd_rn(v[a], cr[a]);
+    }
+    const Support ks = kernel_support(x, nx, ny, nz);
+    S.flagged[s] = ks.inside ? 0 : 1;
+}
+
+// update_rigid_motion (ib.cpp:456-489) to step t+1 with host-computed R, c.
+// motion table row (per step): c[3], R[9], v[3], w[3].
+__global__ void ib_motion_kernel(const DevCounters* ctr, IbSolidDev S, const double* table,
+                                 int nx, int ny, int nz) {
+    if (ctr->diverged) return;
+    const unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S.n) return;
+    const double* row = table + (ctr->t + 1 - ctr->chunk_t0) * kMotionRow;
+    motion_apply(row, S, s, nx, ny, nz);
+}
+
+__global__ void ib_motion_once_kernel(IbSolidDev S, const double* row, int nx, int ny, int nz) {
+    const unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S.n) return;
+    motion_apply(row, S, s, nx, ny, nz);
+}
+
+// ---------------------------------------------------------------------------
+// init_fields (runner.cpp:60-107): equilibrium f (both the f(0) buffer and
+// the face slots, which stand in for the initial f_star), rho, u.
+
+__device__ __forceinline__ void init_state(const InitParams& ip, int x, int y, int gz, double& rho,
+                                           double u[3]) {
+    if (ip.kind == 0) {
+        rho = ip.rho0;
+        u[0] = ip.u0[0];
+        u[1] = ip.u0[1];
+        u[2] = ip.u0[2];
+        return;
+    }
+    const double kx = 2.0 * M_PI / ip.NX, ky = 2.0 * M_PI / ip.NY;
+    const double u0 = ip.tg_u;
+    u[0] = -u0 * cos(kx * x) * sin(ky * y);
+    u[1] = u0 * sin(kx * x) * cos(ky * y);
+    u[2] = 0.0;
+    const double pr = -0.25 * u0 * u0 * (cos(2.0 * kx * x) + cos(2.0 * ky * y));
+    rho = ip.rho0 + 3.0 * pr;
+}
+
+__device__ __forceinline__ double feq_shifted(int i, double rho, const double u[3]) {
+    const double w = weight_d(i);
+    const double usq = 1.5 * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+    const double cu = cx(i) * u[0] + cy(i) * u[1] + cz(i) * u[2];
+    const double feq = w * rho * (1.0 + 3.0 * cu + 4.5 * cu * cu - usq);
+    return feq - w;
+}
+
+__global__ void init_kernel(const FluidParams P, InitParams ip) {
+    const RegionGeo& g = P.g;
+    const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= g.n) return;
+    int x, y, lz;
+    decode(g, k, x, y, lz);
+    const int gz = g.gz0 + lz;
+    double rho, u[3];
+    init_state(ip, x, y, gz, rho, u);
+    float* f0 = P.p.f[0];
+    float* f1 = P.p.f[1];
+    for (int i = 0; i < 27; ++i) {
+        const float v = float(feq_shifted(i, rho, u));
+        f0[g.idx(k, i)] = v;
+        f1[g.idx(k, i)] = v;
+    }
+    P.p.rho[k] = float(rho);
+    P.p.u[k] = float(u[0]);
+    P.p.u[k + g.ns] = float(u[1]);
+    P.p.u[k + 2u * g.ns] = float(u[2]);
+    // face slots (initial f_star = feq, runner.cpp:94) for both parities
+    for (int f = 0; f < 6; ++f) {
+        float* s0 = P.p.slot[0][f];
+        if (!s0) continue;
+        const int a = face_axis(f), sd = face_side(f);
+        const int coord = a == 0 ? x : (a == 1 ? y : gz);
+        const int plane = sd < 0 ? 0 : g.extent(a) - 1;
+        if (coord != plane) continue;
+        for (int i = 0; i < 27; ++i) {
+            if (cc(i, a) != -sd) continue;
+            const float v = float(feq_shifted(i, rho, u));
+            s0[g.slot_index(f, x, y, lz, i)] = v;
+            P.p.slot[1][f][g.slot_index(f, x, y, lz, i)] = v;
+        }
+    }
+    // halos for step 0 (send[0] aliases the neighbour's recv[0] in-process)
+    const unsigned hp = unsigned(y) * g.nx + x;
+    if (lz == 0 && P.p.send_lo[0])
+        for (int i = 1; i <= 9; ++i) P.p.send_lo[0][cross9(i, 2) * g.plane + hp] = f0[g.idx(k, i)];
+    if (lz == g.nzl - 1 && P.p.send_hi[0])
+        for (int i = 18; i <= 26; ++i) P.p.send_hi[0][cross9(i, 2) * g.plane + hp] = f0[g.idx(k, i)];
+}
+
+// Readback: canonical AoS FP64 for local planes [lz0, lz1).
+__global__ void read_f_kernel(const FluidParams P, int parity, unsigned k0, unsigned k1, double* out) {
+    const unsigned k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= k1) return;
+    const float* f = P.p.f[parity];
+    const RegionGeo& g = P.g;
+    for (int i = 0; i < 27; ++i)
+        out[size_t(k - k0) * 27 + i] = double(f[g.idx(k, i)]) + weight_d(i);
+}
+
+__global__ void read_macro_kernel(const FluidParams P, unsigned k0, unsigned k1, double* rho,
+                                  double* u) {
+    const unsigned k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= k1) return;
+    const RegionGeo& g = P.g;
+    if (rho) rho[k - k0] = double(P.p.rho[k]);
+    if (u)
+        for (int a = 0; a < 3; ++a) u[size_t(k - k0) * 3 + a] = double(P.p.u[k + a * g.ns]);
+}
+
+// Cell flags: owner face per (node, direction).
+__global__ void cell_flags_kernel(const FluidParams P, unsigned k0, unsigned k1, unsigned char* out) {
+    const unsigned k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= k1) return;
+    const RegionGeo& g = P.g;
+    int x, y, lz;
+    decode(g, k, x, y, lz);
+    const int gz = g.gz0 + lz;
+    static_for<0, 27>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        out[size_t(k - k0) * 27 + i] = (unsigned char)owner_face_c<i>(g, x, y, gz);
+    });
+}
+
+// Layout change (set_layout, runner.cpp:252-258): pure permutation between
+// two Eq. 9 layouts of the same node count.
+__global__ void relayout_kernel(const float* src, float* dst, RegionGeo gs, RegionGeo gd) {
+    const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= gs.n) return;
+    for (int i = 0; i < 27; ++i) dst[gd.idx(k, i)] = src[gs.idx(k, i)];
+}
+
+// Unit-level collide() on a batch (fp32): omega = f_out - f*.
+template <int KIND, int POLICY>
+__global__ void collide_batch_kernel(ModelConst m, unsigned n, const double* f, const double* rho,
+                                     const double* u, double* omega) {
+    const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    float fs[27], f0[27];
+    for (int i = 0; i < 27; ++i) {
+        fs[i] = float(f[size_t(k) * 27 + i] - weight_d(i));
+        f0[i] = fs[i];
+    }
+    const double r = rho[k];
+    collide_node<KIND, POLICY>(fs, float(r), float(r - 1.0), float(u[3 * k]), float(u[3 * k + 1]),
+                               float(u[3 * k + 2]), 0.f, 0.f, 0.f, false, m);
+    for (int i = 0; i < 27; ++i) omega[size_t(k) * 27 + i] = double(fs[i]) - double(f0[i]);
+}
+
+// ---------------------------------------------------------------------------
+// Host launch wrappers.
+
+namespace {
+inline unsigned blocks_for(unsigned long long n, unsigned t) { return unsigned((n + t - 1) / t); }
+
+template <int KIND, int POLICY>
+void launch_fluid_t(const FluidParams& P, unsigned k0, unsigned k1, int write_macro, cudaStream_t st) {
+    if (k1 <= k0) return;
+    fluid_kernel<KIND, POLICY><<<blocks_for(k1 - k0, 256), 256, 0, st>>>(P, k0, k1, write_macro);
+}
+}  // namespace
+
+void launch_fluid(const FluidParams& P, unsigned k0, unsigned k1, int write_macro, cudaStream_t st) {
+    const int kind = P.m.kind, pol = P.m.policy;
+    if (kind == kBGK) launch_fluid_t<kBGK, kPolicyConstant>(P, k0, k1, write_macro, st);
+    else if (kind == kRawMRT && pol == kPolicyConstant) launch_fluid_t<kRawMRT, kPolicyConstant>(P, k0, k1, write_macro, st);
+    else if (kind == kRawMRT) launch_fluid_t<kRawMRT, kPolicyRelax>(P, k0, k1, write_macro, st);
+    else if (pol == kPolicyConstant) launch_fluid_t<kCentralMRT, kPolicyConstant>(P, k0, k1, write_macro, st);
+    else launch_fluid_t<kCentralMRT, kPolicyRelax>(P, k0, k1, write_macro, st);
+}
+
+void launch_macro(const FluidParams& P, int parity, cudaStream_t st) {
+    macro_kernel<<<blocks_for(P.g.n, 256), 256, 0, st>>>(P, parity);
+}
+
+void launch_ib_mark(const FluidParams& P, const IbSolidDev& S, unsigned* stamp, unsigned* band, cudaStream_t st) {
+    if (S.n == 0) return;
+    ib_mark_kernel<<<blocks_for(S.n, 256), 256, 0, st>>>(P, S, stamp, band);
+}
+
+void launch_ib_band(const FluidParams& P, const unsigned* band, int sm_count, cudaStream_t st) {
+    ib_band_kernel<<<sm_count * 4, 128, 0, st>>>(P, band);
+}
+
+void launch_macro_pack(const FluidParams& P, cudaStream_t st) {
+    macro_pack_kernel<<<blocks_for(P.g.plane, 256), 256, 0, st>>>(P);
+}
+
+void launch_ib_spread(const FluidParams& P, const IbSolidDev& S, cudaStream_t st) {
+    if (S.n == 0) return;
+    ib_spread_kernel<<<blocks_for(S.n, kSpreadThreads), kSpreadThreads, 0, st>>>(P, S);
+}
+
+int totals_blocks(size_t n) {
+    size_t b = (n + kTotThreads - 1) / kTotThreads;
+    return int(b < 1 ? 1 : (b > 256 ? 256 : b));
+}
+
+void launch_ib_totals(const FluidParams& P, const IbSolidDev& S, const double* table, double* partial,
+                      double* out_base, int stride, cudaStream_t st) {
+    const int nb = totals_blocks(S.n);
+    ib_totals_partial_kernel<<<nb, kTotThreads, 0, st>>>(P, S, table, partial);
+    ib_totals_final_kernel<<<1, 32, 0, st>>>(P.ctr, partial, nb, out_base, stride);
+}
+
+void launch_ib_motion(const DevCounters* ctr, const IbSolidDev& S, const double* table, int nx, int ny,
+                      int nz, cudaStream_t st) {
+    if (S.n == 0) return;
+    ib_motion_kernel<<<blocks_for(S.n, 256), 256, 0, st>>>(ctr, S, table, nx, ny, nz);
+}
+
+void launch_ib_motion_once(const IbSolidDev& S, const double* row, int nx, int ny, int nz, cudaStream_t st) {
+    if (S.n == 0) return;
+    ib_motion_once_kernel<<<blocks_for(S.n, 256), 256, 0, st>>>(S, row, nx, ny, nz);
+}
+
+void launch_step_end(DevCounters* ctr, cudaStream_t st) { step_end_kernel<<<1, 1, 0, st>>>(ctr); }
+
+void launch_init(const FluidParams& P, const InitParams& ip, cudaStream_t st) {
+    init_kernel<<<blocks_for(P.g.n, 256), 256, 0, st>>>(P, ip);
+}
+
+void launch_read_f(const FluidParams& P, int parity, unsigned k0, unsigned k1, double* out, cudaStream_t st) {
+    if (k1 > k0) read_f_kernel<<<blocks_for(k1 - k0, 256), 256, 0, st>>>(P, parity, k0, k1, out);
+}
+
+void launch_read_macro(const FluidParams& P, unsigned k0, unsigned k1, double* rho, double* u, cudaStream_t st) {
+    if (k1 > k0) read_macro_kernel<<<blocks_for(k1 - k0, 256), 256, 0, st>>>(P, k0, k1, rho, u);
+}
+
+void launch_cell_flags(const FluidParams& P, unsigned k0, unsigned k1, unsigned char* out, cudaStream_t st) {
+    if (k1 > k0) cell_flags_kernel<<<blocks_for(k1 - k0, 256), 256, 0, st>>>(P, k0, k1, out);
+}
+
+void launch_relayout(const float* src, float* dst, const RegionGeo& gs, const RegionGeo& gd, cudaStream_t st) {
+    relayout_kernel<<<blocks_for(gs.n, 256), 256, 0, st>>>(src, dst, gs, gd);
+}
+
+void launch_collide_batch(const ModelConst& m, unsigned n, const double* f, const double* rho,
+                          const double* u, double* omega, cudaStream_t st) {
+    const unsigned b = blocks_for(n, 128);
+    if (m.kind == kBGK) collide_batch_kernel<kBGK, kPolicyConstant><<<b, 128, 0, st>>>(m, n, f, rho, u, omega);
+    else if (m.kind == kRawMRT && m.policy == kPolicyConstant) collide_batch_kernel<kRawMRT, kPolicyConstant><<<b, 128, 0, st>>>(m, n, f, rho, u, omega);
+    else if (m.kind == kRawMRT) collide_batch_kernel<kRawMRT, kPolicyRelax><<<b, 128, 0, st>>>(m, n, f, rho, u, omega);
+    else if (m.policy == kPolicyConstant) collide_batch_kernel<kCentralMRT, kPolicyConstant><<<b, 128, 0, st>>>(m, n, f, rho, u, omega);
+    else collide_batch_kernel<kCentralMRT, kPolicyRelax><<<b, 128, 0, st>>>(m, n, f, rho, u, omega);
+}
+
+}  // namespace lbmg

@@ -1,0 +1,791 @@
+// Runner orchestration on the device (runner.cpp:22-319 of the reference,
+// re-designed: one fused kernel per region per step, device-side step
+// counter, CUDA-graph replay, in-process or NCCL-driven halo exchange).
+#include "runner.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+namespace lbmg {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        throw OomError(std::string(what) + ": " + cudaGetErrorString(e));
+    }
+    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(x) cuda_check((x), #x)
+
+namespace {
+
+unsigned round_up(unsigned n, unsigned a) { return (n + a - 1) / a * a; }
+
+size_t next_pow2(size_t v) {
+    size_t p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+int log2i(size_t v) {
+    int s = 0;
+    while ((size_t(1) << s) < v) ++s;
+    return s;
+}
+
+// equilibrium, collision.cpp:148-157 (FP64, reference operation order).
+double feq(int i, double rho, const double u[3]) {
+    const double usq = 1.5 * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+    const double cu = cx(i) * u[0] + cy(i) * u[1] + cz(i) * u[2];
+    return weight_d(i) * rho * (1.0 + 3.0 * cu + 4.5 * cu * cu - usq);
+}
+
+}  // namespace
+
+FluidParams Runner::Region::params() const { return FluidParams{geo, {}, {}, ptr, nullptr}; }
+
+void* Runner::dalloc(size_t bytes, bool zero) {
+    if (bytes == 0) bytes = 16;
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw OomError("device allocation of " + std::to_string(bytes) + " bytes failed: " +
+                       cudaGetErrorString(e));
+    }
+    if (zero) CK(cudaMemset(p, 0, bytes));
+    allocs_.push_back(p);
+    return p;
+}
+
+void Runner::dfree(void* p) {
+    if (!p) return;
+    auto it = std::find(allocs_.begin(), allocs_.end(), p);
+    if (it != allocs_.end()) allocs_.erase(it);
+    cudaFree(p);
+}
+
+Runner::Runner(const lbmg_scene& scene, int regions, int device, int world, int rank) {
+    scene_ = scene;
+    scene_.cfg.solids = scene_.solid_cfgs.empty() ? nullptr : scene_.solid_cfgs.data();
+    scene_.cfg.n_solids = int(scene_.solid_cfgs.size());
+    const lbmg_scene_config& c = scene_.cfg;
+    validate_config(c);
+    nx_ = c.nx;
+    ny_ = c.ny;
+    nz_ = c.nz;
+    if (int64_t(nx_) * ny_ * nz_ >= (int64_t(1) << 31) && world == 0 && regions == 1)
+        throw ConfigError("grid: a single slab must hold fewer than 2^31 nodes; use more regions");
+    rank_mode_ = world > 0;
+    m_global_ = rank_mode_ ? world : regions;
+    rank_ = rank_mode_ ? rank : 0;
+    if (m_global_ < 1 || m_global_ > nz_)
+        throw ConfigError("decomp: region count must satisfy 1 <= m <= nz (got m=" +
+                          std::to_string(m_global_) + ", nz=" + std::to_string(nz_) + ")");
+    if (rank_mode_ && (rank < 0 || rank >= world)) throw ConfigError("rank out of range");
+    const auto slabs = split_domain(nz_, m_global_);
+    // runner.cpp:32-37: z outflow reads one plane into the slab interior
+    for (int f = 4; f < 6; ++f)
+        if (c.faces[f].condition == LBMG_OUTFLOW && m_global_ > 1)
+            for (const auto& s : slabs)
+                if (s[1] - s[0] < 2) throw ConfigError("decomp: z outflow needs slabs at least 2 planes thick");
+
+    const auto rates = make_rates(c);
+    const auto& T = model_tables();
+    model_.kind = c.kind;
+    // only cm-mrt carries the rate policy (scene.cpp:33-37: raw_mrt/bgk are Constant)
+    model_.policy = c.kind == LBMG_CENTRAL_MRT ? c.policy : LBMG_POLICY_CONSTANT;
+    model_.omega = float(1.0 / (3.0 * c.viscosity + 0.5));
+    model_.eps0 = float(c.policy_eps0);
+    for (int mu = 0; mu < 27; ++mu) model_.rate[mu] = float(rates[T.mu_to_row[mu]]);
+    for (int a = 0; a < 3; ++a) model_.body[a] = float(c.body_force[a]);
+    for (int f = 0; f < 6; ++f) {
+        faces_.cond[f] = c.faces[f].condition;
+        for (int i = 0; i < 27; ++i)
+            faces_.inlet[f][i] = float(feq(i, 1.0, c.faces[f].velocity) - weight_d(i));
+    }
+    has_solids_ = !scene_.solids.empty();
+    for (const auto& s : scene_.solids) {
+        moving_.push_back(s.moving ? 1 : 0);
+        total_samples_ += s.samples.size();
+    }
+    ell_ = c.block_edge;
+    layout_.alpha_req = c.alpha;
+
+    device_ = device;
+    CK(cudaSetDevice(device));
+    CK(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+
+    const int first = rank_mode_ ? rank_ : 0;
+    const int count = rank_mode_ ? 1 : m_global_;
+    regions_.resize(count);
+    for (int r = 0; r < count; ++r) {
+        regions_[r].z0 = slabs[first + r][0];
+        regions_[r].z1 = slabs[first + r][1];
+        const int g = first + r;
+        regions_[r].has_lo = g > 0 || c.faces[4].condition == LBMG_PERIODIC;
+        regions_[r].has_hi = g + 1 < m_global_ || c.faces[4].condition == LBMG_PERIODIC;
+    }
+    build_regions(device);
+    link_halos();
+    ctr_ = static_cast<DevCounters*>(dalloc(sizeof(DevCounters)));
+    if (has_solids_) {
+        const size_t ns = scene_.solids.size();
+        motion_tab_ = static_cast<double*>(dalloc(sizeof(double) * (cap_ + 2) * ns * kMotionRow));
+        totals_dev_ = static_cast<double*>(dalloc(sizeof(double) * cap_ * regions_.size() * ns * 6));
+    }
+    upload_solids();
+    init_fields();
+    if (rank_mode_ && has_solids_) fill_motion_table(0, cap_ + 1);
+    CK(cudaStreamSynchronize(stream_));
+}
+
+Runner::~Runner() {
+    invalidate_graphs();
+    for (void* p : allocs_) cudaFree(p);
+    allocs_.clear();
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Runner::invalidate_graphs() {
+    for (auto& g : graph_)
+        if (g) {
+            cudaGraphExecDestroy(g);
+            g = nullptr;
+        }
+}
+
+void Runner::compute_geo(Region& r) const {
+    RegionGeo& g = r.geo;
+    g.nx = nx_;
+    g.ny = ny_;
+    g.nzl = r.z1 - r.z0;
+    g.NZ = nz_;
+    g.gz0 = r.z0;
+    for (int a = 0; a < 3; ++a) g.per[a] = scene_.cfg.faces[2 * a].condition == LBMG_PERIODIC;
+    g.plane = unsigned(nx_) * unsigned(ny_);
+    g.n = g.plane * unsigned(g.nzl);
+    g.ns = round_up(g.n, 32);
+    const size_t a = next_pow2(std::max<size_t>(layout_.alpha_req, 32));
+    if (a >= g.n) {  // SoA: one group of n_pad nodes
+        g.la = 31;
+        g.amask = 0x7fffffffu;
+        g.n_pad = round_up(g.n, 32);
+        g.A = g.n_pad;
+    } else {
+        g.la = log2i(a);
+        g.amask = unsigned(a - 1);
+        g.n_pad = round_up(g.n, unsigned(a));
+        g.A = unsigned(a);
+    }
+    g.div_nx = FastDiv(unsigned(nx_));
+    g.div_ny = FastDiv(unsigned(ny_));
+}
+
+void Runner::alloc_f(Region& r) {
+    for (int p = 0; p < 2; ++p) {
+        r.f[p] = static_cast<float*>(dalloc(sizeof(float) * 27ull * r.geo.n_pad, false));
+        r.ptr.f[p] = r.f[p];
+    }
+}
+
+void Runner::build_regions(int) {
+    for (auto& r : regions_) {
+        compute_geo(r);
+        RegionGeo& g = r.geo;
+        alloc_f(r);
+        r.ptr.rho = static_cast<float*>(dalloc(sizeof(float) * g.ns));
+        r.ptr.u = static_cast<float*>(dalloc(sizeof(float) * 3ull * g.ns));
+        if (has_solids_) {
+            r.ptr.gib = static_cast<float*>(dalloc(sizeof(float) * 3ull * g.ns));
+            r.ptr.tflag = static_cast<unsigned char*>(dalloc(g.ns / 32 + 1));
+            r.stamp = static_cast<unsigned*>(dalloc(sizeof(unsigned) * g.ns));
+            const size_t cap = std::max<size_t>(1, std::min<size_t>(g.n, 8 * total_samples_));
+            r.band = static_cast<unsigned*>(dalloc(sizeof(unsigned) * cap));
+            r.ptr.band_count = static_cast<unsigned*>(dalloc(sizeof(unsigned)));
+            r.partial = static_cast<double*>(dalloc(sizeof(double) * 6 * 256));
+        }
+        for (int f = 0; f < 6; ++f) {
+            const int a = face_axis(f);
+            bool present = scene_.cfg.faces[f].condition != LBMG_PERIODIC;
+            if (a == 2) present = present && ((f == 4 && r.z0 == 0) || (f == 5 && r.z1 == nz_));
+            for (int p = 0; p < 2; ++p)
+                r.ptr.slot[p][f] =
+                    present ? static_cast<float*>(dalloc(sizeof(float) * 9ull * g.slot_plane(f))) : nullptr;
+        }
+        const size_t hb = sizeof(float) * 9ull * g.plane;
+        for (int p = 0; p < 2; ++p) {
+            if (r.has_lo) r.recv_lo[p] = static_cast<float*>(dalloc(hb));
+            if (r.has_hi) r.recv_hi[p] = static_cast<float*>(dalloc(hb));
+            r.ptr.recv_lo[p] = r.recv_lo[p];
+            r.ptr.recv_hi[p] = r.recv_hi[p];
+            if (rank_mode_) {
+                if (r.has_lo) r.own_send_lo[p] = static_cast<float*>(dalloc(hb));
+                if (r.has_hi) r.own_send_hi[p] = static_cast<float*>(dalloc(hb));
+            }
+        }
+        if (has_solids_) {
+            const size_t mb = sizeof(float) * 4ull * g.plane;
+            if (r.has_lo) r.mrecv_lo = static_cast<float*>(dalloc(mb));
+            if (r.has_hi) r.mrecv_hi = static_cast<float*>(dalloc(mb));
+            if (rank_mode_) {
+                if (r.has_lo) r.own_msend_lo = static_cast<float*>(dalloc(mb));
+                if (r.has_hi) r.own_msend_hi = static_cast<float*>(dalloc(mb));
+            }
+            r.ptr.mrecv_lo = r.mrecv_lo;
+            r.ptr.mrecv_hi = r.mrecv_hi;
+        }
+    }
+}
+
+// In-process: a region's outgoing halo IS the neighbour's incoming buffer
+// (region r's send_hi == region r+1's recv_lo; periodic z wraps, a single
+// periodic slab feeds itself).  Rank mode: own send buffers, moved by NCCL.
+void Runner::link_halos() {
+    const int m = int(regions_.size());
+    for (int r = 0; r < m; ++r) {
+        Region& R = regions_[r];
+        if (rank_mode_) {
+            for (int p = 0; p < 2; ++p) {
+                R.ptr.send_lo[p] = R.own_send_lo[p];
+                R.ptr.send_hi[p] = R.own_send_hi[p];
+            }
+            R.ptr.msend_lo = R.own_msend_lo;
+            R.ptr.msend_hi = R.own_msend_hi;
+            continue;
+        }
+        const int lo = r > 0 ? r - 1 : m - 1;
+        const int hi = r + 1 < m ? r + 1 : 0;
+        for (int p = 0; p < 2; ++p) {
+            R.ptr.send_lo[p] = R.has_lo ? regions_[lo].recv_hi[p] : nullptr;
+            R.ptr.send_hi[p] = R.has_hi ? regions_[hi].recv_lo[p] : nullptr;
+        }
+        R.ptr.msend_lo = R.has_lo && has_solids_ ? regions_[lo].mrecv_hi : nullptr;
+        R.ptr.msend_hi = R.has_hi && has_solids_ ? regions_[hi].mrecv_lo : nullptr;
+    }
+}
+
+void Runner::upload_solids() {
+    for (auto& r : regions_) {
+        r.solids.clear();
+        for (const auto& s : scene_.solids) {
+            IbSolidDev d{};
+            const size_t n = s.samples.size();
+            d.n = unsigned(n);
+            d.pos = static_cast<double*>(dalloc(sizeof(double) * 3 * n));
+            d.ref = static_cast<double*>(dalloc(sizeof(double) * 3 * n));
+            d.ub = static_cast<double*>(dalloc(sizeof(double) * 3 * n));
+            d.force = static_cast<double*>(dalloc(sizeof(double) * 3 * n));
+            d.sampled = static_cast<double*>(dalloc(sizeof(double) * 3 * n));
+            d.source = static_cast<unsigned*>(dalloc(sizeof(unsigned) * n));
+            d.flagged = static_cast<unsigned char*>(dalloc(n));
+            std::vector<double> pos(3 * n), ref(3 * n);
+            for (size_t k = 0; k < n; ++k)
+                for (int a = 0; a < 3; ++a) {
+                    pos[3 * k + a] = s.samples.positions[k][a];
+                    ref[3 * k + a] = s.samples.reference_positions[k][a];
+                }
+            if (n) {
+                CK(cudaMemcpy(d.pos, pos.data(), sizeof(double) * 3 * n, cudaMemcpyHostToDevice));
+                CK(cudaMemcpy(d.ref, ref.data(), sizeof(double) * 3 * n, cudaMemcpyHostToDevice));
+                CK(cudaMemcpy(d.source, s.samples.source_id.data(), sizeof(unsigned) * n,
+                              cudaMemcpyHostToDevice));
+            }
+            r.solids.push_back(d);
+        }
+    }
+}
+
+// Rigid motion row at step t (ib.cpp:456-475): centre(t) and Rodrigues R(t)
+// computed on the host with the reference's expressions (glibc cos/sin).
+void Runner::motion_row(int solid, long t, double* row) const {
+    const SolidInstance& s = scene_.solids[solid];
+    const double td = double(t);
+    const V3 center = s.center + s.linear_velocity * td;
+    const double wn = std::sqrt(dot(s.angular_velocity, s.angular_velocity));
+    double R[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+    if (wn > 0.0) {
+        const V3 ax = s.angular_velocity * (1.0 / wn);
+        const double th = wn * td, ct = std::cos(th), st = std::sin(th), vt = 1.0 - ct;
+        R[0][0] = ct + ax.x * ax.x * vt;
+        R[0][1] = ax.x * ax.y * vt - ax.z * st;
+        R[0][2] = ax.x * ax.z * vt + ax.y * st;
+        R[1][0] = ax.y * ax.x * vt + ax.z * st;
+        R[1][1] = ct + ax.y * ax.y * vt;
+        R[1][2] = ax.y * ax.z * vt - ax.x * st;
+        R[2][0] = ax.z * ax.x * vt - ax.y * st;
+        R[2][1] = ax.z * ax.y * vt + ax.x * st;
+        R[2][2] = ct + ax.z * ax.z * vt;
+    }
+    row[0] = center.x;
+    row[1] = center.y;
+    row[2] = center.z;
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) row[3 + 3 * a + b] = R[a][b];
+    for (int a = 0; a < 3; ++a) {
+        row[12 + a] = s.linear_velocity[a];
+        row[15 + a] = s.angular_velocity[a];
+    }
+}
+
+void Runner::fill_motion_table(long t0, long rows) {
+    const size_t ns = scene_.solids.size();
+    std::vector<double> tab(size_t(rows) * ns * kMotionRow);
+    // layout: [step][solid][row]; kernels index (t - t0) * kMotionRow within a
+    // per-solid view, so store solid-major: [solid][step][row]
+    for (size_t s = 0; s < ns; ++s)
+        for (long j = 0; j < rows; ++j) motion_row(int(s), t0 + j, &tab[(s * (cap_ + 2) + j) * kMotionRow]);
+    for (size_t s = 0; s < ns; ++s)
+        CK(cudaMemcpyAsync(motion_tab_ + s * (cap_ + 2) * kMotionRow, &tab[s * (cap_ + 2) * kMotionRow],
+                           sizeof(double) * rows * kMotionRow, cudaMemcpyHostToDevice, stream()));
+    CK(cudaStreamSynchronize(stream()));
+}
+
+void Runner::init_fields() {
+    const lbmg_scene_config& c = scene_.cfg;
+    InitParams ip{};
+    ip.kind = c.init;
+    ip.rho0 = c.init_density;
+    for (int a = 0; a < 3; ++a) ip.u0[a] = c.init_velocity[a];
+    ip.tg_u = c.tg_u_max;
+    ip.NX = nx_;
+    ip.NY = ny_;
+    for (auto& r : regions_) {
+        FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+        launch_init(P, ip, stream());
+    }
+    CK(cudaGetLastError());
+    // update_rigid_motion(t=0) for every solid (runner.cpp:104-106)
+    if (has_solids_) {
+        double* row = static_cast<double*>(dalloc(sizeof(double) * kMotionRow));
+        for (size_t s = 0; s < scene_.solids.size(); ++s) {
+            double h[kMotionRow];
+            motion_row(int(s), 0, h);
+            CK(cudaMemcpy(row, h, sizeof h, cudaMemcpyHostToDevice));
+            for (auto& r : regions_) launch_ib_motion_once(r.solids[s], row, nx_, ny_, nz_, stream());
+            CK(cudaStreamSynchronize(stream()));
+        }
+        dfree(row);
+    }
+    CK(cudaStreamSynchronize(stream()));
+}
+
+void Runner::enqueue_ib_pre() {
+    cudaStream_t st = stream();
+    for (auto& r : regions_) CK(cudaMemsetAsync(r.ptr.band_count, 0, sizeof(unsigned), st));
+    for (auto& r : regions_) {
+        FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+        for (auto& s : r.solids) launch_ib_mark(P, s, r.stamp, r.band, st);
+    }
+    for (auto& r : regions_) {
+        FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+        launch_ib_band(P, r.band, sm_count_, st);
+    }
+    if (m_global_ > 1)
+        for (auto& r : regions_) {
+            FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+            launch_macro_pack(P, st);
+        }
+}
+
+void Runner::enqueue_ib_mid() {
+    cudaStream_t st = stream();
+    const int ns = int(scene_.solids.size());
+    const int m = int(regions_.size());
+    for (auto& r : regions_) {
+        FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+        for (auto& s : r.solids) launch_ib_spread(P, s, st);
+    }
+    for (int ri = 0; ri < m; ++ri) {
+        Region& r = regions_[ri];
+        FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+        for (int s = 0; s < ns; ++s)
+            launch_ib_totals(P, r.solids[s], motion_tab_ + size_t(s) * (cap_ + 2) * kMotionRow, r.partial,
+                             totals_dev_ + size_t(ri * ns + s) * 6, m * ns * 6, st);
+    }
+    for (auto& r : regions_)
+        for (int s = 0; s < ns; ++s)
+            if (moving_[s])
+                launch_ib_motion(ctr_, r.solids[s], motion_tab_ + size_t(s) * (cap_ + 2) * kMotionRow, nx_, ny_,
+                                 nz_, st);
+}
+
+// part: 0 all planes, 1 boundary planes only, 2 interior planes only.
+void Runner::enqueue_fluid(bool write_macro, int part) {
+    cudaStream_t st = stream();
+    for (auto& r : regions_) {
+        FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+        const unsigned plane = r.geo.plane, n = r.geo.n;
+        if (part == 0) {
+            launch_fluid(P, 0, n, write_macro, st);
+        } else if (part == 1) {
+            launch_fluid(P, 0, plane, write_macro, st);
+            if (r.geo.nzl > 1) launch_fluid(P, n - plane, n, write_macro, st);
+        } else if (r.geo.nzl > 2) {
+            launch_fluid(P, plane, n - plane, write_macro, st);
+        }
+    }
+}
+
+void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
+    cudaStream_t st = stream();
+    if (ev) CK(cudaEventRecord((*ev)[0], st));
+    if (has_solids_) {
+        enqueue_ib_pre();
+        enqueue_ib_mid();
+    }
+    if (ev) CK(cudaEventRecord((*ev)[1], st));
+    enqueue_fluid(write_macro, 0);
+    if (has_solids_)
+        for (auto& r : regions_) CK(cudaMemsetAsync(r.ptr.tflag, 0, r.geo.ns / 32 + 1, st));
+    launch_step_end(ctr_, st);
+    if (ev) CK(cudaEventRecord((*ev)[2], st));
+}
+
+Status Runner::advance(long steps, std::vector<Timing>* timings) {
+    if (!status_.ok || steps <= 0) return status_;
+    cudaStream_t st = stream();
+    CK(cudaSetDevice(device_));
+    long done = 0;
+    while (done < steps) {
+        const long chunk = std::min(cap_, steps - done);
+        const long t0 = t_;
+        if (has_solids_) fill_motion_table(t0, chunk + 1);
+        long long t0d = t0;
+        CK(cudaMemcpyAsync(&ctr_->chunk_t0, &t0d, sizeof t0d, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+        std::vector<std::array<cudaEvent_t, 3>> evs;
+        for (long j = 0; j < chunk; ++j) {
+            const bool last = done + j == steps - 1;
+            if (timings) {
+                std::vector<cudaEvent_t> e(3);
+                for (auto& x : e) CK(cudaEventCreate(&x));
+                enqueue_step(last, &e);
+                evs.push_back({e[0], e[1], e[2]});
+            } else {
+                cudaGraphExec_t& g = graph_[last ? 1 : 0];
+                if (!g) {
+                    cudaGraph_t graph;
+                    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+                    enqueue_step(last, nullptr);
+                    CK(cudaStreamEndCapture(st, &graph));
+                    CK(cudaGraphInstantiate(&g, graph, 0));
+                    CK(cudaGraphDestroy(graph));
+                }
+                CK(cudaGraphLaunch(g, st));
+            }
+        }
+        CK(cudaStreamSynchronize(st));
+        CK(cudaGetLastError());
+        if (timings) {
+            for (size_t j = 0; j < evs.size(); ++j) {
+                float ib = 0, fl = 0;
+                CK(cudaEventElapsedTime(&ib, evs[j][0], evs[j][1]));
+                CK(cudaEventElapsedTime(&fl, evs[j][1], evs[j][2]));
+                const long step = t0 + long(j);
+                if (has_solids_) timings->push_back({"ib", step, ib * 1e-3});
+                timings->push_back({"fluid", step, fl * 1e-3});
+                timings->push_back({"total", step, (ib + fl) * 1e-3});
+                for (auto x : evs[j]) cudaEventDestroy(x);
+            }
+        }
+        finish_chunk(t0, chunk);
+        if (!status_.ok) break;
+        done += chunk;
+    }
+    return status_;
+}
+
+void Runner::finish_chunk(long t0, long) {
+    DevCounters h{};
+    CK(cudaMemcpy(&h, ctr_, sizeof h, cudaMemcpyDeviceToHost));
+    const long completed = long(h.t) - t0;
+    if (has_solids_ && completed > 0) {
+        const size_t ns = scene_.solids.size(), m = regions_.size();
+        std::vector<double> tot(size_t(completed) * m * ns * 6);
+        CK(cudaMemcpy(tot.data(), totals_dev_, sizeof(double) * tot.size(), cudaMemcpyDeviceToHost));
+        for (long j = 0; j < completed; ++j) {
+            std::array<double, 6> sum{};
+            for (size_t r = 0; r < m; ++r)
+                for (size_t s = 0; s < ns; ++s)
+                    for (int a = 0; a < 6; ++a) sum[a] += tot[((size_t(j) * m + r) * ns + s) * 6 + a];
+            totals_.push_back(sum);
+        }
+    }
+    t_ = long(h.t);
+    if (h.mach) status_.mach_warning = true;
+    if (h.diverged && status_.ok) {
+        status_.ok = false;
+        status_.step = long(h.diverged_step);
+        status_.reason = "divergence: non-positive or non-finite density";
+        // rho*/u* of the diverging step from f(t) (solver.cpp:113-122)
+        for (auto& r : regions_) {
+            FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+            launch_macro(P, int(t_ & 1), stream());
+        }
+        // the reference returns before update_rigid_motion(t+1)
+        if (has_solids_) {
+            double* row = static_cast<double*>(dalloc(sizeof(double) * kMotionRow));
+            for (size_t s = 0; s < scene_.solids.size(); ++s) {
+                if (!moving_[s]) continue;
+                double hrow[kMotionRow];
+                motion_row(int(s), t_, hrow);
+                CK(cudaMemcpy(row, hrow, sizeof hrow, cudaMemcpyHostToDevice));
+                for (auto& r : regions_) launch_ib_motion_once(r.solids[s], row, nx_, ny_, nz_, stream());
+                CK(cudaStreamSynchronize(stream()));
+            }
+            dfree(row);
+        }
+        CK(cudaStreamSynchronize(stream()));
+    }
+}
+
+void Runner::slab(int* z0, int* z1) const {
+    *z0 = regions_.front().z0;
+    *z1 = regions_.back().z1;
+}
+
+void Runner::gather(int what, double* out) const {
+    const size_t beta = what == 0 ? 1 : (what == 1 ? 3 : 27);
+    const unsigned chunk = 1u << 20;
+    double* stage = nullptr;
+    CK(cudaMalloc(&stage, sizeof(double) * beta * chunk));
+    const size_t base_plane = size_t(regions_.front().z0) * regions_.front().geo.plane;
+    try {
+        for (const auto& r : regions_) {
+            FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+            const size_t off = size_t(r.z0) * r.geo.plane - base_plane;
+            for (unsigned k0 = 0; k0 < r.geo.n; k0 += chunk) {
+                const unsigned k1 = std::min(r.geo.n, k0 + chunk);
+                if (what == 2) launch_read_f(P, int(t_ & 1), k0, k1, stage, stream());
+                else launch_read_macro(P, k0, k1, what == 0 ? stage : nullptr, what == 1 ? stage : nullptr, stream());
+                CK(cudaGetLastError());
+                CK(cudaMemcpyAsync(out + (off + k0) * beta, stage, sizeof(double) * beta * (k1 - k0),
+                                   cudaMemcpyDeviceToHost, stream()));
+                CK(cudaStreamSynchronize(stream()));
+            }
+        }
+    } catch (...) {
+        cudaFree(stage);
+        throw;
+    }
+    cudaFree(stage);
+}
+
+size_t Runner::sample_count(int region, int solid) const {
+    if (region < 0 || region >= int(regions_.size()) || solid < 0 || solid >= int(scene_.solids.size()))
+        throw StateError("region/solid index out of range");
+    return regions_[region].solids[solid].n;
+}
+
+void Runner::samples(int region, int solid, double* pos, double* ub, double* force, double* sampled,
+                     uint32_t* src, uint8_t* flagged) const {
+    const IbSolidDev& d = regions_[region].solids[sample_count(region, solid) >= 0 ? solid : 0];
+    const size_t n = d.n;
+    if (n == 0) return;
+    CK(cudaStreamSynchronize(stream()));
+    if (pos) CK(cudaMemcpy(pos, d.pos, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
+    if (ub) CK(cudaMemcpy(ub, d.ub, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
+    if (force) CK(cudaMemcpy(force, d.force, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
+    if (sampled) CK(cudaMemcpy(sampled, d.sampled, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
+    if (src) CK(cudaMemcpy(src, d.source, sizeof(unsigned) * n, cudaMemcpyDeviceToHost));
+    if (flagged) CK(cudaMemcpy(flagged, d.flagged, n, cudaMemcpyDeviceToHost));
+}
+
+void Runner::cell_flags(uint8_t* out) const {
+    const size_t base_plane = size_t(regions_.front().z0) * regions_.front().geo.plane;
+    for (const auto& r : regions_) {
+        unsigned char* d = nullptr;
+        CK(cudaMalloc(&d, size_t(r.geo.n) * 27));
+        FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+        launch_cell_flags(P, 0, r.geo.n, d, stream());
+        CK(cudaStreamSynchronize(stream()));
+        const size_t off = size_t(r.z0) * r.geo.plane - base_plane;
+        cudaError_t e = cudaMemcpy(out + off * 27, d, size_t(r.geo.n) * 27, cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        CK(e);
+    }
+}
+
+// Runner::set_layout (runner.cpp:252-258): permute f into the new Eq. 9
+// layout and re-sort every sample replica by the new block edge.
+void Runner::set_layout(int ell, size_t alpha) {
+    if (ell < 1) throw ConfigError("reorder_samples: block edge must be >= 1");
+    if (alpha < 1) throw ConfigError("layout: alpha and beta must be >= 1");
+    CK(cudaSetDevice(device_));
+    CK(cudaStreamSynchronize(stream()));
+    const Layout old = layout_;
+    layout_.alpha_req = alpha;
+    for (auto& r : regions_) {
+        const RegionGeo go = r.geo;
+        compute_geo(r);
+        const RegionGeo gn = r.geo;
+        if (gn.la == go.la && gn.A == go.A && gn.n_pad == go.n_pad) continue;
+        for (int p = 0; p < 2; ++p) {
+            float* nf = static_cast<float*>(dalloc(sizeof(float) * 27ull * gn.n_pad, false));
+            launch_relayout(r.f[p], nf, go, gn, stream());
+            CK(cudaStreamSynchronize(stream()));
+            dfree(r.f[p]);
+            r.f[p] = nf;
+            r.ptr.f[p] = nf;
+        }
+    }
+    (void)old;
+    for (auto& r : regions_)
+        for (auto& d : r.solids) {
+            const size_t n = d.n;
+            if (n == 0) continue;
+            std::vector<double> pos(3 * n), ref(3 * n), ub(3 * n), fo(3 * n), sa(3 * n);
+            std::vector<unsigned> src(n);
+            std::vector<unsigned char> fl(n);
+            CK(cudaMemcpy(pos.data(), d.pos, 24 * n, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(ref.data(), d.ref, 24 * n, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(ub.data(), d.ub, 24 * n, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(fo.data(), d.force, 24 * n, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(sa.data(), d.sampled, 24 * n, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(src.data(), d.source, 4 * n, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(fl.data(), d.flagged, n, cudaMemcpyDeviceToHost));
+            std::vector<V3> p3(n);
+            for (size_t k = 0; k < n; ++k) p3[k] = v3(&pos[3 * k]);
+            const auto perm = reorder_permutation(p3, std::vector<uint32_t>(src.begin(), src.end()), ell);
+            auto permute3 = [&](std::vector<double>& v) {
+                std::vector<double> o(v.size());
+                for (size_t k = 0; k < n; ++k)
+                    for (int a = 0; a < 3; ++a) o[3 * k + a] = v[3 * perm[k] + a];
+                v.swap(o);
+            };
+            permute3(pos);
+            permute3(ref);
+            permute3(ub);
+            permute3(fo);
+            permute3(sa);
+            std::vector<unsigned> s2(n);
+            std::vector<unsigned char> f2(n);
+            for (size_t k = 0; k < n; ++k) {
+                s2[k] = src[perm[k]];
+                f2[k] = fl[perm[k]];
+            }
+            CK(cudaMemcpy(d.pos, pos.data(), 24 * n, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(d.ref, ref.data(), 24 * n, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(d.ub, ub.data(), 24 * n, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(d.force, fo.data(), 24 * n, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(d.sampled, sa.data(), 24 * n, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(d.source, s2.data(), 4 * n, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(d.flagged, f2.data(), n, cudaMemcpyHostToDevice));
+        }
+    ell_ = ell;
+    invalidate_graphs();
+}
+
+std::unique_ptr<Runner> Runner::clone() const {
+    auto c = std::make_unique<Runner>(scene_, rank_mode_ ? 1 : m_global_, device_, rank_mode_ ? m_global_ : 0,
+                                      rank_);
+    if (layout_.alpha_req != c->layout_.alpha_req || ell_ != c->ell_) c->set_layout(ell_, layout_.alpha_req);
+    c->copy_state_from(*this);
+    return c;
+}
+
+void Runner::copy_state_from(const Runner& o) {
+    CK(cudaStreamSynchronize(o.stream()));
+    auto cp = [](void* d, const void* s, size_t b) {
+        if (d && s && b) CK(cudaMemcpy(d, s, b, cudaMemcpyDeviceToDevice));
+    };
+    for (size_t ri = 0; ri < regions_.size(); ++ri) {
+        Region& d = regions_[ri];
+        const Region& s = o.regions_[ri];
+        const RegionGeo& g = d.geo;
+        for (int p = 0; p < 2; ++p) {
+            cp(d.f[p], s.f[p], sizeof(float) * 27ull * g.n_pad);
+            cp(d.recv_lo[p], s.recv_lo[p], sizeof(float) * 9ull * g.plane);
+            cp(d.recv_hi[p], s.recv_hi[p], sizeof(float) * 9ull * g.plane);
+            cp(d.own_send_lo[p], s.own_send_lo[p], sizeof(float) * 9ull * g.plane);
+            cp(d.own_send_hi[p], s.own_send_hi[p], sizeof(float) * 9ull * g.plane);
+            for (int f = 0; f < 6; ++f) cp(d.ptr.slot[p][f], s.ptr.slot[p][f], sizeof(float) * 9ull * g.slot_plane(f));
+        }
+        cp(d.ptr.rho, s.ptr.rho, sizeof(float) * g.ns);
+        cp(d.ptr.u, s.ptr.u, sizeof(float) * 3ull * g.ns);
+        if (has_solids_) {
+            cp(d.stamp, s.stamp, sizeof(unsigned) * g.ns);
+            cp(d.mrecv_lo, s.mrecv_lo, sizeof(float) * 4ull * g.plane);
+            cp(d.mrecv_hi, s.mrecv_hi, sizeof(float) * 4ull * g.plane);
+            for (size_t k = 0; k < d.solids.size(); ++k) {
+                const IbSolidDev &a = d.solids[k], &b = s.solids[k];
+                const size_t n = a.n;
+                cp(a.pos, b.pos, 24 * n);
+                cp(a.ref, b.ref, 24 * n);
+                cp(a.ub, b.ub, 24 * n);
+                cp(a.force, b.force, 24 * n);
+                cp(a.sampled, b.sampled, 24 * n);
+                cp(a.source, b.source, 4 * n);
+                cp(a.flagged, b.flagged, n);
+            }
+        }
+    }
+    cp(ctr_, o.ctr_, sizeof(DevCounters));
+    t_ = o.t_;
+    status_ = o.status_;
+    totals_ = o.totals_;
+}
+
+// ---- rank mode -----------------------------------------------------------
+
+void Runner::halo_f(int parity, void** send_lo, void** send_hi, void** recv_lo, void** recv_hi,
+                    size_t* bytes) {
+    const int p = parity & 1;
+    const Region& r = regions_.front();
+    *send_lo = r.ptr.send_lo[p];
+    *send_hi = r.ptr.send_hi[p];
+    *recv_lo = const_cast<float*>(r.ptr.recv_lo[p]);
+    *recv_hi = const_cast<float*>(r.ptr.recv_hi[p]);
+    *bytes = sizeof(float) * 9ull * r.geo.plane;
+}
+
+void Runner::halo_macro(void** send_lo, void** send_hi, void** recv_lo, void** recv_hi, size_t* bytes) {
+    const Region& r = regions_.front();
+    *send_lo = r.ptr.msend_lo;
+    *send_hi = r.ptr.msend_hi;
+    *recv_lo = const_cast<float*>(r.ptr.mrecv_lo);
+    *recv_hi = const_cast<float*>(r.ptr.mrecv_hi);
+    *bytes = sizeof(float) * 4ull * r.geo.plane;
+}
+
+void Runner::phase(int ph, int write_macro) {
+    if (!rank_mode_) throw StateError("phase(): only valid for a rank-mode runner");
+    CK(cudaSetDevice(device_));
+    switch (ph) {
+        case LBMG_PHASE_PRE:
+            // the motion/totals tables cover cap_ steps: call sync() at least
+            // that often (lbmg_runner_sync)
+            if (has_solids_) enqueue_ib_pre();
+            break;
+        case LBMG_PHASE_MID:
+            if (has_solids_) enqueue_ib_mid();
+            break;
+        case LBMG_PHASE_FLUID_EDGE: enqueue_fluid(write_macro != 0, 1); break;
+        case LBMG_PHASE_FLUID_BULK: enqueue_fluid(write_macro != 0, 2); break;
+        case LBMG_PHASE_END:
+            if (has_solids_)
+                for (auto& r : regions_) CK(cudaMemsetAsync(r.ptr.tflag, 0, r.geo.ns / 32 + 1, stream()));
+            launch_step_end(ctr_, stream());
+            break;
+        default: throw StateError("unknown phase");
+    }
+    CK(cudaGetLastError());
+}
+
+Status Runner::sync_external() {
+    CK(cudaStreamSynchronize(stream()));
+    finish_chunk(ext_chunk_t0_, 0);
+    ext_chunk_t0_ = t_;
+    if (has_solids_) {
+        fill_motion_table(t_, cap_ + 1);
+        long long t0d = t_;
+        CK(cudaMemcpy(&ctr_->chunk_t0, &t0d, sizeof t0d, cudaMemcpyHostToDevice));
+    }
+    return status_;
+}
+
+}  // namespace lbmg

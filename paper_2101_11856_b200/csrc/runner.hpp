@@ -1,0 +1,167 @@
+// Device-engine Runner: the GPU counterpart of lbm::Runner
+// (runner.hpp:25-83 / runner.cpp).  Owns every device allocation; host-side
+// results (status, step count, totals log) mirror the reference semantics.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+#include "scene.hpp"
+
+namespace lbmg {
+
+struct CudaError : std::runtime_error {
+    explicit CudaError(const std::string& m) : std::runtime_error(m) {}
+};
+struct OomError : std::runtime_error {
+    explicit OomError(const std::string& m) : std::runtime_error(m) {}
+};
+struct StateError : std::runtime_error {
+    explicit StateError(const std::string& m) : std::runtime_error(m) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+
+struct Status {
+    bool ok = true;
+    bool mach_warning = false;
+    long step = -1;
+    std::string reason;
+};
+
+struct Timing {
+    std::string phase;
+    long step;
+    double seconds;
+};
+
+struct Layout {
+    size_t alpha_req = 1;  // API value (Runner::alpha)
+    int la = 5;            // effective device group log2 (31 = SoA)
+    bool soa = false;
+};
+
+class Runner {
+public:
+    // world/rank: rank mode (one slab of `world`, external halo exchange).
+    // world == 0: in-process mode with `regions` slabs on one device.
+    Runner(const lbmg_scene& scene, int regions, int device, int world, int rank);
+    ~Runner();
+    Runner(const Runner&) = delete;
+    Runner& operator=(const Runner&) = delete;
+
+    std::unique_ptr<Runner> clone() const;
+
+    Status advance(long steps, std::vector<Timing>* timings);
+    long step_count() const { return t_; }
+    const Status& status() const { return status_; }
+    int region_count() const { return int(regions_.size()); }
+    int global_regions() const { return m_global_; }
+    void set_layout(int ell, size_t alpha);
+    size_t alpha() const { return layout_.alpha_req; }
+    int block_edge() const { return ell_; }
+    int nx() const { return nx_; }
+    int ny() const { return ny_; }
+    int nz() const { return nz_; }
+    void slab(int* z0, int* z1) const;
+
+    void gather(int what, double* out) const;  // 0 rho, 1 u, 2 f
+    const std::vector<std::array<double, 6>>& totals_log() const { return totals_; }
+    size_t sample_count(int region, int solid) const;
+    void samples(int region, int solid, double* pos, double* ub, double* force, double* sampled,
+                 uint32_t* src, uint8_t* flagged) const;
+    void cell_flags(uint8_t* out) const;
+    void set_stream(cudaStream_t s) { ext_stream_ = s; invalidate_graphs(); }
+    cudaStream_t stream() const { return ext_stream_ ? ext_stream_ : stream_; }
+
+    // rank mode
+    void halo_f(int parity, void** send_lo, void** send_hi, void** recv_lo, void** recv_hi, size_t* bytes);
+    void halo_macro(void** send_lo, void** send_hi, void** recv_lo, void** recv_hi, size_t* bytes);
+    void phase(int ph, int write_macro);
+    Status sync_external();
+
+private:
+    struct SolidDev {
+        IbSolidDev d;
+    };
+    struct Region {
+        int z0 = 0, z1 = 0;
+        bool has_lo = false, has_hi = false;
+        RegionGeo geo{};
+        RegionPtrs ptr{};
+        float* f[2] = {nullptr, nullptr};
+        float* recv_lo[2] = {nullptr, nullptr};
+        float* recv_hi[2] = {nullptr, nullptr};
+        float* own_send_lo[2] = {nullptr, nullptr};  // rank mode only
+        float* own_send_hi[2] = {nullptr, nullptr};
+        float* mrecv_lo = nullptr;
+        float* mrecv_hi = nullptr;
+        float* own_msend_lo = nullptr;
+        float* own_msend_hi = nullptr;
+        unsigned* stamp = nullptr;
+        unsigned* band = nullptr;
+        double* partial = nullptr;
+        std::vector<IbSolidDev> solids;
+        FluidParams params() const;
+    };
+
+    void* dalloc(size_t bytes, bool zero = true);
+    void dfree(void* p);
+    void build_regions(int device);
+    void compute_geo(Region& r) const;
+    void alloc_f(Region& r);
+    void link_halos();
+    void init_fields();
+    void upload_solids();
+    void fill_motion_table(long t0, long rows);
+    void motion_row(int solid, long t, double* row) const;
+    void enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev);
+    void enqueue_ib_pre();
+    void enqueue_ib_mid();
+    void enqueue_fluid(bool write_macro, int part);
+    void invalidate_graphs();
+    void finish_chunk(long t0, long requested);
+    void copy_state_from(const Runner& o);
+
+    lbmg_scene scene_;
+    int nx_ = 0, ny_ = 0, nz_ = 0;
+    int m_global_ = 1;  // total slabs (regions, or world in rank mode)
+    bool rank_mode_ = false;
+    int rank_ = 0;
+    int device_ = 0;
+    int sm_count_ = 148;
+    std::vector<Region> regions_;
+    Layout layout_;
+    int ell_ = 1;
+    FaceTable faces_{};
+    ModelConst model_{};
+    bool has_solids_ = false;
+    std::vector<char> moving_;
+    size_t total_samples_ = 0;
+
+    DevCounters* ctr_ = nullptr;
+    double* motion_tab_ = nullptr;  // [cap+1][nsolid][kMotionRow]
+    double* totals_dev_ = nullptr;  // [cap][regions][nsolid][6]
+    long cap_ = 256;
+    std::vector<void*> allocs_;
+
+    cudaStream_t stream_ = nullptr;
+    cudaStream_t ext_stream_ = nullptr;
+    cudaGraphExec_t graph_[2] = {nullptr, nullptr};
+
+    long t_ = 0;
+    Status status_;
+    std::vector<std::array<double, 6>> totals_;
+    long ext_chunk_t0_ = 0;  // rank mode: start of the externally driven chunk
+};
+
+}  // namespace lbmg
+
+struct lbmg_runner {
+    std::unique_ptr<lbmg::Runner> impl;
+};

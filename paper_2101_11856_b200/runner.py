@@ -1,0 +1,365 @@
+"""Python mirror of the reference's Runner / build_scene API over the C ABI.
+
+Every call goes through the in-tree sm_100a library `_build/liblbmg.so`
+(include/lbmg.h).  There is no CPU fallback: if the library is missing the
+import fails loudly, and every device call raises when CUDA is unavailable.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from pathlib import Path
+from typing import List, Optional
+
+import numpy as np
+
+from . import _abi
+from .scene import ConfigError, SceneConfig
+
+_LIB_PATH = Path(__file__).resolve().parent / "_build" / "liblbmg.so"
+_lib = None
+
+
+class LbmError(RuntimeError):
+    pass
+
+
+class CudaError(LbmError):
+    pass
+
+
+class StateError(LbmError):
+    pass
+
+
+def lib():
+    """Load liblbmg.so (built by paper_2101_11856_b200/build.py)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not _LIB_PATH.exists():
+        raise ImportError(f"{_LIB_PATH} is missing: run `python -m paper_2101_11856_b200.build` "
+                          "(the engine has no CPU fallback)")
+    L = C.CDLL(str(_LIB_PATH))
+    P, D, I, SZ = C.c_void_p, C.POINTER(C.c_double), C.c_int, C.c_size_t
+    U32P, U8P = C.POINTER(C.c_uint32), C.POINTER(C.c_uint8)
+    sig = {
+        "lbmg_abi_version": (I, []),
+        "lbmg_last_error": (C.c_char_p, []),
+        "lbmg_device_count": (I, []),
+        "lbmg_scene_config_default": (None, [C.POINTER(_abi.SceneConfigC)]),
+        "lbmg_validate_config": (I, [C.POINTER(_abi.SceneConfigC), D]),
+        "lbmg_scene_build": (I, [C.POINTER(_abi.SceneConfigC), C.POINTER(P)]),
+        "lbmg_scene_destroy": (None, [P]),
+        "lbmg_scene_solid_count": (I, [P]),
+        "lbmg_scene_sample_count": (SZ, [P, I]),
+        "lbmg_scene_samples": (I, [P, I, D, D, U32P, U8P, D, C.POINTER(I)]),
+        "lbmg_scene_set_samples": (I, [P, I, SZ, D, D, U32P]),
+        "lbmg_morton3": (C.c_uint64, [C.c_uint32, C.c_uint32, C.c_uint32]),
+        "lbmg_reorder_permutation": (I, [SZ, D, U32P, I, U32P]),
+        "lbmg_split_domain": (I, [I, I, C.POINTER(I)]),
+        "lbmg_runner_create": (I, [P, I, I, C.POINTER(P)]),
+        "lbmg_runner_create_rank": (I, [P, I, I, I, C.POINTER(P)]),
+        "lbmg_runner_destroy": (None, [P]),
+        "lbmg_runner_clone": (I, [P, C.POINTER(P)]),
+        "lbmg_runner_set_stream": (I, [P, P]),
+        "lbmg_runner_advance": (I, [P, C.c_long, C.POINTER(_abi.StatusC), C.POINTER(_abi.TimingRowC), SZ,
+                                    C.POINTER(SZ)]),
+        "lbmg_runner_step_count": (C.c_long, [P]),
+        "lbmg_runner_status": (I, [P, C.POINTER(_abi.StatusC)]),
+        "lbmg_runner_dims": (I, [P, C.POINTER(I), C.POINTER(I), C.POINTER(I)]),
+        "lbmg_runner_region_count": (I, [P]),
+        "lbmg_runner_set_layout": (I, [P, I, SZ]),
+        "lbmg_runner_alpha": (SZ, [P]),
+        "lbmg_runner_block_edge": (I, [P]),
+        "lbmg_runner_gather_rho": (I, [P, D]),
+        "lbmg_runner_gather_u": (I, [P, D]),
+        "lbmg_runner_gather_f": (I, [P, D]),
+        "lbmg_runner_slab": (I, [P, C.POINTER(I), C.POINTER(I)]),
+        "lbmg_runner_totals_count": (SZ, [P]),
+        "lbmg_runner_totals": (I, [P, D, SZ]),
+        "lbmg_runner_sample_count": (SZ, [P, I, I]),
+        "lbmg_runner_samples": (I, [P, I, I, D, D, D, D, U32P, U8P]),
+        "lbmg_runner_cell_flags": (I, [P, U8P]),
+        "lbmg_runner_halo_f": (I, [P, I, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(SZ)]),
+        "lbmg_runner_halo_macro": (I, [P, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P),
+                                       C.POINTER(SZ)]),
+        "lbmg_runner_phase": (I, [P, I, I]),
+        "lbmg_runner_sync": (I, [P, C.POINTER(_abi.StatusC)]),
+        "lbmg_collide_batch": (I, [C.POINTER(_abi.SceneConfigC), SZ, D, D, D, D]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def _check(code: int):
+    if code == 0:
+        return
+    msg = lib().lbmg_last_error().decode(errors="replace")
+    if code == 1:
+        raise ConfigError(msg)
+    if code in (2, 3):
+        raise CudaError(msg)
+    raise StateError(msg)
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _u32(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_uint32))
+
+
+def _u8(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_uint8))
+
+
+def device_count() -> int:
+    return lib().lbmg_device_count()
+
+
+def model_rates(cfg: SceneConfig) -> np.ndarray:
+    """Effective rates in canonical moment-row order (SceneConfig::make_model)."""
+    cs = cfg.to_c()
+    out = np.zeros(27)
+    _check(lib().lbmg_validate_config(cs.ptr, _dp(out)))
+    return out
+
+
+def morton3(x: int, y: int, z: int) -> int:
+    return int(lib().lbmg_morton3(x, y, z))
+
+
+def reorder_permutation(positions: np.ndarray, source_id: np.ndarray, ell: int) -> np.ndarray:
+    pos = np.ascontiguousarray(positions, dtype=np.float64)
+    src = np.ascontiguousarray(source_id, dtype=np.uint32)
+    perm = np.zeros(len(src), dtype=np.uint32)
+    _check(lib().lbmg_reorder_permutation(len(src), _dp(pos), _u32(src), ell, _u32(perm)))
+    return perm
+
+
+def split_domain(nz: int, m: int) -> List[tuple]:
+    buf = (C.c_int * (2 * max(m, 1)))()
+    _check(lib().lbmg_split_domain(nz, m, buf))
+    return [(buf[2 * r], buf[2 * r + 1]) for r in range(m)]
+
+
+@dataclass
+class StepStatus:
+    ok: bool = True
+    mach_warning: bool = False
+    step: int = -1
+    reason: str = ""
+
+    @staticmethod
+    def _from(c: _abi.StatusC) -> "StepStatus":
+        return StepStatus(bool(c.ok), bool(c.mach_warning), int(c.step), c.reason.decode())
+
+
+@dataclass
+class TimingRow:
+    phase: str
+    step: int
+    seconds: float
+
+
+class Scene:
+    """build_scene (scene.cpp:341-366): sampled, ordered, motion-annotated solids."""
+
+    def __init__(self, cfg: SceneConfig):
+        self.cfg = cfg
+        cs = cfg.to_c()
+        h = C.c_void_p()
+        _check(lib().lbmg_scene_build(cs.ptr, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().lbmg_scene_destroy(self._h)
+            self._h = None
+
+    @property
+    def solid_count(self) -> int:
+        return lib().lbmg_scene_solid_count(self._h)
+
+    def samples(self, solid: int) -> dict:
+        n = lib().lbmg_scene_sample_count(self._h, solid)
+        pos, ref = np.zeros((n, 3)), np.zeros((n, 3))
+        src = np.zeros(n, dtype=np.uint32)
+        bbox = np.zeros(6)
+        ell = C.c_int()
+        _check(lib().lbmg_scene_samples(self._h, solid, _dp(pos), _dp(ref), _u32(src), None, _dp(bbox),
+                                        C.byref(ell)))
+        return {"positions": pos, "reference_positions": ref, "source_id": src, "bbox_lo": bbox[:3],
+                "bbox_hi": bbox[3:], "block_edge": ell.value}
+
+    def set_samples(self, solid: int, positions, reference_positions, source_id):
+        pos = np.ascontiguousarray(positions, dtype=np.float64)
+        ref = np.ascontiguousarray(reference_positions, dtype=np.float64)
+        src = np.ascontiguousarray(source_id, dtype=np.uint32)
+        _check(lib().lbmg_scene_set_samples(self._h, solid, len(src), _dp(pos), _dp(ref), _u32(src)))
+
+
+def build_scene(cfg: SceneConfig) -> Scene:
+    return Scene(cfg)
+
+
+class Runner:
+    """lbm::Runner (runner.hpp:25-83) on the B200 engine."""
+
+    def __init__(self, scene: Scene, regions: Optional[int] = None, device: int = 0, *,
+                 world: int = 0, rank: int = 0, _handle=None):
+        self.scene = scene
+        if _handle is not None:
+            self._h = _handle
+            return
+        h = C.c_void_p()
+        if world > 0:
+            _check(lib().lbmg_runner_create_rank(scene._h, world, rank, device, C.byref(h)))
+        else:
+            m = scene.cfg.regions if regions is None else regions
+            _check(lib().lbmg_runner_create(scene._h, m, device, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().lbmg_runner_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    # -- stepping ----------------------------------------------------------
+    def advance(self, steps: int, timings: Optional[list] = None) -> StepStatus:
+        st = _abi.StatusC()
+        if timings is None:
+            _check(lib().lbmg_runner_advance(self._h, steps, C.byref(st), None, 0, None))
+        else:
+            cap = max(1, steps) * 3
+            rows = (_abi.TimingRowC * cap)()
+            n = C.c_size_t()
+            _check(lib().lbmg_runner_advance(self._h, steps, C.byref(st), rows, cap, C.byref(n)))
+            for k in range(n.value):
+                timings.append(TimingRow(rows[k].phase.decode(), rows[k].step, rows[k].seconds))
+        return StepStatus._from(st)
+
+    def step_count(self) -> int:
+        return int(lib().lbmg_runner_step_count(self._h))
+
+    def status(self) -> StepStatus:
+        st = _abi.StatusC()
+        _check(lib().lbmg_runner_status(self._h, C.byref(st)))
+        return StepStatus._from(st)
+
+    def dims(self):
+        x, y, z = C.c_int(), C.c_int(), C.c_int()
+        _check(lib().lbmg_runner_dims(self._h, C.byref(x), C.byref(y), C.byref(z)))
+        return (x.value, y.value, z.value)
+
+    def region_count(self) -> int:
+        return lib().lbmg_runner_region_count(self._h)
+
+    def set_layout(self, block_edge: int, alpha: int):
+        _check(lib().lbmg_runner_set_layout(self._h, block_edge, alpha))
+
+    def alpha(self) -> int:
+        return int(lib().lbmg_runner_alpha(self._h))
+
+    def block_edge(self) -> int:
+        return int(lib().lbmg_runner_block_edge(self._h))
+
+    def clone(self) -> "Runner":
+        h = C.c_void_p()
+        _check(lib().lbmg_runner_clone(self._h, C.byref(h)))
+        return Runner(self.scene, _handle=h)
+
+    def set_stream(self, stream_ptr: int):
+        _check(lib().lbmg_runner_set_stream(self._h, C.c_void_p(stream_ptr)))
+
+    # -- readback ----------------------------------------------------------
+    def slab(self):
+        z0, z1 = C.c_int(), C.c_int()
+        _check(lib().lbmg_runner_slab(self._h, C.byref(z0), C.byref(z1)))
+        return z0.value, z1.value
+
+    def _n_local(self):
+        nx, ny, _ = self.dims()
+        z0, z1 = self.slab()
+        return nx * ny * (z1 - z0)
+
+    def gather_rho(self) -> np.ndarray:
+        out = np.empty(self._n_local())
+        _check(lib().lbmg_runner_gather_rho(self._h, _dp(out)))
+        return out
+
+    def gather_u(self) -> np.ndarray:
+        out = np.empty((self._n_local(), 3))
+        _check(lib().lbmg_runner_gather_u(self._h, _dp(out)))
+        return out
+
+    def gather_f(self) -> np.ndarray:
+        out = np.empty((self._n_local(), 27))
+        _check(lib().lbmg_runner_gather_f(self._h, _dp(out)))
+        return out
+
+    def totals_log(self) -> np.ndarray:
+        n = lib().lbmg_runner_totals_count(self._h)
+        out = np.zeros((n, 6))
+        if n:
+            _check(lib().lbmg_runner_totals(self._h, _dp(out), n))
+        return out
+
+    def samples(self, region: int, solid: int) -> dict:
+        n = lib().lbmg_runner_sample_count(self._h, region, solid)
+        arrs = {k: np.zeros((n, 3)) for k in ("positions", "boundary_velocity", "penalty_force",
+                                               "sampled_velocity")}
+        src = np.zeros(n, dtype=np.uint32)
+        fl = np.zeros(n, dtype=np.uint8)
+        _check(lib().lbmg_runner_samples(self._h, region, solid, _dp(arrs["positions"]),
+                                         _dp(arrs["boundary_velocity"]), _dp(arrs["penalty_force"]),
+                                         _dp(arrs["sampled_velocity"]), _u32(src), _u8(fl)))
+        arrs["source_id"] = src
+        arrs["flagged"] = fl
+        return arrs
+
+    def cell_flags(self) -> np.ndarray:
+        out = np.zeros((self._n_local(), 27), dtype=np.uint8)
+        _check(lib().lbmg_runner_cell_flags(self._h, _u8(out)))
+        return out
+
+    # -- rank mode (multi-process halo exchange) ---------------------------
+    def halo_f(self, parity: int):
+        ptrs = [C.c_void_p() for _ in range(4)]
+        nb = C.c_size_t()
+        _check(lib().lbmg_runner_halo_f(self._h, parity, *[C.byref(p) for p in ptrs], C.byref(nb)))
+        return [p.value for p in ptrs], nb.value
+
+    def halo_macro(self):
+        ptrs = [C.c_void_p() for _ in range(4)]
+        nb = C.c_size_t()
+        _check(lib().lbmg_runner_halo_macro(self._h, *[C.byref(p) for p in ptrs], C.byref(nb)))
+        return [p.value for p in ptrs], nb.value
+
+    def phase(self, ph: int, write_macro: bool = False):
+        _check(lib().lbmg_runner_phase(self._h, ph, int(write_macro)))
+
+    def sync(self) -> StepStatus:
+        st = _abi.StatusC()
+        _check(lib().lbmg_runner_sync(self._h, C.byref(st)))
+        return StepStatus._from(st)
+
+
+def collide_batch(cfg: SceneConfig, f: np.ndarray, rho: np.ndarray, u: np.ndarray) -> np.ndarray:
+    """collide() of n nodes on the device (fp32 arithmetic)."""
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    rho = np.ascontiguousarray(rho, dtype=np.float64)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    out = np.zeros_like(f)
+    cs = cfg.to_c()
+    _check(lib().lbmg_collide_batch(cs.ptr, len(rho), _dp(f), _dp(rho), _dp(u), _dp(out)))
+    return out

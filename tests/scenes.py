@@ -1,0 +1,83 @@
+"""Parity scenes shared by the tests (SURVEY.md §8(d) configs and their
+small twins).  All use cm-mrt + relax-toward-one with high_order_rate 1.5 so
+the adaptive (ACM) path is exercised."""
+from paper_2101_11856_b200 import FaceSpec, MeshConfig, RigidMotion, SceneConfig, SolidConfig
+
+
+def acm(cfg: SceneConfig) -> SceneConfig:
+    cfg.kind = "cm-mrt"
+    cfg.high_order_rate = 1.5
+    cfg.policy = "relax-toward-one"
+    cfg.policy_eps0 = 0.01
+    return cfg
+
+
+def faces(*conds, inlet=(0.05, 0.0, 0.0)):
+    out = []
+    for c in conds:
+        out.append(FaceSpec(c, inlet if c == "inlet" else (0.0, 0.0, 0.0)))
+    return out
+
+
+def cavity(n=64, nu=0.02, lid=0.05) -> SceneConfig:
+    """C1: lid-driven cavity, z+ inlet lid, other faces no-slip."""
+    cfg = acm(SceneConfig(nx=n, ny=n, nz=n, viscosity=nu))
+    cfg.faces = faces("no-slip", "no-slip", "no-slip", "no-slip", "no-slip", "inlet", inlet=(lid, 0.0, 0.0))
+    return cfg
+
+
+def closed_box(n=16, u0=(0.02, -0.01, 0.005)) -> SceneConfig:
+    cfg = acm(SceneConfig(nx=n, ny=n + 2, nz=n + 1, viscosity=0.02))
+    cfg.init_velocity = u0
+    return cfg
+
+
+def taylor_green(nx=64, ny=64, nz=4, nu=0.02, kind="cm-mrt") -> SceneConfig:
+    cfg = acm(SceneConfig(nx=nx, ny=ny, nz=nz, viscosity=nu))
+    cfg.kind = kind
+    cfg.faces = faces(*["periodic"] * 6)
+    cfg.init = "taylor-green"
+    cfg.tg_u_max = 0.02
+    return cfg
+
+
+def sphere(nx=256, ny=128, nz=128, center=(80, 64, 64), radius=16.0, subdiv=4, r=0.5) -> SceneConfig:
+    """C2: flow past a sphere, x- inlet, x+ outflow, y/z no-slip."""
+    cfg = acm(SceneConfig(nx=nx, ny=ny, nz=nz, viscosity=0.02))
+    cfg.faces = faces("inlet", "outflow", "no-slip", "no-slip", "no-slip", "no-slip")
+    cfg.init_velocity = (0.05, 0.0, 0.0)
+    cfg.solids = [SolidConfig(MeshConfig(type="sphere", center=center, radius=radius, subdivisions=subdiv),
+                              poisson_radius=r)]
+    cfg.block_edge = 2
+    cfg.seed = 1
+    return cfg
+
+
+def channel(n=128, nz=None) -> SceneConfig:
+    """C3 twin: y walls, x and z periodic, body force along z."""
+    cfg = acm(SceneConfig(nx=n, ny=n, nz=nz or n, viscosity=0.002))
+    cfg.faces = faces("periodic", "periodic", "no-slip", "no-slip", "periodic", "periodic")
+    cfg.body_force = (0.0, 0.0, 1e-6)
+    return cfg
+
+
+def rotating_fins(nx=128, ny=64, nz=64) -> SceneConfig:
+    """C5 twin: rotating fin comb about x (SURVEY App. B `twins`)."""
+    import math
+    cfg = acm(SceneConfig(nx=nx, ny=ny, nz=nz, viscosity=0.02))
+    cfg.faces = faces("no-slip", "no-slip", "no-slip", "no-slip", "no-slip", "no-slip")
+    cfg.solids = [SolidConfig(MeshConfig(type="fin-comb", origin=(52, 22, 22), fins=8, fin_length=20,
+                                         fin_height=16, fin_spacing=2.5), poisson_radius=0.5,
+                              motion=RigidMotion(angular_velocity=(2 * math.pi / 500, 0, 0),
+                                                 center=(62, 30.75, 30)))]
+    cfg.block_edge = 2
+    return cfg
+
+
+def outflow_mix(nx=10, ny=8, nz=7) -> SceneConfig:
+    """Edge semantics stress: outflow faces meeting no-slip/inlet/outflow
+    (stale outflow-edge reads)."""
+    cfg = acm(SceneConfig(nx=nx, ny=ny, nz=nz, viscosity=0.05))
+    cfg.faces = faces("inlet", "outflow", "no-slip", "outflow", "outflow", "inlet", inlet=(0.03, 0.01, -0.01))
+    cfg.init_velocity = (0.02, 0.0, 0.0)
+    return cfg

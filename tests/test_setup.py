@@ -1,0 +1,145 @@
+"""CPU tests: host-side setup and the C ABI surface, checked bit-exact
+against the unmodified reference (oracle/_ref) and the golden fixtures."""
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2101_11856_b200 as lbm
+from oracle import refpy
+from tests import scenes
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def test_library_exports_every_declared_symbol():
+    header = (ROOT / "include" / "lbmg.h").read_text()
+    declared = set(re.findall(r"\b(lbmg_[a-z0-9_]+)\s*\(", header))
+    L = lbm.lib()
+    missing = [s for s in sorted(declared) if not hasattr(L, s)]
+    assert not missing, missing
+    assert L.lbmg_abi_version() == 1
+
+
+def test_lattice_tables_match_reference():
+    c, w, opp = refpy.ref_lattice()
+    q, deg = refpy.ref_moment_exponents()
+    # our constexpr tables are restated in oracle/lbm_oracle.c and csrc/lattice.cuh;
+    # check the documented invariants the kernels rely on
+    for i in range(27):
+        t = (c[i, 0] + 1) + 3 * (c[i, 1] + 1) + 9 * (c[i, 2] + 1)
+        assert t == (13 if i == 0 else (i - 1 if i <= 13 else i))
+        assert opp[i] == (0 if i == 0 else 27 - i)
+    assert set(np.where(c[:, 2] == -1)[0]) == set(range(1, 10))
+    assert set(np.where(c[:, 2] == 1)[0]) == set(range(18, 27))
+    assert np.isclose(w.sum(), 1.0)
+    assert list(np.bincount(deg)) == [1, 3, 6, 7, 6, 3, 1]
+
+
+@pytest.mark.parametrize("kind,hor,policy", [("bgk", 1.0, "constant"), ("rm-mrt", 1.3, "constant"),
+                                             ("cm-mrt", 1.5, "relax-toward-one")])
+def test_model_rates_match_reference(kind, hor, policy):
+    cfg = lbm.SceneConfig(nx=4, ny=4, nz=4, viscosity=0.02, kind=kind, high_order_rate=hor, policy=policy)
+    assert np.array_equal(lbm.model_rates(cfg), refpy.ref_rates(cfg))
+
+
+def test_rate_validation_errors():
+    cfg = lbm.SceneConfig(nx=4, ny=4, nz=4, viscosity=0.02, kind="cm-mrt", high_order_rate=2.5)
+    with pytest.raises(lbm.ConfigError):
+        lbm.model_rates(cfg)
+    cfg = lbm.SceneConfig(nx=4, ny=4, nz=4, viscosity=-1.0)
+    with pytest.raises(lbm.ConfigError):
+        lbm.model_rates(cfg)
+
+
+def test_morton3_spec_examples():
+    # SPEC.md:335 examples + exhaustive small cube vs reference
+    assert lbm.morton3(1, 1, 1) == 7
+    assert lbm.morton3(3, 5, 7) == 431
+    rng = np.random.default_rng(3)
+    for x, y, z in rng.integers(0, 1 << 21, size=(200, 3)):
+        assert lbm.morton3(int(x), int(y), int(z)) == refpy.ref_morton3(int(x), int(y), int(z))
+
+
+@pytest.mark.parametrize("nz,m", [(8, 4), (10, 4), (7, 2), (128, 3), (5, 5), (512, 8)])
+def test_split_domain_matches_reference(nz, m):
+    assert lbm.split_domain(nz, m) == refpy.ref_split_domain(nz, m)
+
+
+def test_split_domain_spec_examples():
+    # SPEC.md:454-456
+    assert [b - a for a, b in lbm.split_domain(8, 4)] == [2, 2, 2, 2]
+    assert [b - a for a, b in lbm.split_domain(10, 4)] == [3, 3, 2, 2]
+    assert [b - a for a, b in lbm.split_domain(7, 2)] == [4, 3]
+    with pytest.raises(lbm.ConfigError):
+        lbm.split_domain(4, 5)
+
+
+@pytest.mark.parametrize("ell", [1, 2, 3, 4, 7])
+def test_reorder_permutation_matches_reference(ell):
+    rng = np.random.default_rng(ell)
+    pos = rng.uniform(-3.0, 17.0, size=(2000, 3))
+    pos[::7] = np.floor(pos[::7])  # exact cell corners
+    src = rng.permutation(2000).astype(np.uint32)
+    assert np.array_equal(lbm.reorder_permutation(pos, src, ell), refpy.ref_reorder_permutation(pos, src, ell))
+
+
+SCENES = {
+    "c2_sphere": lambda: scenes.sphere(),
+    "sphere_small_elim": lambda: _elim(scenes.sphere(48, 32, 32, center=(16, 16, 16), radius=6.0, subdiv=3, r=0.6)),
+    "fin_comb_moving": lambda: scenes.rotating_fins(),
+    "boxes": lambda: _boxes(),
+}
+
+
+def _elim(cfg):
+    cfg.solids[0].sampling = "elimination"
+    return cfg
+
+
+def _boxes():
+    cfg = scenes.sphere(64, 32, 40)
+    cfg.solids = [lbm.SolidConfig(lbm.MeshConfig(type="box", lo=(10, 1.2, 8), hi=(18, 20, 15)), poisson_radius=0.7),
+                  lbm.SolidConfig(lbm.MeshConfig(type="box", lo=(30, 1.2, 20), hi=(36, 12, 30)), poisson_radius=0.7),
+                  lbm.SolidConfig(lbm.MeshConfig(type="quad", size=6.0, plane_z=3.5), poisson_radius=0.5)]
+    cfg.block_edge = 3
+    cfg.seed = 7
+    return cfg
+
+
+@pytest.mark.parametrize("name", sorted(SCENES))
+def test_scene_samples_bit_exact(name):
+    cfg = SCENES[name]()
+    ours = lbm.build_scene(cfg)
+    ref = refpy.RefRunner(cfg, threads=2)
+    for s in range(len(cfg.solids)):
+        a, b = ours.samples(s), ref.scene_samples(s)
+        assert len(a["source_id"]) > 0
+        assert np.array_equal(a["positions"], b["positions"])
+        assert np.array_equal(a["reference_positions"], b["reference_positions"])
+        assert np.array_equal(a["source_id"], b["source_id"])
+        assert np.array_equal(a["bbox_lo"], b["bbox_lo"]) and np.array_equal(a["bbox_hi"], b["bbox_hi"])
+        assert a["block_edge"] == b["block_edge"]
+
+
+def test_c2_sample_count_matches_survey():
+    # C2 recommended scene -> 8,329 samples
+    assert len(lbm.build_scene(scenes.sphere()).samples(0)["source_id"]) == 8329
+
+
+def test_scene_json_roundtrip_and_strictness():
+    text = """{"grid": {"nx": 8, "ny": 8, "nz": 8}, "viscosity": 0.02,
+      "collision": {"kind": "cm-mrt", "high_order_rate": 1.5, "policy": "relax-toward-one"},
+      "faces": {"x-": {"condition": "inlet", "velocity": [0.05, 0, 0]}, "x+": {"condition": "outflow"},
+                "y-": {"condition": "no-slip"}, "y+": {"condition": "no-slip"},
+                "z-": {"condition": "periodic"}, "z+": {"condition": "periodic"}},
+      "solids": [{"mesh": {"type": "sphere", "center": [4, 4, 4], "radius": 2}, "poisson_radius": 0.5}],
+      "layout": {"alpha": 64, "block_edge": 2}, "seed": 3}"""
+    cfg = lbm.parse_scene_config(text)
+    assert cfg.kind == "cm-mrt" and cfg.alpha == 64 and cfg.block_edge == 2
+    assert cfg.faces[1].condition == "outflow" and cfg.solids[0].mesh.radius == 2.0
+    with pytest.raises(lbm.ConfigError):
+        lbm.parse_scene_config(text.replace('"seed": 3', '"sede": 3'))
+    with pytest.raises(lbm.ConfigError):
+        lbm.parse_scene_config(text.replace('"z+": {"condition": "periodic"}', '"z+": {"condition": "no-slip"}'))
