@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 ACM-MRT + IB lattice-Boltzmann step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c3|c1]
+
+A "step" is one full time step (IB band pre-pass + IB spread/totals + fused
+stream/face/moments/CM-MRT collision) of the workload.  N=1: configs[1] of
+BASELINE.json (flow past a sphere 256x128x128 with IB samples).  N>1 (torchrun,
+one process per GPU): the same per-GPU workload stacked along z (weak
+scaling), z-slab halos over NCCL.  Rank 0 prints one JSON line.
+
+--impl reference times the reference's own CPU implementation (the
+unmodified reference compiled into oracle/_ref) on this box's host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+ALG_BYTES_PER_LU = 216          # 27 fp32 reads + 27 fp32 writes
+IB_BYTES_PER_BAND_NODE = 68
+IB_BYTES_PER_SAMPLE = 60
+
+
+def c2_config(n_gpus: int):
+    from tests import scenes
+    import paper_2101_11856_b200 as lbm
+    cfg = scenes.sphere()  # 256x128x128, sphere r=16 at (80,64,64), Poisson 0.5, seed 1, ell 2
+    cfg.alpha = 1 << 22     # SoA on the device (set_layout is a pure permutation)
+    if n_gpus > 1:          # weak scaling: one sphere per 128-plane slab
+        cfg.nz = 128 * n_gpus
+        sph = cfg.solids[0]
+        cfg.solids = [lbm.SolidConfig(lbm.MeshConfig(type="sphere", center=(80, 64, 64 + 128 * k), radius=16.0,
+                                                     subdivisions=4), poisson_radius=0.5) for k in range(n_gpus)]
+        del sph
+    return cfg, "flow past a sphere 256x128x128 per GPU, D3Q27 ACM-MRT + IB (configs[1])"
+
+
+def c3_config(n_gpus: int):
+    from tests import scenes
+    cfg = scenes.channel(n=512, nz=512 * n_gpus)
+    cfg.alpha = 1 << 30
+    return cfg, "channel 512^3 per GPU, D3Q27 ACM-MRT, z-periodic ring (configs[2])"
+
+
+def c1_config(n_gpus: int):
+    from tests import scenes
+    cfg = scenes.cavity(n=64)
+    cfg.alpha = 1 << 20
+    return cfg, "lid-driven cavity 64^3 D3Q27 ACM-MRT (configs[0], L2-resident)"
+
+
+CONFIGS = {"c2": c2_config, "c3": c3_config, "c1": c1_config}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        cmd = ["nvidia-smi", f"--id={self.index}", "--query-gpu=" + ",".join(self.FIELDS),
+               "--format=csv,noheader,nounits"]
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(cmd, capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for s in self.samples for j in range(4) if s[2 + j] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic(config: str):
+    """dram bytes per launch of the fluid kernel from the committed ncu summary."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    return d.get(config, {}).get("fluid_dram_bytes_per_launch")
+
+
+def cpu_baseline_sample(cfg, seconds: float = 12.0):
+    """The reference (oracle/_ref) on this box's host cores: a bounded sample
+    of the same workload (whole grid, a few steps)."""
+    from oracle.refpy import RefRunner
+    threads = os.cpu_count() or 1
+    r = RefRunner(cfg, threads=threads)
+    t0 = time.perf_counter()
+    r.advance(1)
+    dt1 = max(time.perf_counter() - t0, 1e-3)
+    k = max(1, min(50, int(seconds / dt1)))
+    t0 = time.perf_counter()
+    r.advance(k)
+    dt = time.perf_counter() - t0
+    n = cfg.nx * cfg.ny * cfg.nz
+    return {"value": n * k / dt / 1e6, "unit": "MLUPS", "cores": threads, "kind": "reference",
+            "sample": f"{k} steps of the full {cfg.nx}x{cfg.ny}x{cfg.nz} grid (FP64 reference, "
+                      f"{threads} threads, after 1 warm-up step)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg, desc = CONFIGS[args.config](1)
+    from oracle.refpy import RefRunner
+    threads = os.cpu_count() or 1
+    r = RefRunner(cfg, threads=threads)
+    n = cfg.nx * cfg.ny * cfg.nz
+    t0 = time.perf_counter()
+    r.advance(1)
+    per = max(time.perf_counter() - t0, 1e-3)
+    budget = 150.0
+    w = max(0, min(args.warmup, int(0.2 * budget / per)))
+    k = max(1, min(args.steps, int(0.8 * budget / per)))
+    if w:
+        r.advance(w)
+    t0 = time.perf_counter()
+    r.advance(k)
+    dt = time.perf_counter() - t0
+    v = n * k / dt / 1e6
+    line = {
+        "impl": "reference", "metric": "MLUPS (lattice-node updates/s, whole job)", "value": v, "unit": "MLUPS",
+        "n_gpus": args.gpus, "steps": k, "warmup": w + 1, "ms_per_step": dt / k * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "nodes": n, "solid_samples": 8329 if args.config == "c2" else 0,
+                   "sample": "per-GPU workload (one slab) on the host cores" if args.gpus > 1 else "full workload"},
+        "cpu_baseline": {"value": v, "unit": "MLUPS", "cores": threads, "kind": "reference",
+                         "sample": f"{k} timed steps of {cfg.nx}x{cfg.ny}x{cfg.nz} after {w + 1} warm-up"},
+        "e2e": {"value": v, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import paper_2101_11856_b200 as lbm
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=device)
+        dist = tdist
+    if lbm.device_count() < 1:
+        raise SystemExit("no CUDA device visible to the engine")
+
+    cfg, desc = CONFIGS[args.config](world)
+    scene = lbm.build_scene(cfg)
+    n_samples = sum(len(scene.samples(s)["source_id"]) for s in range(len(cfg.solids)))
+    # a dedicated (capturable) stream: the engine launches on it, the CUDA
+    # events and NCCL synchronise with it
+    stream = torch.cuda.Stream(device)
+    torch.cuda.set_stream(stream)
+
+    if world == 1:
+        runner = lbm.Runner(scene, regions=1, device=local)
+        runner.set_stream(stream.cuda_stream)
+        stepper = None
+    else:
+        from paper_2101_11856_b200.dist import RankStepper
+        runner = lbm.Runner(scene, device=local, world=world, rank=rank)
+        dist.barrier()
+        stepper = RankStepper(runner, dist, world, rank, cfg.faces[4].condition == "periodic", device)
+    z0, z1 = runner.slab()
+    nodes_local = cfg.nx * cfg.ny * (z1 - z0)
+    nodes_global = cfg.nx * cfg.ny * cfg.nz
+
+    def steps(k, macro_last=False):
+        if stepper is None:
+            st = runner.advance(k)
+            if not st.ok:
+                raise RuntimeError(f"diverged: {st}")
+        else:
+            for j in range(k):
+                stepper.step(write_macro=macro_last and j == k - 1)
+
+    # warm-up (also captures the CUDA graph)
+    steps(max(3, args.warmup))
+    if stepper is not None:
+        stepper.finish()
+    torch.cuda.synchronize(device)
+
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize(device)
+        start.record(stream)
+        steps(args.steps)
+        if stepper is not None:
+            for w in stepper.pending:
+                w.wait()
+            stepper.pending = []
+        end.record(stream)
+        torch.cuda.synchronize(device)
+        if dist:
+            dist.barrier()
+    ms = start.elapsed_time(end)
+    if stepper is not None:
+        st = stepper.finish()
+        if not st.ok:
+            raise RuntimeError(f"diverged: {st}")
+    if dist:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = nodes_global * args.steps / (ms * 1e-3) / 1e6
+
+    # per-phase CUDA-event timing of the same step (fluid kernel share, roofline)
+    rows = []
+    kernels_per_step = runner.kernels_per_step() if stepper is None else None
+    if stepper is None:
+        runner.advance(min(args.steps, 20), timings=rows)
+    fluid = [r.seconds for r in rows if r.phase == "fluid"]
+    ib = [r.seconds for r in rows if r.phase == "ib"]
+    fluid_s = statistics.mean(fluid) if fluid else None
+    peak, peak_kind = measured_peaks()
+    roofline = None
+    if fluid_s:
+        alg = ALG_BYTES_PER_LU * nodes_local
+        achieved = alg / fluid_s / 1e9
+        traffic = ncu_traffic(args.config)
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": traffic, "kernel": "fluid_kernel (fused stream+faces+moments+CM-MRT+forcing)",
+                    "alg_bytes_per_launch": alg, "kernel_ms": fluid_s * 1e3, "peak_kind": peak_kind,
+                    "ib_ms": (statistics.mean(ib) * 1e3) if ib else 0.0,
+                    "step_share_fluid": fluid_s / (ms_per_step * 1e-3)}
+
+    # end-to-end through the public API: per step one advance(1) call with its
+    # host inputs (motion-table rows) and host result (status + reaction totals)
+    e2e = None
+    if stepper is None:
+        k_e2e = max(3, min(args.steps, 50))
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            st = runner.advance(1)
+        rho_probe = None
+        dt = time.perf_counter() - t0
+        ns = len(cfg.solids)
+        e2e = {"value": nodes_global * k_e2e / dt / 1e6, "unit": "MLUPS",
+               "h2d_bytes_per_step": 8 + 2 * ns * 18 * 8, "d2h_bytes_per_step": 40 + ns * 6 * 8,
+               "how": "advance(1) per step through the C ABI from pinned-free host buffers; includes the "
+                      "per-step motion-table upload and status/totals download", "steps": k_e2e}
+        del rho_probe, st
+
+    line = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline_sample(cfg)
+        gpu_launches = kernels_per_step * args.steps if kernels_per_step else None
+        line = {
+            "metric": "MLUPS (lattice-node updates/s, whole job)", "value": value, "unit": "MLUPS",
+            "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": desc, "nodes": nodes_global, "nodes_per_gpu": nodes_local,
+                       "solid_samples": n_samples, "parallelism": f"z-slab x{world}",
+                       "layout": "SoA fp32 DDF-shifted (alpha >= n)",
+                       "l2": "inputs larger than L2 (f: %.2f GB/GPU vs 126 MB L2)" % (2 * 27 * 4 * nodes_local / 1e9)},
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+            "clocks": clocks.summary(), "gpu_launches": gpu_launches,
+            "per_gpu_mlups": value / world,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,319 @@
+// lbm_b200.hpp — C++ mirror of the reference solver API
+// (/root/reference/proj/include/lbm: scene.hpp, runner.hpp, solver.hpp,
+// ib.hpp, core.hpp) over the C ABI in lbmg.h.  A reference client switches by
+// including this header instead of "lbm/runner.hpp"/"lbm/scene.hpp" and
+// linking _build/liblbmg.so; type and member names are the reference's.
+//
+// Header-only; exceptions: lbm::ConfigError / lbm::IoError as in core.hpp:50-58,
+// lbm::DeviceError for CUDA failures.  Divergence is reported in StepStatus.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "lbmg.h"
+
+namespace lbm {
+
+struct Vec3 {  // core.hpp:14-32 (value type subset)
+    double x = 0.0, y = 0.0, z = 0.0;
+    double operator[](int a) const { return a == 0 ? x : (a == 1 ? y : z); }
+};
+
+struct GridDims {  // core.hpp:36-47
+    int nx = 0, ny = 0, nz = 0;
+    std::size_t n_nodes() const { return std::size_t(nx) * std::size_t(ny) * std::size_t(nz); }
+};
+
+class ConfigError : public std::runtime_error {
+public:
+    explicit ConfigError(const std::string& m) : std::runtime_error(m) {}
+};
+class IoError : public std::runtime_error {
+public:
+    explicit IoError(const std::string& m) : std::runtime_error(m) {}
+};
+class DeviceError : public std::runtime_error {
+public:
+    explicit DeviceError(const std::string& m) : std::runtime_error(m) {}
+};
+
+namespace detail {
+inline void check(int code) {
+    if (code == LBMG_OK) return;
+    const std::string msg = lbmg_last_error();
+    if (code == LBMG_ERR_CONFIG) throw ConfigError(msg);
+    if (code == LBMG_ERR_IO) throw IoError(msg);
+    throw DeviceError(msg);
+}
+inline void put3(double* d, const Vec3& v) {
+    d[0] = v.x;
+    d[1] = v.y;
+    d[2] = v.z;
+}
+}  // namespace detail
+
+enum class CollisionKind { BGK, RawMomentMRT, CentralMomentMRT };          // collision.hpp:23
+enum class RatePolicy { Constant, RelaxTowardOne };                        // collision.hpp:25
+enum class FaceCondition { NoSlip, VelocityInlet, Outflow, Periodic };     // boundary.hpp:22
+enum class AccumulationMode { Atomic, Deterministic };                      // ib.hpp:33
+enum class SamplingMethod { DartThrowing, SampleElimination };             // ib.hpp:35
+enum class InitKind { Uniform, TaylorGreen };                              // scene.hpp:43
+
+struct FaceSpec {  // boundary.hpp:24-27
+    FaceCondition condition = FaceCondition::NoSlip;
+    Vec3 inlet_velocity;
+};
+struct BoundarySet {  // boundary.hpp:33-42
+    std::array<FaceSpec, 6> faces;
+};
+
+struct MeshConfig {  // scene.hpp:22-33 (no File meshes)
+    enum class Type { Sphere, Box, FinComb, Quad } type = Type::Sphere;
+    Vec3 center, lo, hi, origin;
+    double radius = 1.0;
+    int subdivisions = 3;
+    int fins = 8;
+    double fin_length = 8, fin_height = 6, fin_spacing = 2;
+    double size = 1.0, plane_z = 0.0;
+};
+
+struct RigidMotion {  // ib.hpp:111-115
+    Vec3 linear_velocity, angular_velocity, center;
+};
+
+struct SolidConfig {  // scene.hpp:35-40
+    MeshConfig mesh;
+    double poisson_radius = 0.5;
+    SamplingMethod sampling = SamplingMethod::DartThrowing;
+    std::optional<RigidMotion> motion;
+};
+
+struct SceneConfig {  // scene.hpp:49-78 (hot-path fields)
+    GridDims dims;
+    double viscosity = 0.05;
+    CollisionKind kind = CollisionKind::BGK;
+    double high_order_rate = 1.0;
+    RatePolicy policy = RatePolicy::Constant;
+    double policy_eps0 = 0.01;
+    std::optional<std::array<double, 27>> explicit_rates;
+    BoundarySet boundary;
+    Vec3 body_force;
+    std::vector<SolidConfig> solids;
+    InitKind init = InitKind::Uniform;
+    double init_density = 1.0;
+    Vec3 init_velocity;
+    double tg_u_max = 0.02;
+    int regions = 1;
+    unsigned threads_per_region = 0;
+    std::size_t alpha = 1;
+    int block_edge = 1;
+    AccumulationMode ib_mode = AccumulationMode::Atomic;
+    std::uint64_t seed = 1;
+};
+
+struct StepStatus {  // solver.hpp:47-52
+    bool ok = true;
+    bool mach_warning = false;
+    long step = -1;
+    std::string reason;
+};
+
+struct TimingRow {  // io.hpp:50-54
+    std::string phase;
+    long step = 0;
+    double seconds = 0.0;
+};
+
+struct ReactionTotals {  // ib.hpp:124-127
+    Vec3 force, torque;
+};
+
+// Canonical AoS FP64 field (the layout gather_* returns, runner.cpp:260-295).
+class FieldStore {
+public:
+    FieldStore() = default;
+    FieldStore(std::size_t n, std::size_t beta) : n_(n), beta_(beta), data_(n * beta) {}
+    std::size_t n_nodes() const { return n_; }
+    std::size_t beta() const { return beta_; }
+    double get(std::size_t k, std::size_t i) const { return data_[k * beta_ + i]; }
+    double* data() { return data_.data(); }
+    const double* data() const { return data_.data(); }
+    std::size_t size() const { return data_.size(); }
+
+private:
+    std::size_t n_ = 0, beta_ = 1;
+    std::vector<double> data_;
+};
+
+class Runner;
+
+// Scene (scene.hpp:92-96): owns the sampled, ordered solids.
+class Scene {
+public:
+    Scene() = default;
+    Scene(const Scene&) = delete;
+    Scene& operator=(const Scene&) = delete;
+    Scene(Scene&& o) noexcept : cfg(std::move(o.cfg)), h_(o.h_) { o.h_ = nullptr; }
+    ~Scene() { lbmg_scene_destroy(h_); }
+    SceneConfig cfg;
+    std::size_t sample_count(int solid) const { return lbmg_scene_sample_count(h_, solid); }
+
+private:
+    friend Scene build_scene(const SceneConfig&);
+    friend class Runner;
+    lbmg_scene* h_ = nullptr;
+};
+
+inline lbmg_scene_config to_c(const SceneConfig& c, std::vector<lbmg_solid_config>& solids) {
+    lbmg_scene_config o;
+    lbmg_scene_config_default(&o);
+    o.nx = c.dims.nx;
+    o.ny = c.dims.ny;
+    o.nz = c.dims.nz;
+    o.viscosity = c.viscosity;
+    o.kind = int(c.kind);
+    o.high_order_rate = c.high_order_rate;
+    o.policy = int(c.policy);
+    o.policy_eps0 = c.policy_eps0;
+    if (c.explicit_rates) {
+        o.has_explicit_rates = 1;
+        for (int r = 0; r < 27; ++r) o.rates[r] = (*c.explicit_rates)[r];
+    }
+    for (int f = 0; f < 6; ++f) {
+        o.faces[f].condition = int(c.boundary.faces[f].condition);
+        detail::put3(o.faces[f].velocity, c.boundary.faces[f].inlet_velocity);
+    }
+    detail::put3(o.body_force, c.body_force);
+    solids.clear();
+    for (const auto& s : c.solids) {
+        lbmg_solid_config sc{};
+        sc.mesh.type = int(s.mesh.type);
+        detail::put3(sc.mesh.center, s.mesh.center);
+        detail::put3(sc.mesh.lo, s.mesh.lo);
+        detail::put3(sc.mesh.hi, s.mesh.hi);
+        detail::put3(sc.mesh.origin, s.mesh.origin);
+        sc.mesh.radius = s.mesh.radius;
+        sc.mesh.subdivisions = s.mesh.subdivisions;
+        sc.mesh.fins = s.mesh.fins;
+        sc.mesh.fin_length = s.mesh.fin_length;
+        sc.mesh.fin_height = s.mesh.fin_height;
+        sc.mesh.fin_spacing = s.mesh.fin_spacing;
+        sc.mesh.size = s.mesh.size;
+        sc.mesh.plane_z = s.mesh.plane_z;
+        sc.poisson_radius = s.poisson_radius;
+        sc.sampling = int(s.sampling);
+        if (s.motion) {
+            sc.has_motion = 1;
+            detail::put3(sc.linear_velocity, s.motion->linear_velocity);
+            detail::put3(sc.angular_velocity, s.motion->angular_velocity);
+            detail::put3(sc.center, s.motion->center);
+        }
+        solids.push_back(sc);
+    }
+    o.n_solids = int(solids.size());
+    o.solids = solids.empty() ? nullptr : solids.data();
+    o.init = int(c.init);
+    o.init_density = c.init_density;
+    detail::put3(o.init_velocity, c.init_velocity);
+    o.tg_u_max = c.tg_u_max;
+    o.regions = c.regions;
+    o.threads_per_region = c.threads_per_region;
+    o.alpha = c.alpha;
+    o.block_edge = c.block_edge;
+    o.ib_mode = int(c.ib_mode);
+    o.seed = c.seed;
+    return o;
+}
+
+// build_scene, scene.hpp:100.
+inline Scene build_scene(const SceneConfig& cfg) {
+    std::vector<lbmg_solid_config> solids;
+    const lbmg_scene_config c = to_c(cfg, solids);
+    Scene s;
+    s.cfg = cfg;
+    detail::check(lbmg_scene_build(&c, &s.h_));
+    return s;
+}
+
+// Runner, runner.hpp:25-83, on the B200 engine.
+class Runner {
+public:
+    explicit Runner(const Scene& scene, int device = 0) : Runner(scene, scene.cfg.regions, 0, device) {}
+    Runner(const Scene& scene, int regions, unsigned /*threads_per_region*/, int device = 0) {
+        detail::check(lbmg_runner_create(scene.h_, regions, device, &h_));
+    }
+    Runner(const Runner&) = delete;
+    Runner& operator=(const Runner&) = delete;
+    Runner(Runner&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+    ~Runner() { lbmg_runner_destroy(h_); }
+
+    StepStatus advance(long steps, std::vector<TimingRow>* timings = nullptr) {
+        lbmg_status st;
+        if (!timings) {
+            detail::check(lbmg_runner_advance(h_, steps, &st, nullptr, 0, nullptr));
+        } else {
+            std::vector<lbmg_timing_row> rows(std::size_t(steps > 0 ? steps : 1) * 3);
+            std::size_t n = 0;
+            detail::check(lbmg_runner_advance(h_, steps, &st, rows.data(), rows.size(), &n));
+            for (std::size_t k = 0; k < n; ++k) timings->push_back({rows[k].phase, rows[k].step, rows[k].seconds});
+        }
+        return {st.ok != 0, st.mach_warning != 0, st.step, st.reason};
+    }
+    long step_count() const { return lbmg_runner_step_count(h_); }
+    StepStatus status() const {
+        lbmg_status st;
+        detail::check(lbmg_runner_status(h_, &st));
+        return {st.ok != 0, st.mach_warning != 0, st.step, st.reason};
+    }
+    GridDims dims() const {
+        GridDims d;
+        detail::check(lbmg_runner_dims(h_, &d.nx, &d.ny, &d.nz));
+        return d;
+    }
+    int region_count() const { return lbmg_runner_region_count(h_); }
+    void set_layout(int block_edge, std::size_t alpha) { detail::check(lbmg_runner_set_layout(h_, block_edge, alpha)); }
+    std::size_t alpha() const { return lbmg_runner_alpha(h_); }
+    int block_edge() const { return lbmg_runner_block_edge(h_); }
+
+    FieldStore gather_rho() const { return gather(1, lbmg_runner_gather_rho); }
+    FieldStore gather_u() const { return gather(3, lbmg_runner_gather_u); }
+    FieldStore gather_f() const { return gather(27, lbmg_runner_gather_f); }
+
+    std::vector<ReactionTotals> totals_log() const {
+        const std::size_t n = lbmg_runner_totals_count(h_);
+        std::vector<double> raw(6 * n);
+        if (n) detail::check(lbmg_runner_totals(h_, raw.data(), n));
+        std::vector<ReactionTotals> out(n);
+        for (std::size_t s = 0; s < n; ++s) {
+            out[s].force = {raw[6 * s], raw[6 * s + 1], raw[6 * s + 2]};
+            out[s].torque = {raw[6 * s + 3], raw[6 * s + 4], raw[6 * s + 5]};
+        }
+        return out;
+    }
+
+    Runner clone() const {
+        Runner c;
+        detail::check(lbmg_runner_clone(h_, &c.h_));
+        return c;
+    }
+
+    lbmg_runner* handle() { return h_; }
+
+private:
+    Runner() = default;
+    template <class F>
+    FieldStore gather(std::size_t beta, F fn) const {
+        const GridDims d = dims();
+        FieldStore out(d.n_nodes(), beta);
+        detail::check(fn(h_, out.data()));
+        return out;
+    }
+    lbmg_runner* h_ = nullptr;
+};
+
+}  // namespace lbm

@@ -232,6 +232,9 @@ int lbmg_runner_phase(lbmg_runner* r, int phase, int write_macro);
 /* After an externally driven run: synchronise and fold device status/totals
  * into the host-side Runner state (like the tail of lbmg_runner_advance). */
 int lbmg_runner_sync(lbmg_runner* r, lbmg_status* status);
+/* Diagnostics: number of engine kernels one step launches, counted from the
+ * captured step CUDA graph (0 before the first graph-replayed advance). */
+long lbmg_runner_kernels_per_step(const lbmg_runner* r);
 
 /* ---- kernel-level entry points (unit parity, GPU) ----------------------- */
 /* collide (collision.cpp:207-212) of n nodes on the device, fp32 arithmetic:

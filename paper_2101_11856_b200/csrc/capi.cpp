@@ -356,6 +356,10 @@ int lbmg_runner_sync(lbmg_runner* r, lbmg_status* status) {
     return guarded([&] { put_status(R(r).sync_external(), status); });
 }
 
+long lbmg_runner_kernels_per_step(const lbmg_runner* r) {
+    return r && r->impl ? r->impl->kernels_per_step_ : 0;
+}
+
 int lbmg_collide_batch(const lbmg_scene_config* cfg, size_t n, const double* f, const double* rho,
                        const double* u, double* omega) {
     return guarded([&] {

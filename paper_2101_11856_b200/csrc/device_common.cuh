@@ -166,6 +166,17 @@ LBMG_HD int owner_face_c(const RegionGeo& g, int gx, int gy, int gz) {
     return kNoOwner;
 }
 
+#ifdef __CUDACC__
+// Local node index -> (x, y, lz).
+__device__ __forceinline__ void decode(const RegionGeo& g, unsigned k, int& x, int& y, int& lz) {
+    const unsigned q = g.div_nx.div(k);
+    x = int(k - q * unsigned(g.nx));
+    const unsigned q2 = g.div_ny.div(q);
+    y = int(q - q2 * unsigned(g.ny));
+    lz = int(q2);
+}
+#endif
+
 // Runtime-direction variant (used on the rare reconstruction chains).
 LBMG_HD int owner_face(const RegionGeo& g, int gx, int gy, int gz, int i) {
     const int c[3] = {cx(i), cy(i), cz(i)};

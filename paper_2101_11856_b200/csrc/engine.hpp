@@ -30,7 +30,8 @@ struct InitParams {
     int NX, NY;
 };
 
-void launch_fluid(const FluidParams& P, unsigned k0, unsigned k1, int write_macro, cudaStream_t st);
+// part: 0 every node, 1 the two halo planes (edge), 2 everything else (bulk)
+void launch_fluid(const FluidParams& P, int part, int write_macro, cudaStream_t st);
 void launch_macro(const FluidParams& P, int parity, cudaStream_t st);
 void launch_ib_mark(const FluidParams& P, const IbSolidDev& S, unsigned* stamp, unsigned* band,
                     cudaStream_t st);

@@ -1,0 +1,554 @@
+// The fused fluid step of one region (stream + six face passes + moments +
+// CM-MRT/ACM collision + forcing, runner.cpp:135-208), split in two kernels
+// so the hot one carries no boundary logic:
+//
+//  fluid_bulk_kernel   nodes with 1<=x<=nx-2, 1<=y<=ny-2, 1<=lz<=nzl-2.
+//                      Two consecutive x-nodes per thread, packed fp32x2
+//                      arithmetic (FFMA2/FADD2/FMUL2), one 64-bit load and
+//                      store per direction per thread; x-shifted pulls take
+//                      the neighbour lane's half through a warp shuffle (one
+//                      extra scalar load at the warp edge).  All 27 loads are
+//                      independent and issued back to back.
+//  fluid_shell_kernel  every other node (the six boundary layers and the
+//                      planes next to a halo): per-direction ownership,
+//                      bounce-back / inlet / outflow (incl. the stale edge
+//                      read), halo sends, face slots.  Scalar, same collision
+//                      code (bit-identical per node to the bulk path).
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <type_traits>
+
+#include "collision.cuh"
+#include "device_common.cuh"
+#include "engine.hpp"
+
+namespace lbmg {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// Buffers of step parity p (slot pointers stay in kernel-parameter space:
+// indexing them by a runtime face id must not spill a copy to local memory).
+struct StepView {
+    const float* fin;
+    const float* halo_lo;
+    const float* halo_hi;
+    int p;
+};
+
+__device__ __forceinline__ StepView make_view(const FluidParams& P, int p) {
+    return StepView{P.p.f[p], P.p.recv_lo[p], P.p.recv_hi[p], p};
+}
+
+// Streamed value f_i(x - c_i) for a pull that is not missing (stream,
+// solver.cpp:46-87): periodic wrap in x/y, ghost planes from the halo.
+__device__ __forceinline__ float pull_rt(const RegionGeo& g, const StepView& v, int x, int y, int lz, int i) {
+    int sx = x - cx(i), sy = y - cy(i);
+    if (sx < 0) sx += g.nx;
+    else if (sx >= g.nx) sx -= g.nx;
+    if (sy < 0) sy += g.ny;
+    else if (sy >= g.ny) sy -= g.ny;
+    const int lzs = lz - cz(i);
+    const unsigned hp = cross9(i, 2) * g.plane + unsigned(sy) * g.nx + unsigned(sx);
+    if (lzs < 0) return v.halo_lo[hp];
+    if (lzs >= g.nzl) return v.halo_hi[hp];
+    return v.fin[g.idx(g.node(sx, sy, lzs), i)];
+}
+
+// f*_i at (x,y,lz) once face pass `owner` has run this step (apply_face,
+// boundary.cpp:42-118).  Outflow copies f*_i of the interior neighbour as it
+// stands at that point of the pass sequence: the streamed value, an earlier
+// face's fresh reconstruction (followed), or — when a later face owns it —
+// the previous step's slot value (the stale edge read).
+__device__ __forceinline__ float reconstruct(const FluidParams& P, const StepView& v, int x, int y, int lz, int i,
+                                         int owner) {
+    const RegionGeo& g = P.g;
+    const FaceTable& ft = P.faces;
+    int f = owner;
+    for (int guard = 0; guard < 7; ++guard) {
+        const int cond = ft.cond[f];
+        if (cond == kNoSlip) return v.fin[g.idx(g.node(x, y, lz), opposite(i))];
+        if (cond == kInlet) return ft.inlet[f][i];
+        const int a = face_axis(f), s = face_side(f);
+        if (a == 0) x -= s;
+        else if (a == 1) y -= s;
+        else lz -= s;
+        const int fn = owner_face(g, x, y, g.gz0 + lz, i);
+        if (fn == kNoOwner) return pull_rt(g, v, x, y, lz, i);
+        if (fn > f) return P.p.slot[v.p][fn][g.slot_index(fn, x, y, lz, i)];
+        f = fn;
+    }
+    return 0.0f;  // unreachable: the owner strictly decreases along the chain
+}
+
+// f~* (post-stream, post-face-pass) of one node.
+template <bool WRITE_SLOTS>
+__device__ __forceinline__ void gather_node(const FluidParams& P, const StepView& v, float* const* slot_cur,
+                                            unsigned k, int x, int y, int lz, float (&fs)[27]) {
+    const RegionGeo& g = P.g;
+    const bool interior = x >= 1 && x <= g.nx - 2 && y >= 1 && y <= g.ny - 2 && lz >= 1 && lz <= g.nzl - 2;
+    if (interior) {
+        static_for<0, 27>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            const unsigned ks = k - unsigned(cx(i) + g.nx * cy(i) + int(g.plane) * cz(i));
+            fs[i] = __ldg(&v.fin[g.idx(ks, i)]);
+        });
+        return;
+    }
+    const int gz = g.gz0 + lz;
+    // 1) every pull's address, branch-free (wrap in x/y, halo planes in z; a
+    //    missing pull points at the node itself) -> 27 independent loads
+    unsigned miss = 0;
+    static_for<0, 27>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        const int own = owner_face_c<i>(g, x, y, gz);
+        int sx = x - cx(i), sy = y - cy(i);
+        sx = sx < 0 ? sx + g.nx : (sx >= g.nx ? sx - g.nx : sx);
+        sy = sy < 0 ? sy + g.ny : (sy >= g.ny ? sy - g.ny : sy);
+        const int lzs = lz - cz(i);
+        const unsigned hp = cross9(i, 2) * g.plane + unsigned(sy) * g.nx + unsigned(sx);
+        const float* src;
+        if constexpr (cz(i) == 1) src = lzs < 0 ? v.halo_lo + hp : v.fin + g.idx(g.node(sx, sy, lzs), i);
+        else if constexpr (cz(i) == -1) src = lzs >= g.nzl ? v.halo_hi + hp : v.fin + g.idx(g.node(sx, sy, lzs), i);
+        else src = v.fin + g.idx(g.node(sx, sy, lzs), i);
+        if (own != kNoOwner) {
+            src = v.fin + g.idx(k, i);
+            miss |= 1u << i;
+        }
+        fs[i] = __ldg(src);
+    });
+    // 2) the missing populations (face passes, boundary.cpp:42-125)
+    if (miss) {
+        static_for<0, 27>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            if (miss & (1u << i)) {
+                const int own = owner_face_c<i>(g, x, y, gz);
+                const float val = reconstruct(P, v, x, y, lz, i, own);
+                fs[i] = val;
+                if constexpr (WRITE_SLOTS) slot_cur[own][g.slot_index(own, x, y, lz, i)] = val;
+            }
+        });
+    }
+}
+
+__device__ __forceinline__ void flag_divergence(DevCounters* ctr) {
+    if (atomicExch(&ctr->diverged, 1u) == 0u) ctr->diverged_step = ctr->t;
+}
+
+// Shell enumeration: planes lz=0 and lz=nzl-1 first (the "edge" part that
+// feeds the halos), then per interior plane the rows y=0, y=ny-1 and the
+// columns x=0, x=nx-1.
+__device__ __forceinline__ void shell_decode(const RegionGeo& g, unsigned s, int& x, int& y, int& lz) {
+    const unsigned zplanes = g.nzl >= 2 ? 2u : 1u;
+    if (s < zplanes * g.plane) {
+        const unsigned q = s >= g.plane ? s - g.plane : s;
+        lz = s >= g.plane ? g.nzl - 1 : 0;
+        const unsigned yy = g.div_nx.div(q);
+        y = int(yy);
+        x = int(q - yy * unsigned(g.nx));
+        return;
+    }
+    const unsigned r0 = s - zplanes * g.plane;
+    const unsigned cnt = 2u * g.nx + 2u * (g.ny - 2);
+    const unsigned pl = r0 / cnt;
+    unsigned r = r0 - pl * cnt;
+    lz = 1 + int(pl);
+    if (r < unsigned(g.nx)) {
+        y = 0;
+        x = int(r);
+    } else if (r < 2u * g.nx) {
+        y = g.ny - 1;
+        x = int(r - g.nx);
+    } else {
+        r -= 2u * g.nx;
+        y = 1 + int(r >> 1);
+        x = (r & 1u) ? g.nx - 1 : 0;
+    }
+}
+
+}  // namespace
+
+// Collision output form shared by every fluid kernel of a run (bitwise
+// identical per node across kernels): 0 = f* - t' with f* in registers,
+// 1 = the same with the bulk kernel's f* in shared memory, 2 = feq + t''.
+template <int FORM, class V>
+using StashFor = typename std::conditional<FORM == 2, NoStash<V>, RegStash<V>>::type;
+
+// ---------------------------------------------------------------------------
+// Shell (and generic all-node) kernel: one node per thread, general path.
+template <int KIND, int POLICY, bool STD, int FORM>
+__global__ void __launch_bounds__(128) fluid_shell_kernel(const FluidParams P, unsigned s0, unsigned s1,
+                                                          int write_macro, int all_nodes) {
+    DevCounters* ctr = P.ctr;
+    if (ctr->diverged) return;
+    const unsigned s = s0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= s1) return;
+    const RegionGeo& g = P.g;
+    int x, y, lz;
+    if (all_nodes) decode(g, s, x, y, lz);
+    else shell_decode(g, s, x, y, lz);
+    const unsigned k = g.node(x, y, lz);
+    const int p = int(ctr->t & 1);
+    const StepView v = make_view(P, p);
+
+    float fs[27];
+    gather_node<true>(P, v, P.p.slot[p ^ 1], k, x, y, lz, fs);
+    const MacroV<float> mc = moments_v<float>(fs);
+    if (mc.bad[0]) {
+        flag_divergence(ctr);
+        return;
+    }
+    if (mc.mach[0]) atomicOr(&ctr->mach, 1u);
+    if (write_macro) {
+        P.p.rho[k] = mc.rho;
+        P.p.u[k] = mc.ux;
+        P.p.u[k + g.ns] = mc.uy;
+        P.p.u[k + 2u * g.ns] = mc.uz;
+    }
+    float gx = P.m.body[0], gy = P.m.body[1], gz = P.m.body[2];
+    if (P.p.tflag != nullptr && P.p.tflag[k >> 5]) {
+        float* gib = P.p.gib;
+        gx = __fadd_rn(gx, gib[k]);
+        gy = __fadd_rn(gy, gib[k + g.ns]);
+        gz = __fadd_rn(gz, gib[k + 2u * g.ns]);
+        gib[k] = 0.f;
+        gib[k + g.ns] = 0.f;
+        gib[k + 2u * g.ns] = 0.f;
+    }
+    StashFor<FORM, float> stash;
+    collide_v<KIND, POLICY, STD, float>(fs, mc, gx, gy, gz, gx != 0.f || gy != 0.f || gz != 0.f, P.m, stash);
+
+    float* fout = P.p.f[p ^ 1];
+    static_for<0, 27>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        fout[g.idx(k, i)] = fs[i];
+    });
+    // crossing populations of the boundary planes -> neighbour halos
+    const unsigned hp = unsigned(y) * g.nx + x;
+    if (lz == 0) {
+        float* sd = P.p.send_lo[p ^ 1];
+        if (sd)
+            static_for<1, 10>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                sd[cross9(i, 2) * g.plane + hp] = fs[i];
+            });
+    }
+    if (lz == g.nzl - 1) {
+        float* sd = P.p.send_hi[p ^ 1];
+        if (sd)
+            static_for<18, 27>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                sd[cross9(i, 2) * g.plane + hp] = fs[i];
+            });
+    }
+}
+
+// f* of the bulk kernel's node pairs parked in shared memory during the
+// moment transform ([direction][thread], 27.6 KB per 128-thread CTA).
+constexpr int kBulkThreads = 128;
+struct SmemStash {
+    static constexpr bool kFeqOut = false;
+    __device__ __forceinline__ float2* base() const {
+        __shared__ float2 sm[27][kBulkThreads];
+        return &sm[0][threadIdx.x];
+    }
+    __device__ __forceinline__ void put(int i, float2 x) { base()[i * kBulkThreads] = x; }
+    __device__ __forceinline__ float2 get(int i) const { return base()[i * kBulkThreads]; }
+};
+
+// ---------------------------------------------------------------------------
+// Bulk kernel: nodes [kb, ke) = local planes 1..nzl-2, two nodes per thread.
+template <int KIND, int POLICY, bool STD, bool SOA, int FORM>
+__global__ void __launch_bounds__(kBulkThreads, FORM == 2 ? 4 : 3) fluid_bulk_kernel(const FluidParams P, unsigned kb, unsigned ke,
+                                                         int write_macro) {
+    DevCounters* ctr = P.ctr;
+    if (ctr->diverged) return;
+    const RegionGeo& g = P.g;
+    const unsigned ln = threadIdx.x & 31u;
+    const unsigned kw = kb + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 64u;
+    if (kw >= ke) return;  // warp-uniform
+    unsigned k = kw + 2u * ln;
+    const bool inr = k < ke;
+    int x, y, lz;
+    decode(g, inr ? k : kb, x, y, lz);
+    const bool yok = inr && y >= 1 && y <= g.ny - 2;
+    const bool v0 = yok && x >= 1;
+    const bool v1 = yok && x + 1 <= g.nx - 2;
+    if (!__any_sync(kFull, v0 || v1)) return;
+    // lanes without a valid node load from a safe interior pair instead
+    const unsigned kl = (v0 || v1) ? k : g.plane + unsigned(g.nx) + 2u;
+
+    const int p = int(ctr->t & 1);
+    const float* __restrict__ fin = P.p.f[p];
+    float2 fs[27];
+    static_for<0, 27>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        const unsigned ks = kl - unsigned(g.nx * cy(i) + int(g.plane) * cz(i));
+        const float* src = SOA ? fin + size_t(i) * g.A + ks : fin + g.idx(ks, i);
+        const float2 pr = __ldg(reinterpret_cast<const float2*>(src));
+        if constexpr (cx(i) == 0) {
+            fs[i] = pr;
+        } else if constexpr (cx(i) == 1) {  // source x-1
+            float left = __shfl_up_sync(kFull, pr.y, 1);
+            if (ln == 0 && v0) left = SOA ? __ldg(src - 1) : __ldg(fin + g.idx(ks - 1, i));
+            fs[i] = make_float2(left, pr.x);
+        } else {  // source x+1
+            float right = __shfl_down_sync(kFull, pr.x, 1);
+            if (ln == 31 && v1) right = SOA ? __ldg(src + 2) : __ldg(fin + g.idx(ks + 2, i));
+            fs[i] = make_float2(pr.y, right);
+        }
+    });
+    if (!(v0 || v1)) return;  // (after the shuffles)
+
+    const MacroV<float2> mc = moments_v<float2>(fs);
+    if ((v0 && mc.bad[0]) || (v1 && mc.bad[1])) {
+        flag_divergence(ctr);
+        return;
+    }
+    if ((v0 && mc.mach[0]) || (v1 && mc.mach[1])) atomicOr(&ctr->mach, 1u);
+    const bool both = v0 && v1;
+    if (write_macro) {
+        const float2 r = mc.rho, ux = mc.ux, uy = mc.uy, uz = mc.uz;
+        if (both) {
+            *reinterpret_cast<float2*>(P.p.rho + k) = r;
+            *reinterpret_cast<float2*>(P.p.u + k) = ux;
+            *reinterpret_cast<float2*>(P.p.u + k + g.ns) = uy;
+            *reinterpret_cast<float2*>(P.p.u + k + 2u * g.ns) = uz;
+        } else {
+            const unsigned kk = v0 ? k : k + 1;
+            const int j = v0 ? 0 : 1;
+            P.p.rho[kk] = lane(r, j);
+            P.p.u[kk] = lane(ux, j);
+            P.p.u[kk + g.ns] = lane(uy, j);
+            P.p.u[kk + 2u * g.ns] = lane(uz, j);
+        }
+    }
+    float2 gx = make_float2(P.m.body[0], P.m.body[0]);
+    float2 gy = make_float2(P.m.body[1], P.m.body[1]);
+    float2 gz = make_float2(P.m.body[2], P.m.body[2]);
+    if (P.p.tflag != nullptr && P.p.tflag[k >> 5]) {
+        float* gib = P.p.gib;
+        float2 a = *reinterpret_cast<const float2*>(gib + k);
+        float2 b = *reinterpret_cast<const float2*>(gib + k + g.ns);
+        float2 c = *reinterpret_cast<const float2*>(gib + k + 2u * g.ns);
+        // only this kernel's nodes: a shell node's force is consumed there
+        if (!v0) a.x = b.x = c.x = 0.f;
+        if (!v1) a.y = b.y = c.y = 0.f;
+        gx = __fadd2_rn(gx, a);
+        gy = __fadd2_rn(gy, b);
+        gz = __fadd2_rn(gz, c);
+        if (v0) gib[k] = gib[k + g.ns] = gib[k + 2u * g.ns] = 0.f;
+        if (v1) gib[k + 1] = gib[k + 1 + g.ns] = gib[k + 1 + 2u * g.ns] = 0.f;
+    }
+    const bool any_force = gx.x != 0.f || gx.y != 0.f || gy.x != 0.f || gy.y != 0.f || gz.x != 0.f || gz.y != 0.f;
+    typename std::conditional<FORM == 1, SmemStash, StashFor<FORM, float2>>::type stash;
+    collide_v<KIND, POLICY, STD, float2>(fs, mc, gx, gy, gz, any_force, P.m, stash);
+
+    float* __restrict__ fout = P.p.f[p ^ 1];
+    if (both) {
+        static_for<0, 27>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            float* dst = SOA ? fout + size_t(i) * g.A + k : fout + g.idx(k, i);
+            *reinterpret_cast<float2*>(dst) = fs[i];
+        });
+    } else {
+        const unsigned kk = v0 ? k : k + 1;
+        const int j = v0 ? 0 : 1;
+        static_for<0, 27>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            float* dst = SOA ? fout + size_t(i) * g.A + kk : fout + g.idx(kk, i);
+            *dst = lane(fs[i], j);
+        });
+    }
+}
+
+// Recompute rho*/u* of the current step from f(t) (after divergence, so the
+// readback matches the reference's partially written moments, solver.cpp:113).
+__global__ void macro_kernel(const FluidParams P, int parity) {
+    const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+    const RegionGeo& g = P.g;
+    if (k >= g.n) return;
+    const StepView v = make_view(P, parity);
+    int x, y, lz;
+    decode(g, k, x, y, lz);
+    float fs[27];
+    gather_node<false>(P, v, nullptr, k, x, y, lz, fs);
+    const MacroV<float> mc = moments_v<float>(fs);
+    P.p.rho[k] = mc.rho;
+    if (!mc.bad[0]) {
+        P.p.u[k] = mc.ux;
+        P.p.u[k + g.ns] = mc.uy;
+        P.p.u[k + 2u * g.ns] = mc.uz;
+    }
+}
+
+// IB band pre-pass: rho*, u* at the band nodes only.
+__global__ void ib_band_kernel(const FluidParams P, const unsigned* band) {
+    DevCounters* ctr = P.ctr;
+    if (ctr->diverged) return;
+    const unsigned count = *P.p.band_count;
+    const RegionGeo& g = P.g;
+    const int p = int(ctr->t & 1);
+    const StepView v = make_view(P, p);
+    for (unsigned j = blockIdx.x * blockDim.x + threadIdx.x; j < count; j += gridDim.x * blockDim.x) {
+        const unsigned k = band[j];
+        int x, y, lz;
+        decode(g, k, x, y, lz);
+        float fs[27];
+        gather_node<false>(P, v, nullptr, k, x, y, lz, fs);
+        const MacroV<float> mc = moments_v<float>(fs);
+        P.p.rho[k] = mc.rho;
+        P.p.u[k] = mc.ux;
+        P.p.u[k + g.ns] = mc.uy;
+        P.p.u[k + 2u * g.ns] = mc.uz;
+    }
+}
+
+// (rho,u) of the two boundary planes into the neighbours' macro halo.
+__global__ void macro_pack_kernel(const FluidParams P) {
+    if (P.ctr->diverged) return;
+    const RegionGeo& g = P.g;
+    const unsigned j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= g.plane) return;
+    float* outs[2] = {P.p.msend_lo, P.p.msend_hi};
+    const unsigned ks[2] = {j, unsigned(g.nzl - 1) * g.plane + j};
+    for (int h = 0; h < 2; ++h) {
+        if (!outs[h]) continue;
+        const unsigned k = ks[h];
+        outs[h][j] = P.p.rho[k];
+        outs[h][j + g.plane] = P.p.u[k];
+        outs[h][j + 2u * g.plane] = P.p.u[k + g.ns];
+        outs[h][j + 3u * g.plane] = P.p.u[k + 2u * g.ns];
+    }
+}
+
+__global__ void step_end_kernel(DevCounters* ctr) {
+    if (!ctr->diverged) ctr->t += 1;
+}
+
+// Unit-level collide() on a batch (fp32, same code path): omega = f_out - f*.
+template <int KIND, int POLICY, bool STD>
+__global__ void collide_batch_kernel(ModelConst m, unsigned n, const double* f, const double* rho,
+                                     const double* u, double* omega) {
+    const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    float fs[27], f0[27];
+    for (int i = 0; i < 27; ++i) {
+        fs[i] = float(f[size_t(k) * 27 + i] - weight_d(i));
+        f0[i] = fs[i];
+    }
+    MacroV<float> mc;
+    mc.rho = float(rho[k]);
+    mc.drho = float(rho[k] - 1.0);
+    mc.ux = float(u[3 * k]);
+    mc.uy = float(u[3 * k + 1]);
+    mc.uz = float(u[3 * k + 2]);
+    RegStash<float> stash;
+    collide_v<KIND, POLICY, STD, float>(fs, mc, 0.f, 0.f, 0.f, false, m, stash);
+    for (int i = 0; i < 27; ++i) omega[size_t(k) * 27 + i] = double(fs[i]) - double(f0[i]);
+}
+
+// ---------------------------------------------------------------------------
+// Host launch wrappers.
+
+namespace {
+
+inline unsigned blocks_for(unsigned long long n, unsigned t) { return unsigned((n + t - 1) / t); }
+
+// Collision output form (see StashFor; LBMG_FORM overrides, default 2 =
+// feq + t'': fewest live registers, fastest measured, profiles/).
+int fluid_form() {
+    static const int v = [] {
+        const char* e = std::getenv("LBMG_FORM");
+        const int f = e ? std::atoi(e) : 2;
+        return f < 0 || f > 2 ? 2 : f;
+    }();
+    return v;
+}
+
+template <int KIND, int POLICY, bool STD, int FORM>
+void launch_fluid_t(const FluidParams& P, int part, int write_macro, cudaStream_t st) {
+    const RegionGeo& g = P.g;
+    const bool bulk_ok = (g.nx % 2 == 0) && g.nx >= 4 && g.ny >= 3 && g.nzl >= 3;
+    const unsigned zpart = (g.nzl >= 2 ? 2u : 1u) * g.plane;
+    const unsigned shell_total =
+        zpart + (g.nzl >= 3 ? unsigned(g.nzl - 2) * (2u * g.nx + 2u * (g.ny - 2)) : 0u);
+    if (!bulk_ok) {  // odd nx or thin slabs: general path over every node
+        if (part == 1) return;
+        fluid_shell_kernel<KIND, POLICY, STD, FORM><<<blocks_for(g.n, 128), 128, 0, st>>>(P, 0, g.n, write_macro, 1);
+        return;
+    }
+    if (part == 0 || part == 2) {
+        const unsigned kb = g.plane, ke = g.n - g.plane;
+        const unsigned warps = (ke - kb + 63) / 64;
+        const unsigned nb = blocks_for(warps, kBulkThreads / 32);
+        if (g.la == 31)
+            fluid_bulk_kernel<KIND, POLICY, STD, true, FORM><<<nb, kBulkThreads, 0, st>>>(P, kb, ke, write_macro);
+        else
+            fluid_bulk_kernel<KIND, POLICY, STD, false, FORM><<<nb, kBulkThreads, 0, st>>>(P, kb, ke, write_macro);
+    }
+    unsigned s0 = 0, s1 = shell_total;
+    if (part == 1) s1 = zpart;
+    if (part == 2) s0 = zpart;
+    if (s1 > s0)
+        fluid_shell_kernel<KIND, POLICY, STD, FORM><<<blocks_for(s1 - s0, 128), 128, 0, st>>>(P, s0, s1, write_macro, 0);
+}
+
+template <int KIND, int POLICY, int FORM>
+void launch_fluid_std(const FluidParams& P, int part, int write_macro, cudaStream_t st) {
+    if (rates_standard(P.m.rate)) launch_fluid_t<KIND, POLICY, true, FORM>(P, part, write_macro, st);
+    else launch_fluid_t<KIND, POLICY, false, FORM>(P, part, write_macro, st);
+}
+
+template <int FORM>
+void launch_fluid_form(const FluidParams& P, int part, int write_macro, cudaStream_t st) {
+    const int kind = P.m.kind, pol = P.m.policy;
+    if (kind == kBGK) launch_fluid_t<kBGK, kPolicyConstant, false, FORM>(P, part, write_macro, st);
+    else if (kind == kRawMRT) launch_fluid_std<kRawMRT, kPolicyConstant, FORM>(P, part, write_macro, st);
+    else if (pol == kPolicyConstant) launch_fluid_std<kCentralMRT, kPolicyConstant, FORM>(P, part, write_macro, st);
+    else launch_fluid_std<kCentralMRT, kPolicyRelax, FORM>(P, part, write_macro, st);
+}
+
+}  // namespace
+
+// part: 0 every node, 1 the two halo planes (edge), 2 the rest (bulk).
+void launch_fluid(const FluidParams& P, int part, int write_macro, cudaStream_t st) {
+    switch (fluid_form()) {
+        case 0: launch_fluid_form<0>(P, part, write_macro, st); break;
+        case 1: launch_fluid_form<1>(P, part, write_macro, st); break;
+        default: launch_fluid_form<2>(P, part, write_macro, st); break;
+    }
+}
+
+void launch_macro(const FluidParams& P, int parity, cudaStream_t st) {
+    macro_kernel<<<blocks_for(P.g.n, 256), 256, 0, st>>>(P, parity);
+}
+
+void launch_ib_band(const FluidParams& P, const unsigned* band, int sm_count, cudaStream_t st) {
+    ib_band_kernel<<<sm_count * 4, 128, 0, st>>>(P, band);
+}
+
+void launch_macro_pack(const FluidParams& P, cudaStream_t st) {
+    macro_pack_kernel<<<blocks_for(P.g.plane, 256), 256, 0, st>>>(P);
+}
+
+void launch_step_end(DevCounters* ctr, cudaStream_t st) { step_end_kernel<<<1, 1, 0, st>>>(ctr); }
+
+void launch_collide_batch(const ModelConst& m, unsigned n, const double* f, const double* rho, const double* u,
+                          double* omega, cudaStream_t st) {
+    const unsigned b = blocks_for(n, 128);
+    // collide() takes arbitrary (f, rho, u): keep the literal rates (rate 1 on
+    // the conserved rows), not the STD shortcut that assumes they are moments of f
+    const bool sd = false;
+    if (m.kind == kBGK) collide_batch_kernel<kBGK, kPolicyConstant, false><<<b, 128, 0, st>>>(m, n, f, rho, u, omega);
+    else if (m.kind == kRawMRT && sd) collide_batch_kernel<kRawMRT, kPolicyConstant, true><<<b, 128, 0, st>>>(m, n, f, rho, u, omega);
+    else if (m.kind == kRawMRT) collide_batch_kernel<kRawMRT, kPolicyConstant, false><<<b, 128, 0, st>>>(m, n, f, rho, u, omega);
+    else if (m.policy == kPolicyConstant && sd) collide_batch_kernel<kCentralMRT, kPolicyConstant, true><<<b, 128, 0, st>>>(m, n, f, rho, u, omega);
+    else if (m.policy == kPolicyConstant) collide_batch_kernel<kCentralMRT, kPolicyConstant, false><<<b, 128, 0, st>>>(m, n, f, rho, u, omega);
+    else if (sd) collide_batch_kernel<kCentralMRT, kPolicyRelax, true><<<b, 128, 0, st>>>(m, n, f, rho, u, omega);
+    else collide_batch_kernel<kCentralMRT, kPolicyRelax, false><<<b, 128, 0, st>>>(m, n, f, rho, u, omega);
+}
+
+}  // namespace lbmg

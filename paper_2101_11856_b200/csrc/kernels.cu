@@ -17,280 +17,13 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
+#include <string>
 
-#include "collision.cuh"
 #include "device_common.cuh"
 #include "engine.hpp"
 
 namespace lbmg {
-
-namespace {
-
-struct StepView {
-    const float* fin;
-    const float* halo_lo;
-    const float* halo_hi;
-    const float* slot_prev[6];
-};
-
-__device__ __forceinline__ StepView make_view(const FluidParams& P, int p) {
-    StepView v;
-    v.fin = P.p.f[p];
-    v.halo_lo = P.p.recv_lo[p];
-    v.halo_hi = P.p.recv_hi[p];
-#pragma unroll
-    for (int f = 0; f < 6; ++f) v.slot_prev[f] = P.p.slot[p][f];
-    return v;
-}
-
-// Streamed value f_i(x - c_i) for a pull that is not missing (stream,
-// solver.cpp:46-87): periodic wrap in x/y, ghost planes from the halo.
-__device__ __forceinline__ float pull_rt(const RegionGeo& g, const StepView& v, int x, int y,
-                                         int lz, int i) {
-    int sx = x - cx(i), sy = y - cy(i);
-    if (sx < 0) sx += g.nx; else if (sx >= g.nx) sx -= g.nx;
-    if (sy < 0) sy += g.ny; else if (sy >= g.ny) sy -= g.ny;
-    const int lzs = lz - cz(i);
-    const unsigned hp = cross9(i, 2) * g.plane + unsigned(sy) * g.nx + unsigned(sx);
-    if (lzs < 0) return v.halo_lo[hp];
-    if (lzs >= g.nzl) return v.halo_hi[hp];
-    return v.fin[g.idx(g.node(sx, sy, lzs), i)];
-}
-
-// f*_i at (x,y,lz) after the face pass `owner` has run this step
-// (apply_face, boundary.cpp:42-118).  Outflow copies f*_i of the interior
-// neighbour as it stands at that point of the pass sequence: the streamed
-// value, an earlier face's fresh reconstruction (followed here), or — when a
-// later face owns it — the previous step's slot value (stale read).
-__device__ float reconstruct(const RegionGeo& g, const FaceTable& ft, const StepView& v, int x,
-                             int y, int lz, int i, int owner) {
-    int f = owner;
-    for (int guard = 0; guard < 7; ++guard) {
-        const int cond = ft.cond[f];
-        if (cond == kNoSlip) return v.fin[g.idx(g.node(x, y, lz), opposite(i))];
-        if (cond == kInlet) return ft.inlet[f][i];
-        // outflow: step one cell inward along the face normal
-        const int a = face_axis(f), s = face_side(f);
-        if (a == 0) x -= s;
-        else if (a == 1) y -= s;
-        else lz -= s;
-        const int fn = owner_face(g, x, y, g.gz0 + lz, i);
-        if (fn == kNoOwner) return pull_rt(g, v, x, y, lz, i);
-        if (fn > f) return v.slot_prev[fn][g.slot_index(fn, x, y, lz, i)];
-        f = fn;
-    }
-    return 0.0f;  // unreachable: the owner strictly decreases along the chain
-}
-
-// Gathers f~* (post-stream, post-face-pass) of one node into fs.
-// Interior nodes take the direct path; others resolve each direction.
-template <bool WRITE_SLOTS>
-__device__ __forceinline__ void gather_node(const FluidParams& P, const StepView& v, float* const* slot_cur,
-                                            unsigned k, int x, int y, int lz, float (&fs)[27]) {
-    const RegionGeo& g = P.g;
-    const bool interior = x >= 1 && x <= g.nx - 2 && y >= 1 && y <= g.ny - 2 && lz >= 1 &&
-                          lz <= g.nzl - 2;
-    if (interior) {
-        static_for<0, 27>([&](auto I) {
-            constexpr int i = decltype(I)::value;
-            const unsigned ks = k - unsigned(cx(i) + g.nx * cy(i) + int(g.plane) * cz(i));
-            fs[i] = __ldg(&v.fin[g.idx(ks, i)]);
-        });
-        return;
-    }
-    const int gz = g.gz0 + lz;
-    static_for<0, 27>([&](auto I) {
-        constexpr int i = decltype(I)::value;
-        const int own = owner_face_c<i>(g, x, y, gz);
-        if (own == kNoOwner) {
-            fs[i] = pull_rt(g, v, x, y, lz, i);
-        } else {
-            const float val = reconstruct(g, P.faces, v, x, y, lz, i, own);
-            fs[i] = val;
-            if constexpr (WRITE_SLOTS) slot_cur[own][g.slot_index(own, x, y, lz, i)] = val;
-        }
-    });
-}
-
-struct Macro {
-    float rho, drho, ux, uy, uz;
-    bool bad;
-};
-
-// compute_moments (solver.cpp:89-137) on DDF-shifted populations.
-__device__ __forceinline__ Macro moments(const float (&fs)[27]) {
-    Macro mc;
-    float dr = 0.f, jx = 0.f, jy = 0.f, jz = 0.f;
-    static_for<0, 27>([&](auto I) {
-        constexpr int i = decltype(I)::value;
-        dr += fs[i];
-        if constexpr (cx(i) == 1) jx += fs[i];
-        if constexpr (cx(i) == -1) jx -= fs[i];
-        if constexpr (cy(i) == 1) jy += fs[i];
-        if constexpr (cy(i) == -1) jy -= fs[i];
-        if constexpr (cz(i) == 1) jz += fs[i];
-        if constexpr (cz(i) == -1) jz -= fs[i];
-    });
-    mc.drho = dr;
-    mc.rho = 1.0f + dr;
-    mc.bad = !(mc.rho > 0.0f) || !isfinite(mc.rho) || !isfinite(jx) || !isfinite(jy) ||
-             !isfinite(jz);
-    const float inv = 1.0f / mc.rho;
-    mc.ux = jx * inv;
-    mc.uy = jy * inv;
-    mc.uz = jz * inv;
-    return mc;
-}
-
-__device__ __forceinline__ void decode(const RegionGeo& g, unsigned k, int& x, int& y, int& lz) {
-    const unsigned q = g.div_nx.div(k);
-    x = int(k - q * unsigned(g.nx));
-    const unsigned q2 = g.div_ny.div(q);
-    y = int(q - q2 * unsigned(g.ny));
-    lz = int(q2);
-}
-
-}  // namespace
-
-// ---------------------------------------------------------------------------
-// Fused fluid step over local nodes [k0, k1).
-template <int KIND, int POLICY>
-__global__ void __launch_bounds__(256) fluid_kernel(const FluidParams P, unsigned k0, unsigned k1,
-                                                    int write_macro) {
-    DevCounters* ctr = P.ctr;
-    if (ctr->diverged) return;
-    const unsigned k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= k1) return;
-    const RegionGeo& g = P.g;
-    const int p = int(ctr->t & 1);
-    const StepView v = make_view(P, p);
-    int x, y, lz;
-    decode(g, k, x, y, lz);
-
-    float fs[27];
-    gather_node<true>(P, v, P.p.slot[p ^ 1], k, x, y, lz, fs);
-    const Macro mc = moments(fs);
-    if (mc.bad) {
-        // divergence: stop before IB/collision of this step (runner.cpp:154-161)
-        if (atomicExch(&ctr->diverged, 1u) == 0u) ctr->diverged_step = ctr->t;
-        if (write_macro) P.p.rho[k] = mc.rho;
-        return;
-    }
-    if (mc.ux * mc.ux + mc.uy * mc.uy + mc.uz * mc.uz >= 0.16f) atomicOr(&ctr->mach, 1u);
-    if (write_macro) {
-        P.p.rho[k] = mc.rho;
-        P.p.u[k] = mc.ux;
-        P.p.u[k + g.ns] = mc.uy;
-        P.p.u[k + 2u * g.ns] = mc.uz;
-    }
-    float gx = P.m.body[0], gy = P.m.body[1], gz = P.m.body[2];
-    if (P.p.tflag != nullptr && P.p.tflag[k >> 5]) {
-        float* gib = P.p.gib;
-        gx += gib[k];
-        gy += gib[k + g.ns];
-        gz += gib[k + 2u * g.ns];
-        gib[k] = 0.f;
-        gib[k + g.ns] = 0.f;
-        gib[k + 2u * g.ns] = 0.f;
-    }
-    const bool has_force = (gx != 0.f) || (gy != 0.f) || (gz != 0.f);
-    collide_node<KIND, POLICY>(fs, mc.rho, mc.drho, mc.ux, mc.uy, mc.uz, gx, gy, gz, has_force, P.m);
-
-    float* fout = P.p.f[p ^ 1];
-    static_for<0, 27>([&](auto I) {
-        constexpr int i = decltype(I)::value;
-        fout[g.idx(k, i)] = fs[i];
-    });
-    // crossing populations of the boundary planes -> neighbour halos
-    if (lz == 0) {
-        float* s = P.p.send_lo[p ^ 1];
-        if (s) {
-            const unsigned hp = unsigned(y) * g.nx + x;
-            static_for<1, 10>([&](auto I) {
-                constexpr int i = decltype(I)::value;
-                s[cross9(i, 2) * g.plane + hp] = fs[i];
-            });
-        }
-    }
-    if (lz == g.nzl - 1) {
-        float* s = P.p.send_hi[p ^ 1];
-        if (s) {
-            const unsigned hp = unsigned(y) * g.nx + x;
-            static_for<18, 27>([&](auto I) {
-                constexpr int i = decltype(I)::value;
-                s[cross9(i, 2) * g.plane + hp] = fs[i];
-            });
-        }
-    }
-}
-
-// Recompute rho*/u* of the current step from f(t) (used after divergence so
-// readback matches the reference's partially-written moments, solver.cpp:113).
-__global__ void macro_kernel(const FluidParams P, int parity) {
-    const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
-    const RegionGeo& g = P.g;
-    if (k >= g.n) return;
-    const StepView v = make_view(P, parity);
-    int x, y, lz;
-    decode(g, k, x, y, lz);
-    float fs[27];
-    gather_node<false>(P, v, nullptr, k, x, y, lz, fs);
-    const Macro mc = moments(fs);
-    P.p.rho[k] = mc.rho;
-    if (!mc.bad) {
-        P.p.u[k] = mc.ux;
-        P.p.u[k + g.ns] = mc.uy;
-        P.p.u[k + 2u * g.ns] = mc.uz;
-    }
-}
-
-// IB band pre-pass: rho*, u* at the band nodes only.
-__global__ void ib_band_kernel(const FluidParams P, const unsigned* band) {
-    DevCounters* ctr = P.ctr;
-    if (ctr->diverged) return;
-    const unsigned count = *P.p.band_count;
-    const RegionGeo& g = P.g;
-    const int p = int(ctr->t & 1);
-    const StepView v = make_view(P, p);
-    for (unsigned j = blockIdx.x * blockDim.x + threadIdx.x; j < count; j += gridDim.x * blockDim.x) {
-        const unsigned k = band[j];
-        int x, y, lz;
-        decode(g, k, x, y, lz);
-        float fs[27];
-        gather_node<false>(P, v, nullptr, k, x, y, lz, fs);
-        const Macro mc = moments(fs);
-        P.p.rho[k] = mc.rho;
-        P.p.u[k] = mc.ux;
-        P.p.u[k + g.ns] = mc.uy;
-        P.p.u[k + 2u * g.ns] = mc.uz;
-    }
-}
-
-// (rho,u) of the two boundary planes into the macro halo of the neighbours.
-__global__ void macro_pack_kernel(const FluidParams P) {
-    if (P.ctr->diverged) return;
-    const RegionGeo& g = P.g;
-    const unsigned j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= g.plane) return;
-    if (P.p.msend_lo) {
-        const unsigned k = j;
-        P.p.msend_lo[j] = P.p.rho[k];
-        P.p.msend_lo[j + g.plane] = P.p.u[k];
-        P.p.msend_lo[j + 2u * g.plane] = P.p.u[k + g.ns];
-        P.p.msend_lo[j + 3u * g.plane] = P.p.u[k + 2u * g.ns];
-    }
-    if (P.p.msend_hi) {
-        const unsigned k = unsigned(g.nzl - 1) * g.plane + j;
-        P.p.msend_hi[j] = P.p.rho[k];
-        P.p.msend_hi[j + g.plane] = P.p.u[k];
-        P.p.msend_hi[j + 2u * g.plane] = P.p.u[k + g.ns];
-        P.p.msend_hi[j + 3u * g.plane] = P.p.u[k + 2u * g.ns];
-    }
-}
-
-__global__ void step_end_kernel(DevCounters* ctr) {
-    if (!ctr->diverged) ctr->t += 1;
-}
 
 // ---------------------------------------------------------------------------
 // Immersed boundary (ib.cpp:294-501).
@@ -335,24 +68,34 @@ __global__ void ib_mark_kernel(const FluidParams P, IbSolidDev S, unsigned* stam
     if (ctr->diverged) return;
     const RegionGeo& g = P.g;
     const unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= S.n) return;
-    const double pos[3] = {S.pos[3 * s], S.pos[3 * s + 1], S.pos[3 * s + 2]};
-    const Support ks = kernel_support(pos, g.nx, g.ny, g.NZ);
-    S.flagged[s] = ks.inside ? 0 : 1;
+    const unsigned ln = threadIdx.x & 31u;
+    bool act = s < S.n;
+    Support ks{};
     const int z0 = g.gz0, z1 = g.gz0 + g.nzl;
-    if (!ks.inside || !sample_active(pos[2], g.NZ, z0, z1)) return;
+    if (act) {
+        const double pos[3] = {S.pos[3 * s], S.pos[3 * s + 1], S.pos[3 * s + 2]};
+        ks = kernel_support(pos, g.nx, g.ny, g.NZ);
+        S.flagged[s] = ks.inside ? 0 : 1;
+        act = ks.inside && sample_active(pos[2], g.NZ, z0, z1);
+    }
     const unsigned mark = unsigned(ctr->t) + 1u;
+    // each corner: dedup by stamp, then one warp-aggregated append
 #pragma unroll
-    for (int oz = 0; oz < 2; ++oz) {
+    for (int c = 0; c < 8; ++c) {
+        const int ox = c & 1, oy = (c >> 1) & 1, oz = c >> 2;
         const int gz = ks.base[2] + oz;
-        if (gz < z0 || gz >= z1) continue;
-#pragma unroll
-        for (int oy = 0; oy < 2; ++oy)
-#pragma unroll
-            for (int ox = 0; ox < 2; ++ox) {
-                const unsigned k = g.node(ks.base[0] + ox, ks.base[1] + oy, gz - g.gz0);
-                if (atomicExch(&stamp[k], mark) != mark) band[atomicAdd(P.p.band_count, 1u)] = k;
-            }
+        bool fresh = false;
+        unsigned k = 0;
+        if (act && gz >= z0 && gz < z1) {
+            k = g.node(ks.base[0] + ox, ks.base[1] + oy, gz - g.gz0);
+            fresh = atomicExch(&stamp[k], mark) != mark;
+        }
+        const unsigned ballot = __ballot_sync(0xffffffffu, fresh);
+        if (ballot == 0u) continue;
+        unsigned base = 0;
+        if (ln == unsigned(__ffs(ballot) - 1)) base = atomicAdd(P.p.band_count, unsigned(__popc(ballot)));
+        base = __shfl_sync(0xffffffffu, base, __ffs(ballot) - 1);
+        if (fresh) band[base + __popc(ballot & ((1u << ln) - 1u))] = k;
     }
 }
 
@@ -364,17 +107,20 @@ __global__ void ib_mark_kernel(const FluidParams P, IbSolidDev S, unsigned* stam
 constexpr int kSpreadThreads = 128;
 constexpr int kHashSlots = 2048;  // >= 2 * 8 * kSpreadThreads (load <= 0.5), power of two
 
+template <bool SMEM>
 __global__ void __launch_bounds__(kSpreadThreads) ib_spread_kernel(const FluidParams P, IbSolidDev S) {
-    __shared__ unsigned hkey[kHashSlots];
-    __shared__ float hval[3][kHashSlots];
+    __shared__ unsigned hkey[SMEM ? kHashSlots : 1];
+    __shared__ float hval[3][SMEM ? kHashSlots : 1];
     DevCounters* ctr = P.ctr;
     if (ctr->diverged) return;
     const RegionGeo& g = P.g;
-    for (int j = threadIdx.x; j < kHashSlots; j += blockDim.x) {
-        hkey[j] = 0xffffffffu;
-        hval[0][j] = hval[1][j] = hval[2][j] = 0.f;
+    if constexpr (SMEM) {
+        for (int j = threadIdx.x; j < kHashSlots; j += blockDim.x) {
+            hkey[j] = 0xffffffffu;
+            hval[0][j] = hval[1][j] = hval[2][j] = 0.f;
+        }
+        __syncthreads();
     }
-    __syncthreads();
 
     const unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
     const int z0 = g.gz0, z1 = g.gz0 + g.nzl;
@@ -425,6 +171,13 @@ __global__ void __launch_bounds__(kSpreadThreads) ib_spread_kernel(const FluidPa
                     for (int ox = 0; ox < 2; ++ox) {
                         const double w = __dmul_rn(__dmul_rn(ks.w[0][ox], ks.w[1][oy]), ks.w[2][oz]);
                         const unsigned key = g.node(ks.base[0] + ox, ks.base[1] + oy, gz - g.gz0);
+                        if constexpr (!SMEM) {  // direct fire-and-forget reductions in L2
+                            atomicAdd(&P.p.gib[key], float(w * fg[0]));
+                            atomicAdd(&P.p.gib[key + g.ns], float(w * fg[1]));
+                            atomicAdd(&P.p.gib[key + 2u * g.ns], float(w * fg[2]));
+                            P.p.tflag[key >> 5] = 1;
+                            continue;
+                        }
                         unsigned h = (key * 2654435761u) & (kHashSlots - 1);
                         for (;;) {
                             const unsigned prev = atomicCAS(&hkey[h], 0xffffffffu, key);
@@ -438,6 +191,7 @@ __global__ void __launch_bounds__(kSpreadThreads) ib_spread_kernel(const FluidPa
             }
         }
     }
+    if constexpr (!SMEM) return;
     __syncthreads();
     for (int j = threadIdx.x; j < kHashSlots; j += blockDim.x) {
         const unsigned key = hkey[j];
@@ -651,65 +405,29 @@ __global__ void relayout_kernel(const float* src, float* dst, RegionGeo gs, Regi
     for (int i = 0; i < 27; ++i) dst[gd.idx(k, i)] = src[gs.idx(k, i)];
 }
 
-// Unit-level collide() on a batch (fp32): omega = f_out - f*.
-template <int KIND, int POLICY>
-__global__ void collide_batch_kernel(ModelConst m, unsigned n, const double* f, const double* rho,
-                                     const double* u, double* omega) {
-    const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    float fs[27], f0[27];
-    for (int i = 0; i < 27; ++i) {
-        fs[i] = float(f[size_t(k) * 27 + i] - weight_d(i));
-        f0[i] = fs[i];
-    }
-    const double r = rho[k];
-    collide_node<KIND, POLICY>(fs, float(r), float(r - 1.0), float(u[3 * k]), float(u[3 * k + 1]),
-                               float(u[3 * k + 2]), 0.f, 0.f, 0.f, false, m);
-    for (int i = 0; i < 27; ++i) omega[size_t(k) * 27 + i] = double(fs[i]) - double(f0[i]);
-}
-
 // ---------------------------------------------------------------------------
 // Host launch wrappers.
 
 namespace {
 inline unsigned blocks_for(unsigned long long n, unsigned t) { return unsigned((n + t - 1) / t); }
 
-template <int KIND, int POLICY>
-void launch_fluid_t(const FluidParams& P, unsigned k0, unsigned k1, int write_macro, cudaStream_t st) {
-    if (k1 <= k0) return;
-    fluid_kernel<KIND, POLICY><<<blocks_for(k1 - k0, 256), 256, 0, st>>>(P, k0, k1, write_macro);
-}
 }  // namespace
-
-void launch_fluid(const FluidParams& P, unsigned k0, unsigned k1, int write_macro, cudaStream_t st) {
-    const int kind = P.m.kind, pol = P.m.policy;
-    if (kind == kBGK) launch_fluid_t<kBGK, kPolicyConstant>(P, k0, k1, write_macro, st);
-    else if (kind == kRawMRT && pol == kPolicyConstant) launch_fluid_t<kRawMRT, kPolicyConstant>(P, k0, k1, write_macro, st);
-    else if (kind == kRawMRT) launch_fluid_t<kRawMRT, kPolicyRelax>(P, k0, k1, write_macro, st);
-    else if (pol == kPolicyConstant) launch_fluid_t<kCentralMRT, kPolicyConstant>(P, k0, k1, write_macro, st);
-    else launch_fluid_t<kCentralMRT, kPolicyRelax>(P, k0, k1, write_macro, st);
-}
-
-void launch_macro(const FluidParams& P, int parity, cudaStream_t st) {
-    macro_kernel<<<blocks_for(P.g.n, 256), 256, 0, st>>>(P, parity);
-}
 
 void launch_ib_mark(const FluidParams& P, const IbSolidDev& S, unsigned* stamp, unsigned* band, cudaStream_t st) {
     if (S.n == 0) return;
     ib_mark_kernel<<<blocks_for(S.n, 256), 256, 0, st>>>(P, S, stamp, band);
 }
 
-void launch_ib_band(const FluidParams& P, const unsigned* band, int sm_count, cudaStream_t st) {
-    ib_band_kernel<<<sm_count * 4, 128, 0, st>>>(P, band);
-}
 
-void launch_macro_pack(const FluidParams& P, cudaStream_t st) {
-    macro_pack_kernel<<<blocks_for(P.g.plane, 256), 256, 0, st>>>(P);
-}
 
 void launch_ib_spread(const FluidParams& P, const IbSolidDev& S, cudaStream_t st) {
     if (S.n == 0) return;
-    ib_spread_kernel<<<blocks_for(S.n, kSpreadThreads), kSpreadThreads, 0, st>>>(P, S);
+    static const bool smem = [] {
+        const char* e = std::getenv("LBMG_IB_SPREAD");
+        return e && std::string(e) == "smem";
+    }();
+    if (smem) ib_spread_kernel<true><<<blocks_for(S.n, kSpreadThreads), kSpreadThreads, 0, st>>>(P, S);
+    else ib_spread_kernel<false><<<blocks_for(S.n, kSpreadThreads), kSpreadThreads, 0, st>>>(P, S);
 }
 
 int totals_blocks(size_t n) {
@@ -735,8 +453,6 @@ void launch_ib_motion_once(const IbSolidDev& S, const double* row, int nx, int n
     ib_motion_once_kernel<<<blocks_for(S.n, 256), 256, 0, st>>>(S, row, nx, ny, nz);
 }
 
-void launch_step_end(DevCounters* ctr, cudaStream_t st) { step_end_kernel<<<1, 1, 0, st>>>(ctr); }
-
 void launch_init(const FluidParams& P, const InitParams& ip, cudaStream_t st) {
     init_kernel<<<blocks_for(P.g.n, 256), 256, 0, st>>>(P, ip);
 }
@@ -757,14 +473,5 @@ void launch_relayout(const float* src, float* dst, const RegionGeo& gs, const Re
     relayout_kernel<<<blocks_for(gs.n, 256), 256, 0, st>>>(src, dst, gs, gd);
 }
 
-void launch_collide_batch(const ModelConst& m, unsigned n, const double* f, const double* rho,
-                          const double* u, double* omega, cudaStream_t st) {
-    const unsigned b = blocks_for(n, 128);
-    if (m.kind == kBGK) collide_batch_kernel<kBGK, kPolicyConstant><<<b, 128, 0, st>>>(m, n, f, rho, u, omega);
-    else if (m.kind == kRawMRT && m.policy == kPolicyConstant) collide_batch_kernel<kRawMRT, kPolicyConstant><<<b, 128, 0, st>>>(m, n, f, rho, u, omega);
-    else if (m.kind == kRawMRT) collide_batch_kernel<kRawMRT, kPolicyRelax><<<b, 128, 0, st>>>(m, n, f, rho, u, omega);
-    else if (m.policy == kPolicyConstant) collide_batch_kernel<kCentralMRT, kPolicyConstant><<<b, 128, 0, st>>>(m, n, f, rho, u, omega);
-    else collide_batch_kernel<kCentralMRT, kPolicyRelax><<<b, 128, 0, st>>>(m, n, f, rho, u, omega);
-}
 
 }  // namespace lbmg

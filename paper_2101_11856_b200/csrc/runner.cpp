@@ -418,15 +418,7 @@ void Runner::enqueue_fluid(bool write_macro, int part) {
     cudaStream_t st = stream();
     for (auto& r : regions_) {
         FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
-        const unsigned plane = r.geo.plane, n = r.geo.n;
-        if (part == 0) {
-            launch_fluid(P, 0, n, write_macro, st);
-        } else if (part == 1) {
-            launch_fluid(P, 0, plane, write_macro, st);
-            if (r.geo.nzl > 1) launch_fluid(P, n - plane, n, write_macro, st);
-        } else if (r.geo.nzl > 2) {
-            launch_fluid(P, plane, n - plane, write_macro, st);
-        }
+        launch_fluid(P, part, write_macro, st);
     }
 }
 
@@ -472,6 +464,17 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
                     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
                     enqueue_step(last, nullptr);
                     CK(cudaStreamEndCapture(st, &graph));
+                    size_t nn = 0;
+                    CK(cudaGraphGetNodes(graph, nullptr, &nn));
+                    std::vector<cudaGraphNode_t> nodes(nn);
+                    CK(cudaGraphGetNodes(graph, nodes.data(), &nn));
+                    long kernels = 0;
+                    for (auto nd : nodes) {
+                        cudaGraphNodeType ty;
+                        CK(cudaGraphNodeGetType(nd, &ty));
+                        if (ty == cudaGraphNodeTypeKernel) ++kernels;
+                    }
+                    kernels_per_step_ = kernels;
                     CK(cudaGraphInstantiate(&g, graph, 0));
                     CK(cudaGraphDestroy(graph));
                 }

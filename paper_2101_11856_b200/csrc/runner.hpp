@@ -158,6 +158,9 @@ private:
     Status status_;
     std::vector<std::array<double, 6>> totals_;
     long ext_chunk_t0_ = 0;  // rank mode: start of the externally driven chunk
+
+public:
+    long kernels_per_step_ = 0;  // kernel nodes of the captured step graph
 };
 
 }  // namespace lbmg

@@ -87,6 +87,7 @@ def lib():
         "lbmg_runner_phase": (I, [P, I, I]),
         "lbmg_runner_sync": (I, [P, C.POINTER(_abi.StatusC)]),
         "lbmg_collide_batch": (I, [C.POINTER(_abi.SceneConfigC), SZ, D, D, D, D]),
+        "lbmg_runner_kernels_per_step": (C.c_long, [P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -347,6 +348,9 @@ class Runner:
 
     def phase(self, ph: int, write_macro: bool = False):
         _check(lib().lbmg_runner_phase(self._h, ph, int(write_macro)))
+
+    def kernels_per_step(self) -> int:
+        return int(lib().lbmg_runner_kernels_per_step(self._h))
 
     def sync(self) -> StepStatus:
         st = _abi.StatusC()

@@ -211,7 +211,12 @@ def test_periodic_momentum_conservation():
     f1 = g.gather_f()
     from oracle.refpy import ref_lattice
     c, _, _ = ref_lattice()
-    assert abs(f1.sum() - f0.sum()) / f0.sum() <= 1e-9
+    # A perfectly uniform state is the worst case for fp32 storage: every node
+    # rounds identically, so the per-step rounding of the stored populations
+    # (~1 ulp of |f - w| ~ 5e-10) accumulates coherently instead of as a random
+    # walk.  Bound: 2e-8 relative over 200 steps (measured 1e-9..4e-9); the
+    # non-uniform closed box above holds 1e-9 over 1000 steps.
+    assert abs(f1.sum() - f0.sum()) / f0.sum() <= 2e-8
     # momentum: fp32 storage drift per node relative to |rho u| (uniform state,
     # so per-node rounding is systematic; measured ~5e-8)
     p0 = f0 @ c
@@ -254,3 +259,88 @@ def test_timings_rows():
     g.advance(3, timings=rows)
     assert [r.phase for r in rows[:3]] == ["ib", "fluid", "total"]
     assert all(r.seconds > 0 for r in rows)
+
+
+# ---- rank mode (multi-process path) on one device --------------------------
+
+def _rank_mode_run(cfg, world, steps):
+    """Drive `world` rank-mode runners through the split step; the NCCL
+    send/recv is replaced by device copies with the same schedule."""
+    import torch
+    from paper_2101_11856_b200 import _abi
+    from paper_2101_11856_b200.dist import as_tensor, neighbours
+    scene = lbm.build_scene(cfg)
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    rs = [lbm.Runner(scene, world=world, rank=r) for r in range(world)]
+    for r in rs:
+        r.set_stream(stream.cuda_stream)
+    per = cfg.faces[4].condition == "periodic"
+    nbs = [neighbours(world, k, per) for k in range(world)]
+
+    def f_bufs(p):
+        out = []
+        for r in rs:
+            (sl, sh, rl, rh), nb = r.halo_f(p)
+            out.append([as_tensor(x, nb, dev) for x in (sl, sh, rl, rh)])
+        return out
+
+    def m_bufs():
+        out = []
+        for r in rs:
+            (sl, sh, rl, rh), nb = r.halo_macro()
+            out.append([as_tensor(x, nb, dev) for x in (sl, sh, rl, rh)])
+        return out
+
+    def swap(bufs):
+        for k in range(world):
+            nb = nbs[k]
+            if nb.lo >= 0:
+                bufs[k][2].copy_(bufs[nb.lo][1])   # my lower ghost <- lower neighbour's top plane
+            if nb.hi >= 0:
+                bufs[k][3].copy_(bufs[nb.hi][0])   # my upper ghost <- upper neighbour's bottom plane
+
+    swap(f_bufs(0))
+    for t in range(steps):
+        for r in rs:
+            r.phase(_abi.PHASE_PRE)
+        if cfg.solids:
+            swap(m_bufs())
+        for r in rs:
+            r.phase(_abi.PHASE_MID)
+        for r in rs:
+            r.phase(_abi.PHASE_FLUID_EDGE, t == steps - 1)
+        swap(f_bufs((t + 1) & 1))
+        for r in rs:
+            r.phase(_abi.PHASE_FLUID_BULK, t == steps - 1)
+        for r in rs:
+            r.phase(_abi.PHASE_END)
+    for r in rs:
+        st = r.sync()
+        assert st.ok
+    torch.cuda.synchronize()
+    return rs
+
+
+@pytest.mark.parametrize("make,world", [(lambda: scenes.channel(n=16, nz=24), 2),
+                                        (lambda: scenes.channel(n=16, nz=24), 3),
+                                        (lambda: scenes.cavity(n=18), 2),
+                                        (lambda: scenes.sphere(40, 24, 32, center=(14, 12, 16), radius=4.0,
+                                                               subdiv=2, r=0.6), 2)])
+def test_rank_mode_matches_in_process_regions(make, world):
+    cfg = make()
+    steps = 23
+    rs = _rank_mode_run(cfg, world, steps)
+    ref = lbm.Runner(lbm.build_scene(cfg), regions=world)
+    ref.advance(steps)
+    f_ref, rho_ref = ref.gather_f(), ref.gather_rho()
+    f_rank = np.concatenate([r.gather_f() for r in rs])
+    rho_rank = np.concatenate([r.gather_rho() for r in rs])
+    assert rs[0].step_count() == steps
+    if cfg.solids:  # fp32 atomics: same values up to accumulation order
+        assert np.abs(f_rank - f_ref).max() <= 1e-6
+        assert np.abs(rho_rank - rho_ref).max() <= 1e-6
+    else:
+        assert np.array_equal(f_rank, f_ref)
+        assert np.array_equal(rho_rank, rho_ref)
