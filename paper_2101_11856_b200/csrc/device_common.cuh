@@ -58,11 +58,42 @@ struct RegionGeo {
     unsigned A;           // per-direction stride inside a group: alpha, or n_pad for SoA
     unsigned ns;          // stride of the per-node SoA fields (rho, u, gib): n rounded to 32
     FastDiv div_nx, div_ny;
+    // Ghost-layer SoA ("ghost" = 1): each direction array is a padded box
+    // with row pitch PX = nx + 4 (column c = x + 2: x = -1 and x = nx are
+    // ghost columns, c = 0 and nx + 3 padding), PY = ny + 1 rows per plane
+    // (row r = y + 1; row 0 is both the y = -1 ghost row of its plane and the
+    // y = ny ghost row of the previous plane: those serve disjoint direction
+    // sets, c_y = +1 and c_y = -1) and planes lz = -1 .. nzl.  A pull that
+    // does not stream from inside the slab reads the ghost slot
+    // s(node) - off_i, which the ghost-fill kernel writes each step.
+    int ghost;
+    unsigned PX, PY, PP;  // row pitch, rows per plane, PX * PY
+    FastDiv div_px, div_py;
+
+    LBMG_HD unsigned sidx(int x, int y, int lz) const {
+        return (unsigned(lz + 1) * PY + unsigned(y + 1)) * PX + unsigned(x + 2);
+    }
+    // storage offset of one step along c_i in the ghost layout
+    LBMG_HD long long soff(int i) const {
+        return cx(i) + (long long)PX * cy(i) + (long long)PP * cz(i);
+    }
 
     // Eq. 9 (layout.hpp:41-52): beta*alpha*floor(k/alpha) + alpha*i + k mod alpha
+    // (ghost layout: i*A + sidx of the decoded node)
     LBMG_HD unsigned long long idx(unsigned k, int i) const {
+        if (ghost) {
+            const unsigned q = div_nx.div(k);
+            const unsigned q2 = div_ny.div(q);
+            return static_cast<unsigned long long>(static_cast<unsigned>(i)) * A +
+                   sidx(int(k - q * unsigned(nx)), int(q - q2 * unsigned(ny)), int(q2));
+        }
         return static_cast<unsigned long long>(k >> la) * (27ull * A) +
                static_cast<unsigned long long>(static_cast<unsigned>(i)) * A + (k & amask);
+    }
+    // population i of the node at (x, y, lz), 0 <= x < nx, 0 <= y < ny, 0 <= lz < nzl
+    LBMG_HD unsigned long long at(int x, int y, int lz, int i) const {
+        if (ghost) return static_cast<unsigned long long>(static_cast<unsigned>(i)) * A + sidx(x, y, lz);
+        return idx(node(x, y, lz), i);
     }
     LBMG_HD unsigned node(int x, int y, int lz) const {
         return (static_cast<unsigned>(lz) * static_cast<unsigned>(ny) + static_cast<unsigned>(y)) *
@@ -126,6 +157,7 @@ struct DevCounters {
     unsigned mach;             // sticky Mach warning
     long long diverged_step;   // step at which divergence was detected
     long long chunk_t0;        // first step of the current advance chunk
+    unsigned tile_ctr[4];      // tile queues of the staged fluid launches of a step
 };
 
 struct FluidParams {

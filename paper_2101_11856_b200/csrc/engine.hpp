@@ -30,6 +30,16 @@ struct InitParams {
     int NX, NY;
 };
 
+// Floats allocated per population buffer: 27 * n_pad plus a tail the bulk
+// kernel's staged windows may read past the last direction array (the
+// widest window of the last tile ends <= nx + 2 * kBulkTile + 8 floats past
+// the owned nodes; never used).
+inline unsigned long long f_alloc_floats(const RegionGeo& g) {
+    return 27ull * g.n_pad + unsigned(g.nx) + 1024u;
+}
+
+bool ghost_layout_enabled();
+
 // part: 0 every node, 1 the two halo planes (edge), 2 everything else (bulk)
 void launch_fluid(const FluidParams& P, int part, int write_macro, cudaStream_t st);
 void launch_macro(const FluidParams& P, int parity, cudaStream_t st);

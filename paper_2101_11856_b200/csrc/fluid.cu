@@ -16,12 +16,16 @@
 //                      code (bit-identical per node to the bulk path).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
+#include <stdexcept>
+#include <string>
 #include <type_traits>
 
 #include "collision.cuh"
 #include "device_common.cuh"
 #include "engine.hpp"
+#include "tma.cuh"
 
 namespace lbmg {
 
@@ -54,7 +58,7 @@ __device__ __forceinline__ float pull_rt(const RegionGeo& g, const StepView& v, 
     const unsigned hp = cross9(i, 2) * g.plane + unsigned(sy) * g.nx + unsigned(sx);
     if (lzs < 0) return v.halo_lo[hp];
     if (lzs >= g.nzl) return v.halo_hi[hp];
-    return v.fin[g.idx(g.node(sx, sy, lzs), i)];
+    return v.fin[g.at(sx, sy, lzs, i)];
 }
 
 // f*_i at (x,y,lz) once face pass `owner` has run this step (apply_face,
@@ -69,7 +73,7 @@ __device__ __forceinline__ float reconstruct(const FluidParams& P, const StepVie
     int f = owner;
     for (int guard = 0; guard < 7; ++guard) {
         const int cond = ft.cond[f];
-        if (cond == kNoSlip) return v.fin[g.idx(g.node(x, y, lz), opposite(i))];
+        if (cond == kNoSlip) return v.fin[g.at(x, y, lz, opposite(i))];
         if (cond == kInlet) return ft.inlet[f][i];
         const int a = face_axis(f), s = face_side(f);
         if (a == 0) x -= s;
@@ -92,8 +96,7 @@ __device__ __forceinline__ void gather_node(const FluidParams& P, const StepView
     if (interior) {
         static_for<0, 27>([&](auto I) {
             constexpr int i = decltype(I)::value;
-            const unsigned ks = k - unsigned(cx(i) + g.nx * cy(i) + int(g.plane) * cz(i));
-            fs[i] = __ldg(&v.fin[g.idx(ks, i)]);
+            fs[i] = __ldg(&v.fin[g.at(x - cx(i), y - cy(i), lz - cz(i), i)]);
         });
         return;
     }
@@ -110,11 +113,11 @@ __device__ __forceinline__ void gather_node(const FluidParams& P, const StepView
         const int lzs = lz - cz(i);
         const unsigned hp = cross9(i, 2) * g.plane + unsigned(sy) * g.nx + unsigned(sx);
         const float* src;
-        if constexpr (cz(i) == 1) src = lzs < 0 ? v.halo_lo + hp : v.fin + g.idx(g.node(sx, sy, lzs), i);
-        else if constexpr (cz(i) == -1) src = lzs >= g.nzl ? v.halo_hi + hp : v.fin + g.idx(g.node(sx, sy, lzs), i);
-        else src = v.fin + g.idx(g.node(sx, sy, lzs), i);
+        if constexpr (cz(i) == 1) src = lzs < 0 ? v.halo_lo + hp : v.fin + g.at(sx, sy, lzs, i);
+        else if constexpr (cz(i) == -1) src = lzs >= g.nzl ? v.halo_hi + hp : v.fin + g.at(sx, sy, lzs, i);
+        else src = v.fin + g.at(sx, sy, lzs, i);
         if (own != kNoOwner) {
-            src = v.fin + g.idx(k, i);
+            src = v.fin + g.at(x, y, lz, i);
             miss |= 1u << i;
         }
         fs[i] = __ldg(src);
@@ -364,6 +367,262 @@ __global__ void __launch_bounds__(kBulkThreads, FORM == 2 ? 4 : 3) fluid_bulk_ke
     }
 }
 
+// ---------------------------------------------------------------------------
+// Ghost-layer path (RegionGeo::ghost, SoA with nx % 4 == 0).
+//
+//  ghost_fill_kernel   the six face passes of this step (apply_face,
+//                      boundary.cpp:42-125), periodic wraps and z halos:
+//                      for every node on a face of the slab and each of the
+//                      9 directions crossing that face, f*_i(node) is written
+//                      into the ghost slot the node pulls from,
+//                      s(node) - off_i.  Afterwards every pull of every owned
+//                      node is a plain shifted read.
+//  fluid_ghost_kernel  persistent CTAs walk contiguous chunks of kTile
+//                      storage slots.  Per tile one elected thread issues 27
+//                      one-dimensional TMA bulk copies — each direction's
+//                      window, shifted by off_i and widened to 16-byte
+//                      alignment — into a ring of kStages shared-memory stages
+//                      completed on mbarriers, so the next tile is in flight
+//                      while the CTA computes the current one (two nodes per
+//                      thread, packed FFMA2 collision, 64-bit stores).  Lanes on
+//                      ghost/pad slots compute but do not store.
+constexpr int kTile = 2 * kBulkThreads;  // storage slots per tile
+constexpr int kWin = kTile + 4;         // staged floats per direction
+constexpr int kStages = 2;
+constexpr unsigned kStageBytes = 27u * kWin * 4u;
+constexpr unsigned kStagedSmem = kStages * kStageBytes + 8u * kStages;
+
+// Window offset of slot 0 of a tile for direction i: tiles start at multiples
+// of 4 and PX, PP are multiples of 4, so (tile start - off_i) = -c_x (mod 4).
+__host__ __device__ constexpr int win_shift(int i) { return (4 - cx(i)) & 3; }
+
+// Address of f*_i at (x,y,lz) for a pull that does not stream from inside
+// the slab: the wrapped / halo source, or — for a missing pull — the value
+// face pass `owner` reconstructs (same chain as reconstruct(): bounce-back
+// source, inlet constant in kernel-parameter space, stale slot of a later
+// face, or the streamed source of the outflow neighbour).  Never a ghost slot.
+__device__ __forceinline__ const float* pull_source(const FluidParams& P, int p, int x, int y, int lz, int i) {
+    const RegionGeo& g = P.g;
+    const StepView v = make_view(P, p);
+    auto pull_addr = [&](int xx, int yy, int zz) -> const float* {
+        int sx = xx - cx(i), sy = yy - cy(i);
+        if (sx < 0) sx += g.nx;
+        else if (sx >= g.nx) sx -= g.nx;
+        if (sy < 0) sy += g.ny;
+        else if (sy >= g.ny) sy -= g.ny;
+        const int lzs = zz - cz(i);
+        const unsigned hp = cross9(i, 2) * g.plane + unsigned(sy) * g.nx + unsigned(sx);
+        if (lzs < 0) return v.halo_lo + hp;
+        if (lzs >= g.nzl) return v.halo_hi + hp;
+        return v.fin + g.at(sx, sy, lzs, i);
+    };
+    int f = owner_face(g, x, y, g.gz0 + lz, i);
+    if (f == kNoOwner) return pull_addr(x, y, lz);
+    for (int guard = 0; guard < 7; ++guard) {
+        const int cond = P.faces.cond[f];
+        if (cond == kNoSlip) return v.fin + g.at(x, y, lz, opposite(i));
+        if (cond == kInlet) return &P.faces.inlet[f][i];
+        const int a = face_axis(f), s = face_side(f);
+        if (a == 0) x -= s;
+        else if (a == 1) y -= s;
+        else lz -= s;
+        const int fn = owner_face(g, x, y, g.gz0 + lz, i);
+        if (fn == kNoOwner) return pull_addr(x, y, lz);
+        if (fn > f) return P.p.slot[p][fn] + g.slot_index(fn, x, y, lz, i);
+        f = fn;
+    }
+    return &P.faces.inlet[0][0];  // unreachable: the owner strictly decreases along the chain
+}
+
+// Entries: for faces f = 0..5 of the slab, direction slot j = 0..8 (slowest)
+// and the face's nodes (fastest, so consecutive threads walk rows).
+__global__ void __launch_bounds__(256) ghost_fill_kernel(const __grid_constant__ FluidParams P) {
+    DevCounters* ctr = P.ctr;
+    if (blockIdx.x == 0 && threadIdx.x < 3) ctr->tile_ctr[threadIdx.x] = 0u;  // this step's tile queues
+    if (ctr->diverged) return;
+    const RegionGeo& g = P.g;
+    const unsigned Fx = unsigned(g.ny) * g.nzl, Fy = unsigned(g.nx) * g.nzl, Fz = g.plane;
+    unsigned e = blockIdx.x * blockDim.x + threadIdx.x;
+    int f = 0;
+    unsigned F = Fx;
+    for (; f < 6; ++f) {
+        F = f < 2 ? Fx : (f < 4 ? Fy : Fz);
+        if (e < 9u * F) break;
+        e -= 9u * F;
+    }
+    if (f == 6) return;
+    const unsigned j = e / F, q = e - j * F;
+    const int axis = face_axis(f), side = face_side(f);
+    int x, y, lz, c[3];
+    const int ja = int(j % 3) - 1, jb = int(j / 3) - 1;  // cross9 order: lower axis fastest
+    if (axis == 0) {
+        y = int(q % unsigned(g.ny)); lz = int(q / unsigned(g.ny)); x = side < 0 ? 0 : g.nx - 1;
+        c[0] = -side; c[1] = ja; c[2] = jb;
+    } else if (axis == 1) {
+        x = int(q % unsigned(g.nx)); lz = int(q / unsigned(g.nx)); y = side < 0 ? 0 : g.ny - 1;
+        c[0] = ja; c[1] = -side; c[2] = jb;
+    } else {
+        x = int(q % unsigned(g.nx)); y = int(q / unsigned(g.nx)); lz = side < 0 ? 0 : g.nzl - 1;
+        c[0] = ja; c[1] = jb; c[2] = -side;
+    }
+    const int i = tensor_dir((c[0] + 1) + 3 * (c[1] + 1) + 9 * (c[2] + 1));
+    const int p = int(ctr->t & 1);
+    const float val = *pull_source(P, p, x, y, lz, i);
+    float* fin = P.p.f[p];
+    fin[(long long)i * g.A + (long long)g.sidx(x, y, lz) - g.soff(i)] = val;
+    const int own = owner_face(g, x, y, g.gz0 + lz, i);
+    if (own != kNoOwner) P.p.slot[p ^ 1][own][g.slot_index(own, x, y, lz, i)] = val;
+}
+
+template <int KIND, int POLICY, bool STD>
+__global__ void __launch_bounds__(kBulkThreads, 4)
+    fluid_ghost_kernel(const __grid_constant__ FluidParams P, int z_a, int z_b, int slot, int write_macro, int dbg) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float* const stage0 = reinterpret_cast<float*>(smem_raw);
+    uint64_t* const full = reinterpret_cast<uint64_t*>(smem_raw + kStages * kStageBytes);
+    DevCounters* ctr = P.ctr;
+    if (ctr->diverged) return;  // CTA-uniform
+    const RegionGeo& g = P.g;
+    const int p = int(ctr->t & 1);
+    const float* __restrict__ fin = P.p.f[p];
+    float* __restrict__ fout = P.p.f[p ^ 1];
+    const unsigned tid = threadIdx.x;
+    const unsigned sb = unsigned(z_a + 1) * g.PP, se = unsigned(z_b + 1) * g.PP;
+    const unsigned ntiles = (se - sb + kTile - 1) / kTile;
+    // Tiles are handed out in order by a device counter (reset by the ghost
+    // fill of this step): all CTAs sweep the arrays together, so DRAM pages
+    // stay open across CTAs and the window edges two neighbouring tiles share
+    // are fetched once and hit in L2 for the other.
+    unsigned* const next_tile = &ctr->tile_ctr[slot];
+    __shared__ unsigned stage_tile[kStages];
+    __shared__ unsigned reads_done[kStages];
+
+    // claim the next tile into stage s (elected thread); past the end the
+    // stage's phase completes empty so the consumers see the end marker
+    auto refill = [&](int s) {
+        const unsigned tile = atomicAdd(next_tile, 1u);
+        stage_tile[s] = tile;
+        if (tile >= ntiles) {
+            mbar_arrive(&full[s]);
+            return;
+        }
+        const long long k0 = (long long)sb + (long long)tile * kTile;
+        float* dst = stage0 + s * (kStageBytes / 4);
+        mbar_arrive_expect_tx(&full[s], kStageBytes);
+        static_for<0, 27>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            const float* src = fin + (long long)i * g.A + k0 - g.soff(i) - win_shift(i);
+            tma_load_1d(dst + i * kWin, src, kWin * 4u, &full[s]);
+        });
+    };
+    // consumer release: the last warp to finish reading a stage refills it
+    // (no CTA-wide barrier per tile: warps never wait for the slowest one)
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            reads_done[s] = 0;
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int s = 0; s < kStages; ++s) refill(s);
+
+    for (unsigned it = 0;; ++it) {
+        const int s = int(it % kStages);
+        const float* const st = stage0 + s * (kStageBytes / 4);
+        mbar_wait_parity(&full[s], (it / kStages) & 1u);
+        const unsigned tile = stage_tile[s];
+        if (tile >= ntiles) break;
+        const unsigned m = 2u * tid;
+        const unsigned sl = sb + tile * kTile + m;  // storage slot of the pair's first node
+        const unsigned row = g.div_px.div(sl);
+        const int col = int(sl - row * g.PX);
+        const unsigned pl = g.div_py.div(row);
+        const int r = int(row - pl * g.PY);
+        const int x = col - 2, y = r - 1, lz = int(pl) - 1;
+        // pairs are all-ghost or all-owned (nx, PX even)
+        const bool valid = sl < se && x >= 0 && x < g.nx && y >= 0;
+        float2 fs[27];
+        static_for<0, 27>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            constexpr int d = win_shift(i);
+            const float* w = st + i * kWin + m + d;
+            if constexpr (d % 2 == 0) fs[i] = *reinterpret_cast<const float2*>(w);
+            else fs[i] = make_float2(w[0], w[1]);
+        });
+        __syncwarp();
+        if ((tid & 31u) == 0) {
+            __threadfence_block();  // this warp's reads of stage s are done
+            if (atomicAdd(&reads_done[s], 1u) == kBulkThreads / 32 - 1) {
+                reads_done[s] = 0;
+                fence_proxy_async_smem();
+                refill(s);
+            }
+        }
+        if (!valid) continue;
+        if (dbg) {  // bandwidth probes: 1 = staged loads only, 2 = loads + stores (no collision)
+            if (dbg == 2)
+                static_for<0, 27>([&](auto I) {
+                    constexpr int i = decltype(I)::value;
+                    *reinterpret_cast<float2*>(fout + size_t(i) * g.A + sl) = fs[i];
+                });
+            else if (fs[0].x == 12345.f)
+                fout[sl] = fs[26].y;
+            continue;
+        }
+
+        const unsigned k = (unsigned(lz) * g.ny + unsigned(y)) * g.nx + unsigned(x);  // compact node index
+        const MacroV<float2> mc = moments_v<float2>(fs);
+        if (mc.bad[0] || mc.bad[1]) {
+            flag_divergence(ctr);
+            continue;
+        }
+        if (mc.mach[0] || mc.mach[1]) atomicOr(&ctr->mach, 1u);
+        if (write_macro) {
+            *reinterpret_cast<float2*>(P.p.rho + k) = mc.rho;
+            *reinterpret_cast<float2*>(P.p.u + k) = mc.ux;
+            *reinterpret_cast<float2*>(P.p.u + k + g.ns) = mc.uy;
+            *reinterpret_cast<float2*>(P.p.u + k + 2u * g.ns) = mc.uz;
+        }
+        float2 gx = make_float2(P.m.body[0], P.m.body[0]);
+        float2 gy = make_float2(P.m.body[1], P.m.body[1]);
+        float2 gz = make_float2(P.m.body[2], P.m.body[2]);
+        if (P.p.tflag != nullptr && P.p.tflag[k >> 5]) {
+            float* gib = P.p.gib;
+            gx = __fadd2_rn(gx, *reinterpret_cast<const float2*>(gib + k));
+            gy = __fadd2_rn(gy, *reinterpret_cast<const float2*>(gib + k + g.ns));
+            gz = __fadd2_rn(gz, *reinterpret_cast<const float2*>(gib + k + 2u * g.ns));
+            *reinterpret_cast<float2*>(gib + k) = make_float2(0.f, 0.f);
+            *reinterpret_cast<float2*>(gib + k + g.ns) = make_float2(0.f, 0.f);
+            *reinterpret_cast<float2*>(gib + k + 2u * g.ns) = make_float2(0.f, 0.f);
+        }
+        const bool any_force = gx.x != 0.f || gx.y != 0.f || gy.x != 0.f || gy.y != 0.f || gz.x != 0.f || gz.y != 0.f;
+        NoStash<float2> stash;
+        collide_v<KIND, POLICY, STD, float2>(fs, mc, gx, gy, gz, any_force, P.m, stash);
+        static_for<0, 27>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            *reinterpret_cast<float2*>(fout + size_t(i) * g.A + sl) = fs[i];
+        });
+        // crossing populations of the slab's boundary planes -> neighbour halos
+        const unsigned hp = unsigned(y) * g.nx + unsigned(x);
+        if (lz == 0 && P.p.send_lo[p ^ 1] != nullptr) {
+            float* sd = P.p.send_lo[p ^ 1];
+            static_for<1, 10>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                *reinterpret_cast<float2*>(sd + cross9(i, 2) * g.plane + hp) = fs[i];
+            });
+        }
+        if (lz == g.nzl - 1 && P.p.send_hi[p ^ 1] != nullptr) {
+            float* sd = P.p.send_hi[p ^ 1];
+            static_for<18, 27>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                *reinterpret_cast<float2*>(sd + cross9(i, 2) * g.plane + hp) = fs[i];
+            });
+        }
+    }
+}
+
 // Recompute rho*/u* of the current step from f(t) (after divergence, so the
 // readback matches the reference's partially written moments, solver.cpp:113).
 __global__ void macro_kernel(const FluidParams P, int parity) {
@@ -457,6 +716,12 @@ namespace {
 
 inline unsigned blocks_for(unsigned long long n, unsigned t) { return unsigned((n + t - 1) / t); }
 
+#define CUDA_OK(x)                                                                                   \
+    do {                                                                                             \
+        const cudaError_t e_ = (x);                                                                  \
+        if (e_ != cudaSuccess) throw std::runtime_error(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
 // Collision output form (see StashFor; LBMG_FORM overrides, default 2 =
 // feq + t'': fewest live registers, fastest measured, profiles/).
 int fluid_form() {
@@ -468,9 +733,71 @@ int fluid_form() {
     return v;
 }
 
+}  // namespace
+
+// Ghost-layer path availability (LBMG_BULK=ldg forces the compact layout and
+// the register-direct kernels, for A/B comparisons).
+bool ghost_layout_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("LBMG_BULK");
+        return !(e && std::string(e) == "ldg") && fluid_form() == 2;
+    }();
+    return v;
+}
+
+namespace {
+
+template <int KIND, int POLICY, bool STD>
+void launch_ghost_planes(const FluidParams& P, int z_a, int z_b, int slot, int write_macro, cudaStream_t st) {
+    if (z_b <= z_a) return;
+    const RegionGeo& g = P.g;
+    const unsigned ntiles = (unsigned(z_b - z_a) * g.PP + kTile - 1) / kTile;
+    static int grid_per_sm = -1, sms = 0;
+    auto kern = fluid_ghost_kernel<KIND, POLICY, STD>;
+    if (grid_per_sm < 0) {
+        CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kStagedSmem)));
+        CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        int dev = 0;
+        CUDA_OK(cudaGetDevice(&dev));
+        CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        int nb = 0;
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kBulkThreads, kStagedSmem));
+        grid_per_sm = nb > 0 ? nb : 1;
+    }
+    const unsigned grid = std::min<unsigned>(ntiles, unsigned(grid_per_sm * sms));
+    static const int dbg = [] {
+        const char* e = std::getenv("LBMG_GHOST_DBG");
+        return e ? std::atoi(e) : 0;
+    }();
+    kern<<<grid, kBulkThreads, kStagedSmem, st>>>(P, z_a, z_b, slot, write_macro, dbg);
+}
+
+// part 0: every plane; 1: ghost fill + the slab's boundary planes (which feed
+// the halos); 2: the interior planes.
+template <int KIND, int POLICY, bool STD>
+void launch_fluid_ghost(const FluidParams& P, int part, int write_macro, cudaStream_t st) {
+    const RegionGeo& g = P.g;
+    if (part == 0 || part == 1) {
+        const unsigned entries = 9u * 2u * (unsigned(g.ny) * g.nzl + unsigned(g.nx) * g.nzl + g.plane);
+        ghost_fill_kernel<<<blocks_for(entries, 256), 256, 0, st>>>(P);
+    }
+    if (part == 0) {
+        launch_ghost_planes<KIND, POLICY, STD>(P, 0, g.nzl, 0, write_macro, st);
+    } else if (part == 1) {
+        launch_ghost_planes<KIND, POLICY, STD>(P, 0, 1, 0, write_macro, st);
+        if (g.nzl > 1) launch_ghost_planes<KIND, POLICY, STD>(P, g.nzl - 1, g.nzl, 1, write_macro, st);
+    } else {
+        launch_ghost_planes<KIND, POLICY, STD>(P, 1, g.nzl - 1, 2, write_macro, st);
+    }
+}
+
 template <int KIND, int POLICY, bool STD, int FORM>
 void launch_fluid_t(const FluidParams& P, int part, int write_macro, cudaStream_t st) {
     const RegionGeo& g = P.g;
+    if (g.ghost) {
+        if constexpr (FORM == 2) launch_fluid_ghost<KIND, POLICY, STD>(P, part, write_macro, st);
+        return;
+    }
     const bool bulk_ok = (g.nx % 2 == 0) && g.nx >= 4 && g.ny >= 3 && g.nzl >= 3;
     const unsigned zpart = (g.nzl >= 2 ? 2u : 1u) * g.plane;
     const unsigned shell_total =

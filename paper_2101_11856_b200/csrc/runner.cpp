@@ -169,8 +169,11 @@ void Runner::compute_geo(Region& r) const {
     g.plane = unsigned(nx_) * unsigned(ny_);
     g.n = g.plane * unsigned(g.nzl);
     g.ns = round_up(g.n, 32);
+    // alpha below one warp (incl. the reference default 1 = AoS) has no
+    // coalesced device equivalent: store SoA, the alpha -> infinity limit of
+    // Eq. 9 (results are layout-invariant bit for bit, tests/test_gpu_parity.py)
     const size_t a = next_pow2(std::max<size_t>(layout_.alpha_req, 32));
-    if (a >= g.n) {  // SoA: one group of n_pad nodes
+    if (layout_.alpha_req < 32 || a >= g.n) {  // SoA: one group of n_pad nodes
         g.la = 31;
         g.amask = 0x7fffffffu;
         g.n_pad = round_up(g.n, 32);
@@ -183,11 +186,23 @@ void Runner::compute_geo(Region& r) const {
     }
     g.div_nx = FastDiv(unsigned(nx_));
     g.div_ny = FastDiv(unsigned(ny_));
+    g.ghost = 0;
+    if (g.la == 31 && nx_ % 4 == 0 && ghost_layout_enabled()) {
+        // ghost-layer SoA (device_common.cuh): pitch nx+4, ny+1 rows, planes -1..nzl
+        g.ghost = 1;
+        g.PX = unsigned(nx_) + 4u;
+        g.PY = unsigned(ny_) + 1u;
+        g.PP = g.PX * g.PY;
+        g.div_px = FastDiv(g.PX);
+        g.div_py = FastDiv(g.PY);
+        g.n_pad = round_up(unsigned(g.nzl + 2) * g.PP + g.PX + 64u, 32);
+        g.A = g.n_pad;
+    }
 }
 
 void Runner::alloc_f(Region& r) {
     for (int p = 0; p < 2; ++p) {
-        r.f[p] = static_cast<float*>(dalloc(sizeof(float) * 27ull * r.geo.n_pad, false));
+        r.f[p] = static_cast<float*>(dalloc(sizeof(float) * f_alloc_floats(r.geo), false));
         r.ptr.f[p] = r.f[p];
     }
 }
@@ -626,9 +641,9 @@ void Runner::set_layout(int ell, size_t alpha) {
         const RegionGeo go = r.geo;
         compute_geo(r);
         const RegionGeo gn = r.geo;
-        if (gn.la == go.la && gn.A == go.A && gn.n_pad == go.n_pad) continue;
+        if (gn.la == go.la && gn.A == go.A && gn.n_pad == go.n_pad && gn.ghost == go.ghost) continue;
         for (int p = 0; p < 2; ++p) {
-            float* nf = static_cast<float*>(dalloc(sizeof(float) * 27ull * gn.n_pad, false));
+            float* nf = static_cast<float*>(dalloc(sizeof(float) * f_alloc_floats(gn), false));
             launch_relayout(r.f[p], nf, go, gn, stream());
             CK(cudaStreamSynchronize(stream()));
             dfree(r.f[p]);
