@@ -66,12 +66,19 @@ struct RegionGeo {
     // sets, c_y = +1 and c_y = -1) and planes lz = -1 .. nzl.  A pull that
     // does not stream from inside the slab reads the ghost slot
     // s(node) - off_i, which the ghost-fill kernel writes each step.
+    // Storage slots are grouped in Eq. 9 CSoA blocks of alpha = 2^la slots
+    // (alpha >= 256; alpha >= slots = SoA): gaddr(s, i).  `base` leading
+    // slots keep the shifted windows of the first tile inside the buffer.
     int ghost;
     unsigned PX, PY, PP;  // row pitch, rows per plane, PX * PY
+    unsigned base;        // leading pad (a multiple of 256 slots)
     FastDiv div_px, div_py;
 
     LBMG_HD unsigned sidx(int x, int y, int lz) const {
-        return (unsigned(lz + 1) * PY + unsigned(y + 1)) * PX + unsigned(x + 2);
+        return base + (unsigned(lz + 1) * PY + unsigned(y + 1)) * PX + unsigned(x + 2);
+    }
+    LBMG_HD unsigned long long gaddr(unsigned long long s, int i) const {
+        return (s >> la) * (27ull * A) + static_cast<unsigned long long>(static_cast<unsigned>(i)) * A + (s & amask);
     }
     // storage offset of one step along c_i in the ghost layout
     LBMG_HD long long soff(int i) const {
@@ -84,15 +91,14 @@ struct RegionGeo {
         if (ghost) {
             const unsigned q = div_nx.div(k);
             const unsigned q2 = div_ny.div(q);
-            return static_cast<unsigned long long>(static_cast<unsigned>(i)) * A +
-                   sidx(int(k - q * unsigned(nx)), int(q - q2 * unsigned(ny)), int(q2));
+            return gaddr(sidx(int(k - q * unsigned(nx)), int(q - q2 * unsigned(ny)), int(q2)), i);
         }
         return static_cast<unsigned long long>(k >> la) * (27ull * A) +
                static_cast<unsigned long long>(static_cast<unsigned>(i)) * A + (k & amask);
     }
     // population i of the node at (x, y, lz), 0 <= x < nx, 0 <= y < ny, 0 <= lz < nzl
     LBMG_HD unsigned long long at(int x, int y, int lz, int i) const {
-        if (ghost) return static_cast<unsigned long long>(static_cast<unsigned>(i)) * A + sidx(x, y, lz);
+        if (ghost) return gaddr(sidx(x, y, lz), i);
         return idx(node(x, y, lz), i);
     }
     LBMG_HD unsigned node(int x, int y, int lz) const {

@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(256) ghost_fill_kernel(const __grid_constant__
     const int p = int(ctr->t & 1);
     const float val = *pull_source(P, p, x, y, lz, i);
     float* fin = P.p.f[p];
-    fin[(long long)i * g.A + (long long)g.sidx(x, y, lz) - g.soff(i)] = val;
+    fin[g.gaddr((unsigned long long)((long long)g.sidx(x, y, lz) - g.soff(i)), i)] = val;
     const int own = owner_face(g, x, y, g.gz0 + lz, i);
     if (own != kNoOwner) P.p.slot[p ^ 1][own][g.slot_index(own, x, y, lz, i)] = val;
 }
@@ -487,8 +487,11 @@ __global__ void __launch_bounds__(kBulkThreads, 4)
     const float* __restrict__ fin = P.p.f[p];
     float* __restrict__ fout = P.p.f[p ^ 1];
     const unsigned tid = threadIdx.x;
-    const unsigned sb = unsigned(z_a + 1) * g.PP, se = unsigned(z_b + 1) * g.PP;
-    const unsigned ntiles = (se - sb + kTile - 1) / kTile;
+    // slots of planes [z_a, z_b); tiles are kTile-aligned (CSoA blocks are
+    // multiples of kTile), lanes outside [sb, se) do not store
+    const unsigned sb = g.base + unsigned(z_a + 1) * g.PP, se = g.base + unsigned(z_b + 1) * g.PP;
+    const unsigned org = (sb / kTile) * kTile - (dbg >> 8);  // tile origin (probe: LBMG_GHOST_DBG >> 8 shift)
+    const unsigned ntiles = (se - org + kTile - 1) / kTile;
     // Tiles are handed out in order by a device counter (reset by the ghost
     // fill of this step): all CTAs sweep the arrays together, so DRAM pages
     // stay open across CTAs and the window edges two neighbouring tiles share
@@ -506,13 +509,18 @@ __global__ void __launch_bounds__(kBulkThreads, 4)
             mbar_arrive(&full[s]);
             return;
         }
-        const long long k0 = (long long)sb + (long long)tile * kTile;
+        const long long k0 = (long long)org + (long long)tile * kTile;
         float* dst = stage0 + s * (kStageBytes / 4);
         mbar_arrive_expect_tx(&full[s], kStageBytes);
         static_for<0, 27>([&](auto I) {
             constexpr int i = decltype(I)::value;
-            const float* src = fin + (long long)i * g.A + k0 - g.soff(i) - win_shift(i);
-            tma_load_1d(dst + i * kWin, src, kWin * 4u, &full[s]);
+            // the window may straddle a CSoA block boundary: two segments
+            const unsigned long long a0 = (unsigned long long)(k0 - g.soff(i) - win_shift(i));
+            const unsigned long long e0 = (a0 | g.amask) + 1ull;
+            const unsigned l0 = e0 - a0 < (unsigned long long)kWin ? unsigned(e0 - a0) : unsigned(kWin);
+            tma_load_1d(dst + i * kWin, fin + g.gaddr(a0, i), l0 * 4u, &full[s]);
+            if (l0 < unsigned(kWin))
+                tma_load_1d(dst + i * kWin + l0, fin + g.gaddr(e0, i), (kWin - l0) * 4u, &full[s]);
         });
     };
     // consumer release: the last warp to finish reading a stage refills it
@@ -535,14 +543,14 @@ __global__ void __launch_bounds__(kBulkThreads, 4)
         const unsigned tile = stage_tile[s];
         if (tile >= ntiles) break;
         const unsigned m = 2u * tid;
-        const unsigned sl = sb + tile * kTile + m;  // storage slot of the pair's first node
-        const unsigned row = g.div_px.div(sl);
-        const int col = int(sl - row * g.PX);
+        const unsigned sl = org + tile * kTile + m;  // storage slot of the pair's first node
+        const unsigned row = g.div_px.div(sl - g.base);
+        const int col = int(sl - g.base - row * g.PX);
         const unsigned pl = g.div_py.div(row);
         const int r = int(row - pl * g.PY);
         const int x = col - 2, y = r - 1, lz = int(pl) - 1;
         // pairs are all-ghost or all-owned (nx, PX even)
-        const bool valid = sl < se && x >= 0 && x < g.nx && y >= 0;
+        const bool valid = sl >= sb && sl < se && x >= 0 && x < g.nx && y >= 0;
         float2 fs[27];
         static_for<0, 27>([&](auto I) {
             constexpr int i = decltype(I)::value;
@@ -561,11 +569,11 @@ __global__ void __launch_bounds__(kBulkThreads, 4)
             }
         }
         if (!valid) continue;
-        if (dbg) {  // bandwidth probes: 1 = staged loads only, 2 = loads + stores (no collision)
-            if (dbg == 2)
+        if (dbg & 3) {  // bandwidth probes: 1 = staged loads only, 2 = loads + stores (no collision)
+            if ((dbg & 3) == 2)
                 static_for<0, 27>([&](auto I) {
                     constexpr int i = decltype(I)::value;
-                    *reinterpret_cast<float2*>(fout + size_t(i) * g.A + sl) = fs[i];
+                    *reinterpret_cast<float2*>(fout + g.gaddr(sl, i)) = fs[i];
                 });
             else if (fs[0].x == 12345.f)
                 fout[sl] = fs[26].y;
@@ -600,9 +608,10 @@ __global__ void __launch_bounds__(kBulkThreads, 4)
         const bool any_force = gx.x != 0.f || gx.y != 0.f || gy.x != 0.f || gy.y != 0.f || gz.x != 0.f || gz.y != 0.f;
         NoStash<float2> stash;
         collide_v<KIND, POLICY, STD, float2>(fs, mc, gx, gy, gz, any_force, P.m, stash);
+        float* const ob = fout + g.gaddr(sl, 0);  // a tile never straddles a CSoA block
         static_for<0, 27>([&](auto I) {
             constexpr int i = decltype(I)::value;
-            *reinterpret_cast<float2*>(fout + size_t(i) * g.A + sl) = fs[i];
+            *reinterpret_cast<float2*>(ob + size_t(i) * g.A) = fs[i];
         });
         // crossing populations of the slab's boundary planes -> neighbour halos
         const unsigned hp = unsigned(y) * g.nx + unsigned(x);
@@ -751,7 +760,7 @@ template <int KIND, int POLICY, bool STD>
 void launch_ghost_planes(const FluidParams& P, int z_a, int z_b, int slot, int write_macro, cudaStream_t st) {
     if (z_b <= z_a) return;
     const RegionGeo& g = P.g;
-    const unsigned ntiles = (unsigned(z_b - z_a) * g.PP + kTile - 1) / kTile;
+    const unsigned ntiles = unsigned(z_b - z_a) * g.PP / kTile + 2;
     static int grid_per_sm = -1, sms = 0;
     auto kern = fluid_ghost_kernel<KIND, POLICY, STD>;
     if (grid_per_sm < 0) {

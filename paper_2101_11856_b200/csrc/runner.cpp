@@ -4,6 +4,7 @@
 #include "runner.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 namespace lbmg {
@@ -187,16 +188,36 @@ void Runner::compute_geo(Region& r) const {
     g.div_nx = FastDiv(unsigned(nx_));
     g.div_ny = FastDiv(unsigned(ny_));
     g.ghost = 0;
-    if (g.la == 31 && nx_ % 4 == 0 && ghost_layout_enabled()) {
-        // ghost-layer SoA (device_common.cuh): pitch nx+4, ny+1 rows, planes -1..nzl
+    if (nx_ % 4 == 0 && ghost_layout_enabled()) {
+        // ghost-layer layout (device_common.cuh): pitch nx+4, ny+1 rows,
+        // planes -1..nzl, CSoA blocks of alpha >= 256 slots (one staged tile
+        // writes one contiguous 27 KB block); alpha >= slots is SoA
         g.ghost = 1;
         g.PX = unsigned(nx_) + 4u;
         g.PY = unsigned(ny_) + 1u;
         g.PP = g.PX * g.PY;
         g.div_px = FastDiv(g.PX);
         g.div_py = FastDiv(g.PY);
-        g.n_pad = round_up(unsigned(g.nzl + 2) * g.PP + g.PX + 64u, 32);
-        g.A = g.n_pad;
+        // a tile's windows reach off_max + 3 = PP + PX + 4 slots below its
+        // first slot and kWin - 1 - off_min above its last one
+        g.base = round_up(g.PX + 264u, 256u);
+        const unsigned slots = round_up(g.base + unsigned(g.nzl + 2) * g.PP + g.PX + 1024u, 256u);
+        size_t areq = layout_.alpha_req;
+        if (const char* e = std::getenv("LBMG_GHOST_ALPHA")) areq = std::strtoull(e, nullptr, 10);  // layout probes
+        // alpha below one 256-slot tile (incl. the reference default 1) has no
+        // device benefit: SoA; otherwise Eq. 9 blocks of next_pow2(alpha)
+        const size_t ga = next_pow2(std::max<size_t>(areq, 256));
+        if (areq < 256 || ga >= slots) {
+            g.la = 31;
+            g.amask = 0x7fffffffu;
+            g.n_pad = slots;
+            g.A = slots;
+        } else {
+            g.la = log2i(ga);
+            g.amask = unsigned(ga - 1);
+            g.n_pad = round_up(slots, unsigned(ga));
+            g.A = unsigned(ga);
+        }
     }
 }
 

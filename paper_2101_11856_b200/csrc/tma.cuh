@@ -38,13 +38,17 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// try_wait suspends the warp until the phase completes or this many ns
+// pass, instead of spinning on issue slots the computing warps need.
+constexpr unsigned kSuspendHintNs = 100000;
+
 __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(kSuspendHintNs)
         : "memory");
 }
 
