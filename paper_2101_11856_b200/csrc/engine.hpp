@@ -41,7 +41,7 @@ inline unsigned long long f_alloc_floats(const RegionGeo& g) {
 bool ghost_layout_enabled();
 
 // part: 0 every node, 1 the two halo planes (edge), 2 everything else (bulk)
-void launch_fluid(const FluidParams& P, int part, int write_macro, cudaStream_t st);
+void launch_fluid(const FluidParams& P, int part, int write_macro, cudaStream_t st, bool fill = true);
 void launch_macro(const FluidParams& P, int parity, cudaStream_t st);
 void launch_ib_mark(const FluidParams& P, const IbSolidDev& S, unsigned* stamp, unsigned* band,
                     cudaStream_t st);
@@ -49,6 +49,11 @@ void launch_ib_band(const FluidParams& P, const unsigned* band, int sm_count, cu
 void launch_macro_pack(const FluidParams& P, cudaStream_t st);
 void launch_ib_spread(const FluidParams& P, const IbSolidDev& S, cudaStream_t st);
 int totals_blocks(size_t n);
+// single-region ghost-layout IB step (interp + penalty + scatter + totals + motion), after launch_ghost_fill
+int fused_blocks(size_t n);
+void launch_ib_fused(const FluidParams& P, const IbSolidDev& S, const double* table, double* partial, unsigned* done,
+                     double* out_base, int stride, bool moving, cudaStream_t st);
+void launch_ghost_fill(const FluidParams& P, cudaStream_t st);
 // table: motion rows per step from DevCounters::chunk_t0; stride in doubles per step
 void launch_ib_totals(const FluidParams& P, const IbSolidDev& S, const double* table, double* partial,
                       double* out_base, int stride, cudaStream_t st);

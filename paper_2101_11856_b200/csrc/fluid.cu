@@ -434,9 +434,84 @@ __device__ __forceinline__ const float* pull_source(const FluidParams& P, int p,
     return &P.faces.inlet[0][0];  // unreachable: the owner strictly decreases along the chain
 }
 
+// One thread per node of a slab face (faces 0..5 in order, contiguous ranges):
+// the 9 directions crossing that face, resolved at compile time.  The common
+// case — the pull is owned by this face itself (or streams periodically) —
+// takes the face's uniform rule directly; edges owned by an earlier face and
+// outflow chains take the general pull_source().  All 9 loads are independent.
+template <int F>
+__device__ __forceinline__ void ghost_fill_face(const FluidParams& P, int p, int x, int y, int lz) {
+    const RegionGeo& g = P.g;
+    constexpr int axis = face_axis(F), side = face_side(F);
+    const int gz = g.gz0 + lz;
+    const int cond = P.faces.cond[F];
+    const float* fin = P.p.f[p];
+    float* fw = P.p.f[p];
+    const unsigned sl = g.sidx(x, y, lz);
+    float val[9];
+    int own_of[9];
+    static_for<1, 27>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        if constexpr (cc(i, axis) == -side) {
+            constexpr int j = cross9(i, axis);
+            const int own = owner_face_c<i>(g, x, y, gz);
+            own_of[j] = own;
+            const float* src;
+            if (own == F && cond == kNoSlip) src = fin + g.gaddr(sl, opposite(i));
+            else if (own == F && cond == kInlet) src = &P.faces.inlet[F][i];
+            else src = pull_source(P, p, x, y, lz, i);  // wraps, halos, outflow chains, edges
+            val[j] = *src;
+        }
+    });
+    static_for<1, 27>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        if constexpr (cc(i, axis) == -side) {
+            constexpr int j = cross9(i, axis);
+            fw[g.gaddr((unsigned long long)((long long)sl - g.soff(i)), i)] = val[j];
+            const int own = own_of[j];
+            if (own != kNoOwner) P.p.slot[p ^ 1][own][g.slot_index(own, x, y, lz, i)] = val[j];
+        }
+    });
+}
+
+__global__ void __launch_bounds__(256) ghost_fill_kernel(const __grid_constant__ FluidParams P) {
+    DevCounters* ctr = P.ctr;
+    if (blockIdx.x == 0 && threadIdx.x < 3) ctr->tile_ctr[threadIdx.x] = 0u;  // this step's tile queues
+    if (ctr->diverged) return;
+    const RegionGeo& g = P.g;
+    const unsigned Fx = unsigned(g.ny) * g.nzl, Fy = unsigned(g.nx) * g.nzl, Fz = g.plane;
+    unsigned q = blockIdx.x * blockDim.x + threadIdx.x;
+    const int p = int(ctr->t & 1);
+    if (q < 2 * Fx) {
+        const int f = q < Fx ? 0 : 1;
+        q -= f * Fx;
+        const int y = int(q % unsigned(g.ny)), lz = int(q / unsigned(g.ny));
+        if (f == 0) ghost_fill_face<0>(P, p, 0, y, lz);
+        else ghost_fill_face<1>(P, p, g.nx - 1, y, lz);
+        return;
+    }
+    q -= 2 * Fx;
+    if (q < 2 * Fy) {
+        const int f = q < Fy ? 0 : 1;
+        q -= f * Fy;
+        const int x = int(q % unsigned(g.nx)), lz = int(q / unsigned(g.nx));
+        if (f == 0) ghost_fill_face<2>(P, p, x, 0, lz);
+        else ghost_fill_face<3>(P, p, x, g.ny - 1, lz);
+        return;
+    }
+    q -= 2 * Fy;
+    if (q < 2 * Fz) {
+        const int f = q < Fz ? 0 : 1;
+        q -= f * Fz;
+        const int x = int(q % unsigned(g.nx)), y = int(q / unsigned(g.nx));
+        if (f == 0) ghost_fill_face<4>(P, p, x, y, 0);
+        else ghost_fill_face<5>(P, p, x, y, g.nzl - 1);
+    }
+}
+
 // Entries: for faces f = 0..5 of the slab, direction slot j = 0..8 (slowest)
 // and the face's nodes (fastest, so consecutive threads walk rows).
-__global__ void __launch_bounds__(256) ghost_fill_kernel(const __grid_constant__ FluidParams P) {
+__global__ void __launch_bounds__(256) ghost_fill_dir_kernel(const __grid_constant__ FluidParams P) {
     DevCounters* ctr = P.ctr;
     if (blockIdx.x == 0 && threadIdx.x < 3) ctr->tile_ctr[threadIdx.x] = 0u;  // this step's tile queues
     if (ctr->diverged) return;
@@ -456,13 +531,16 @@ __global__ void __launch_bounds__(256) ghost_fill_kernel(const __grid_constant__
     int x, y, lz, c[3];
     const int ja = int(j % 3) - 1, jb = int(j / 3) - 1;  // cross9 order: lower axis fastest
     if (axis == 0) {
-        y = int(q % unsigned(g.ny)); lz = int(q / unsigned(g.ny)); x = side < 0 ? 0 : g.nx - 1;
+        const unsigned qq = g.div_ny.div(q);
+        y = int(q - qq * unsigned(g.ny)); lz = int(qq); x = side < 0 ? 0 : g.nx - 1;
         c[0] = -side; c[1] = ja; c[2] = jb;
     } else if (axis == 1) {
-        x = int(q % unsigned(g.nx)); lz = int(q / unsigned(g.nx)); y = side < 0 ? 0 : g.ny - 1;
+        const unsigned qq = g.div_nx.div(q);
+        x = int(q - qq * unsigned(g.nx)); lz = int(qq); y = side < 0 ? 0 : g.ny - 1;
         c[0] = ja; c[1] = -side; c[2] = jb;
     } else {
-        x = int(q % unsigned(g.nx)); y = int(q / unsigned(g.nx)); lz = side < 0 ? 0 : g.nzl - 1;
+        const unsigned qq = g.div_nx.div(q);
+        x = int(q - qq * unsigned(g.nx)); y = int(qq); lz = side < 0 ? 0 : g.nzl - 1;
         c[0] = ja; c[1] = jb; c[2] = -side;
     }
     const int i = tensor_dir((c[0] + 1) + 3 * (c[1] + 1) + 9 * (c[2] + 1));
@@ -756,6 +834,8 @@ bool ghost_layout_enabled() {
 
 namespace {
 
+thread_local bool t_fill = true;  // launch_fluid(..., fill): the ghost fill is part of this launch
+
 template <int KIND, int POLICY, bool STD>
 void launch_ghost_planes(const FluidParams& P, int z_a, int z_b, int slot, int write_macro, cudaStream_t st) {
     if (z_b <= z_a) return;
@@ -786,10 +866,7 @@ void launch_ghost_planes(const FluidParams& P, int z_a, int z_b, int slot, int w
 template <int KIND, int POLICY, bool STD>
 void launch_fluid_ghost(const FluidParams& P, int part, int write_macro, cudaStream_t st) {
     const RegionGeo& g = P.g;
-    if (part == 0 || part == 1) {
-        const unsigned entries = 9u * 2u * (unsigned(g.ny) * g.nzl + unsigned(g.nx) * g.nzl + g.plane);
-        ghost_fill_kernel<<<blocks_for(entries, 256), 256, 0, st>>>(P);
-    }
+    if ((part == 0 || part == 1) && t_fill) launch_ghost_fill(P, st);
     if (part == 0) {
         launch_ghost_planes<KIND, POLICY, STD>(P, 0, g.nzl, 0, write_macro, st);
     } else if (part == 1) {
@@ -850,7 +927,19 @@ void launch_fluid_form(const FluidParams& P, int part, int write_macro, cudaStre
 }  // namespace
 
 // part: 0 every node, 1 the two halo planes (edge), 2 the rest (bulk).
-void launch_fluid(const FluidParams& P, int part, int write_macro, cudaStream_t st) {
+void launch_ghost_fill(const FluidParams& P, cudaStream_t st) {
+    const RegionGeo& g = P.g;
+    static const bool per_node = [] {
+        const char* e = std::getenv("LBMG_FILL");
+        return e && std::string(e) == "node";
+    }();
+    const unsigned nodes = 2u * (unsigned(g.ny) * g.nzl + unsigned(g.nx) * g.nzl + g.plane);
+    if (per_node) ghost_fill_kernel<<<blocks_for(nodes, 256), 256, 0, st>>>(P);
+    else ghost_fill_dir_kernel<<<blocks_for(9ull * nodes, 256), 256, 0, st>>>(P);
+}
+
+void launch_fluid(const FluidParams& P, int part, int write_macro, cudaStream_t st, bool fill) {
+    t_fill = fill;
     switch (fluid_form()) {
         case 0: launch_fluid_form<0>(P, part, write_macro, st); break;
         case 1: launch_fluid_form<1>(P, part, write_macro, st); break;

@@ -291,6 +291,136 @@ __global__ void ib_motion_once_kernel(IbSolidDev S, const double* row, int nx, i
 }
 
 // ---------------------------------------------------------------------------
+// Fused IB step for a single-region run on the ghost layout (no seams), after
+// the ghost fill: one warp per sample.  Lane = corner * 4 + sub: the four
+// lanes of a corner pull 7/6 of its 27 post-BC populations f* straight from
+// the ghost-layer storage (every pull is a plain shifted read there) and
+// reduce rho*, j* by shuffles — the band pre-pass without a band list.  Then
+// interpolation (ib.cpp:321-343, FP64), penalty (ib.cpp:345-365), scatter
+// (ib.cpp:369-454, atomic mode: one lane per corner, fp32 RED into g), the
+// reaction totals (ib.cpp:491-501: per-block FP64 partials, the last block
+// sums them in block order -> deterministic) and, for moving solids, the
+// rigid motion to t+1 (ib.cpp:456-489).
+constexpr int kFusedWarps = 8;
+
+__global__ void __launch_bounds__(kFusedWarps * 32)
+    ib_fused_kernel(const __grid_constant__ FluidParams P, IbSolidDev S, const double* table, double* partial,
+                    unsigned* done, double* out_base, int stride, int moving) {
+    __shared__ double red[kFusedWarps][6];
+    __shared__ bool last;
+    DevCounters* ctr = P.ctr;
+    if (ctr->diverged) return;
+    const RegionGeo& g = P.g;
+    const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const unsigned s = blockIdx.x * kFusedWarps + warp;
+    const int corner = int(lane >> 2), sub = int(lane & 3u);
+    const double* row = table + (ctr->t - ctr->chunk_t0) * kMotionRow;
+    double tot[6] = {0, 0, 0, 0, 0, 0};
+    if (s < S.n) {
+        const double pos[3] = {S.pos[3 * s], S.pos[3 * s + 1], S.pos[3 * s + 2]};
+        const double ub[3] = {S.ub[3 * s], S.ub[3 * s + 1], S.ub[3 * s + 2]};  // (issued early)
+        const Support ks = kernel_support(pos, g.nx, g.ny, g.NZ);
+        if (lane == 0) S.flagged[s] = ks.inside ? 0 : 1;
+        double us[3] = {0.0, 0.0, 0.0}, fg[3] = {0.0, 0.0, 0.0};
+        if (ks.inside) {  // (single region: every support lies in the slab)
+            const int ox = corner & 1, oy = (corner >> 1) & 1, oz = corner >> 2;
+            const int x = ks.base[0] + ox, y = ks.base[1] + oy, lz = ks.base[2] + oz - g.gz0;
+            const float* fin = P.p.f[ctr->t & 1];
+            const long long sl = g.sidx(x, y, lz);
+            float v[7];
+#pragma unroll
+            for (int j = 0; j < 7; ++j) {  // all seven loads in flight at once
+                const int i = sub + 4 * j;
+                v[j] = i < 27 ? __ldcg(&fin[g.gaddr((unsigned long long)(sl - g.soff(i)), i)]) : 0.f;
+            }
+            float r = 0.f, jx = 0.f, jy = 0.f, jz = 0.f;
+#pragma unroll
+            for (int j = 0; j < 7; ++j) {
+                const int i = sub + 4 * j;
+                r += v[j];
+                jx += float(cx(i)) * v[j];
+                jy += float(cy(i)) * v[j];
+                jz += float(cz(i)) * v[j];
+            }
+#pragma unroll
+            for (int o = 1; o < 4; o <<= 1) {
+                r += __shfl_xor_sync(0xffffffffu, r, o);
+                jx += __shfl_xor_sync(0xffffffffu, jx, o);
+                jy += __shfl_xor_sync(0xffffffffu, jy, o);
+                jz += __shfl_xor_sync(0xffffffffu, jz, o);
+            }
+            const float rho = 1.0f + r;
+            const float inv = 1.0f / rho;
+            const double wx = ox ? ks.w[0][1] : ks.w[0][0], wy = oy ? ks.w[1][1] : ks.w[1][0];
+            const double wz = oz ? ks.w[2][1] : ks.w[2][0];
+            const double w = __dmul_rn(__dmul_rn(wx, wy), wz);
+            double c4[4] = {sub == 0 ? w * double(jx * inv) : 0.0, sub == 0 ? w * double(jy * inv) : 0.0,
+                            sub == 0 ? w * double(jz * inv) : 0.0, sub == 0 ? w * double(rho) : 0.0};
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+                for (int a = 0; a < 4; ++a) c4[a] += __shfl_xor_sync(0xffffffffu, c4[a], o);
+            for (int a = 0; a < 3; ++a) {
+                us[a] = c4[a];
+                fg[a] = c4[3] * (ub[a] - us[a]);
+            }
+            if (sub == 0) {  // scatter of this corner (owned: single region)
+                const unsigned k = g.node(x, y, lz);
+                atomicAdd(&P.p.gib[k], float(w * fg[0]));
+                atomicAdd(&P.p.gib[k + g.ns], float(w * fg[1]));
+                atomicAdd(&P.p.gib[k + 2u * g.ns], float(w * fg[2]));
+                P.p.tflag[k >> 5] = 1;
+            }
+        }
+        if (lane == 0) {
+            for (int a = 0; a < 3; ++a) {
+                S.sampled[3 * s + a] = us[a];
+                S.force[3 * s + a] = fg[a];
+            }
+            if (pos[2] >= double(g.gz0) && pos[2] < double(g.gz0 + g.nzl)) {
+                const double rr[3] = {pos[0] - row[0], pos[1] - row[1], pos[2] - row[2]};
+                tot[0] = -fg[0];
+                tot[1] = -fg[1];
+                tot[2] = -fg[2];
+                tot[3] = -(rr[1] * fg[2] - rr[2] * fg[1]);
+                tot[4] = -(rr[2] * fg[0] - rr[0] * fg[2]);
+                tot[5] = -(rr[0] * fg[1] - rr[1] * fg[0]);
+            }
+            if (moving) motion_apply(row + kMotionRow, S, s, g.nx, g.ny, g.NZ);
+        }
+    }
+    if (lane == 0)
+        for (int a = 0; a < 6; ++a) red[warp][a] = tot[a];
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        double acc = 0.0;
+        for (int w = 0; w < kFusedWarps; ++w) acc += red[w][threadIdx.x];
+        partial[blockIdx.x * 6 + threadIdx.x] = acc;
+        __threadfence();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // fixed-order sum of the block partials: thread t takes blocks t, t+T, ...,
+    // then a shared-memory tree (independent of which block finished last)
+    __shared__ double tree[6][kFusedWarps * 32];
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+        for (int a = 0; a < 6; ++a) acc[a] += __ldcg(&partial[b * 6 + a]);
+    for (int a = 0; a < 6; ++a) tree[a][threadIdx.x] = acc[a];
+    __syncthreads();
+    for (unsigned off = blockDim.x / 2; off > 0; off >>= 1) {
+        if (threadIdx.x < off)
+            for (int a = 0; a < 6; ++a) tree[a][threadIdx.x] += tree[a][threadIdx.x + off];
+        __syncthreads();
+    }
+    if (threadIdx.x < 6) out_base[(ctr->t - ctr->chunk_t0) * stride + threadIdx.x] = tree[threadIdx.x][0];
+    if (threadIdx.x == 0) *done = 0u;
+}
+
+// ---------------------------------------------------------------------------
 // init_fields (runner.cpp:60-107): equilibrium f (both the f(0) buffer and
 // the face slots, which stand in for the initial f_star), rho, u.
 
@@ -430,6 +560,13 @@ void launch_ib_spread(const FluidParams& P, const IbSolidDev& S, cudaStream_t st
     else ib_spread_kernel<false><<<blocks_for(S.n, kSpreadThreads), kSpreadThreads, 0, st>>>(P, S);
 }
 
+int fused_blocks(size_t n) { return int((n + kFusedWarps - 1) / kFusedWarps); }
+void launch_ib_fused(const FluidParams& P, const IbSolidDev& S, const double* table, double* partial, unsigned* done,
+                     double* out_base, int stride, bool moving, cudaStream_t st) {
+    if (S.n == 0) return;
+    ib_fused_kernel<<<fused_blocks(S.n), kFusedWarps * 32, 0, st>>>(P, S, table, partial, done, out_base, stride,
+                                                                     moving ? 1 : 0);
+}
 int totals_blocks(size_t n) {
     size_t b = (n + kTotThreads - 1) / kTotThreads;
     return int(b < 1 ? 1 : (b > 256 ? 256 : b));

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 
 namespace lbmg {
 
@@ -243,6 +244,10 @@ void Runner::build_regions(int) {
             r.band = static_cast<unsigned*>(dalloc(sizeof(unsigned) * cap));
             r.ptr.band_count = static_cast<unsigned*>(dalloc(sizeof(unsigned)));
             r.partial = static_cast<double*>(dalloc(sizeof(double) * 6 * 256));
+            size_t nmax = 1;
+            for (const auto& so : scene_.solids) nmax = std::max(nmax, so.samples.size());
+            r.fused_partial = static_cast<double*>(dalloc(sizeof(double) * 6 * size_t(fused_blocks(nmax))));
+            r.fused_done = static_cast<unsigned*>(dalloc(sizeof(unsigned)));
         }
         for (int f = 0; f < 6; ++f) {
             const int a = face_axis(f);
@@ -458,15 +463,40 @@ void Runner::enqueue_fluid(bool write_macro, int part) {
     }
 }
 
+// Single region on the ghost layout: ghost fill first, then one fused IB
+// kernel per solid (no band list, no seams), then the fluid kernel.
+bool Runner::fused_ib() const {
+    static const bool off = [] {
+        const char* e = std::getenv("LBMG_IB_FUSED");
+        return e && std::string(e) == "0";
+    }();
+    return has_solids_ && !off && !rank_mode_ && regions_.size() == 1 && regions_[0].geo.ghost;
+}
+
 void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
     cudaStream_t st = stream();
     if (ev) CK(cudaEventRecord((*ev)[0], st));
-    if (has_solids_) {
+    const bool fused = fused_ib();
+    if (fused) {
+        Region& r = regions_[0];
+        FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+        launch_ghost_fill(P, st);
+        const int ns = int(scene_.solids.size());
+        for (int s = 0; s < ns; ++s)
+            launch_ib_fused(P, r.solids[s], motion_tab_ + size_t(s) * (cap_ + 2) * kMotionRow, r.fused_partial,
+                            r.fused_done, totals_dev_ + size_t(s) * 6, ns * 6, moving_[s] != 0, st);
+    } else if (has_solids_) {
         enqueue_ib_pre();
         enqueue_ib_mid();
     }
     if (ev) CK(cudaEventRecord((*ev)[1], st));
-    enqueue_fluid(write_macro, 0);
+    if (fused) {
+        Region& r = regions_[0];
+        FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+        launch_fluid(P, 0, write_macro, st, false);
+    } else {
+        enqueue_fluid(write_macro, 0);
+    }
     if (has_solids_)
         for (auto& r : regions_) CK(cudaMemsetAsync(r.ptr.tflag, 0, r.geo.ns / 32 + 1, st));
     launch_step_end(ctr_, st);

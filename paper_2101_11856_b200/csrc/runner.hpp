@@ -106,6 +106,8 @@ private:
         unsigned* stamp = nullptr;
         unsigned* band = nullptr;
         double* partial = nullptr;
+        double* fused_partial = nullptr;  // fused IB: per-block totals
+        unsigned* fused_done = nullptr;
         std::vector<IbSolidDev> solids;
         FluidParams params() const;
     };
@@ -123,6 +125,7 @@ private:
     void enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev);
     void enqueue_ib_pre();
     void enqueue_ib_mid();
+    bool fused_ib() const;
     void enqueue_fluid(bool write_macro, int part);
     void invalidate_graphs();
     void finish_chunk(long t0, long requested);
