@@ -72,6 +72,8 @@ struct RegionGeo {
     int ghost;
     unsigned PX, PY, PP;  // row pitch, rows per plane, PX * PY
     unsigned base;        // leading pad (a multiple of 256 slots)
+    int zwrap;            // the slab is its own z neighbour (one periodic region)
+    int has_outflow;      // some face is an outflow face (face slots are read)
     FastDiv div_px, div_py;
 
     LBMG_HD unsigned sidx(int x, int y, int lz) const {
@@ -164,6 +166,7 @@ struct DevCounters {
     long long diverged_step;   // step at which divergence was detected
     long long chunk_t0;        // first step of the current advance chunk
     unsigned tile_ctr[4];      // tile queues of the staged fluid launches of a step
+    unsigned tile_done[4];     // CTAs finished per queue (the last one rewinds it)
 };
 
 struct FluidParams {

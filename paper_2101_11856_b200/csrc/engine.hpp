@@ -53,7 +53,9 @@ int totals_blocks(size_t n);
 int fused_blocks(size_t n);
 void launch_ib_fused(const FluidParams& P, const IbSolidDev& S, const double* table, double* partial, unsigned* done,
                      double* out_base, int stride, bool moving, cudaStream_t st);
-void launch_ghost_fill(const FluidParams& P, cudaStream_t st);
+// ghost slots of this step: full = every entry (after init / relayout),
+// otherwise only what the previous fluid step did not push
+void launch_ghost_fill(const FluidParams& P, cudaStream_t st, bool full = false);
 // table: motion rows per step from DevCounters::chunk_t0; stride in doubles per step
 void launch_ib_totals(const FluidParams& P, const IbSolidDev& S, const double* table, double* partial,
                       double* out_base, int stride, cudaStream_t st);

@@ -434,44 +434,57 @@ __device__ __forceinline__ const float* pull_source(const FluidParams& P, int p,
     return &P.faces.inlet[0][0];  // unreachable: the owner strictly decreases along the chain
 }
 
-// One thread per node of a slab face (faces 0..5 in order, contiguous ranges):
-// the 9 directions crossing that face, resolved at compile time.  The common
-// case — the pull is owned by this face itself (or streams periodically) —
-// takes the face's uniform rule directly; edges owned by an earlier face and
-// outflow chains take the general pull_source().  All 9 loads are independent.
+// One thread per (slab-face node, crossing direction) entry; faces 0..5 in
+// order, direction slot j (the two other velocity components, cross9 order)
+// slowest, so consecutive threads walk a face row.  Common rules inline —
+// bounce-back (f*_i = f_{i'}(N), boundary.cpp:98-100), inlet
+// (feq(1, u_in)_i), periodic wrap / z halo (plain pull) — the outflow chain
+// through pull_source().
 template <int F>
-__device__ __forceinline__ void ghost_fill_face(const FluidParams& P, int p, int x, int y, int lz) {
+__device__ __forceinline__ void ghost_fill_entry(const FluidParams& P, int p, unsigned q, unsigned j) {
     const RegionGeo& g = P.g;
-    constexpr int axis = face_axis(F), side = face_side(F);
-    const int gz = g.gz0 + lz;
-    const int cond = P.faces.cond[F];
-    const float* fin = P.p.f[p];
-    float* fw = P.p.f[p];
-    const unsigned sl = g.sidx(x, y, lz);
-    float val[9];
-    int own_of[9];
-    static_for<1, 27>([&](auto I) {
-        constexpr int i = decltype(I)::value;
-        if constexpr (cc(i, axis) == -side) {
-            constexpr int j = cross9(i, axis);
-            const int own = owner_face_c<i>(g, x, y, gz);
-            own_of[j] = own;
-            const float* src;
-            if (own == F && cond == kNoSlip) src = fin + g.gaddr(sl, opposite(i));
-            else if (own == F && cond == kInlet) src = &P.faces.inlet[F][i];
-            else src = pull_source(P, p, x, y, lz, i);  // wraps, halos, outflow chains, edges
-            val[j] = *src;
+    constexpr int A = face_axis(F), S = face_side(F);
+    int x, y, lz;
+    if constexpr (A == 0) {
+        const unsigned qq = g.div_ny.div(q);
+        y = int(q - qq * unsigned(g.ny));
+        lz = int(qq);
+        x = S < 0 ? 0 : g.nx - 1;
+    } else {
+        const unsigned qq = g.div_nx.div(q);
+        x = int(q - qq * unsigned(g.nx));
+        if constexpr (A == 1) {
+            lz = int(qq);
+            y = S < 0 ? 0 : g.ny - 1;
+        } else {
+            y = int(qq);
+            lz = S < 0 ? 0 : g.nzl - 1;
         }
-    });
-    static_for<1, 27>([&](auto I) {
-        constexpr int i = decltype(I)::value;
-        if constexpr (cc(i, axis) == -side) {
-            constexpr int j = cross9(i, axis);
-            fw[g.gaddr((unsigned long long)((long long)sl - g.soff(i)), i)] = val[j];
-            const int own = own_of[j];
-            if (own != kNoOwner) P.p.slot[p ^ 1][own][g.slot_index(own, x, y, lz, i)] = val[j];
-        }
-    });
+    }
+    const int ja = int(j % 3u) - 1, jb = int(j / 3u) - 1;
+    const int c0 = A == 0 ? -S : ja, c1 = A == 0 ? ja : (A == 1 ? -S : jb), c2 = A == 2 ? -S : jb;
+    const int i = tensor_dir((c0 + 1) + 3 * (c1 + 1) + 9 * (c2 + 1));
+    const int own = owner_face(g, x, y, g.gz0 + lz, i);
+    const unsigned sn = g.sidx(x, y, lz);
+    float* fin = P.p.f[p];
+    float val;
+    if (own == kNoOwner) {  // periodic wrap in x/y, z halo
+        int sx = x - c0, sy = y - c1;
+        sx += sx < 0 ? g.nx : (sx >= g.nx ? -g.nx : 0);
+        sy += sy < 0 ? g.ny : (sy >= g.ny ? -g.ny : 0);
+        const int lzs = lz - c2;
+        const unsigned hp = cross9(i, 2) * g.plane + unsigned(sy) * g.nx + unsigned(sx);
+        if (lzs < 0) val = P.p.recv_lo[p][hp];
+        else if (lzs >= g.nzl) val = P.p.recv_hi[p][hp];
+        else val = fin[g.gaddr(g.sidx(sx, sy, lzs), i)];
+    } else {
+        const int cond = P.faces.cond[own];
+        if (cond == kNoSlip) val = fin[g.gaddr(sn, 27 - i)];
+        else if (cond == kInlet) val = P.faces.inlet[own][i];
+        else val = *pull_source(P, p, x, y, lz, i);
+        P.p.slot[p ^ 1][own][g.slot_index(own, x, y, lz, i)] = val;
+    }
+    fin[g.gaddr((unsigned long long)((long long)sn - g.soff(i)), i)] = val;
 }
 
 __global__ void __launch_bounds__(256) ghost_fill_kernel(const __grid_constant__ FluidParams P) {
@@ -480,76 +493,25 @@ __global__ void __launch_bounds__(256) ghost_fill_kernel(const __grid_constant__
     if (ctr->diverged) return;
     const RegionGeo& g = P.g;
     const unsigned Fx = unsigned(g.ny) * g.nzl, Fy = unsigned(g.nx) * g.nzl, Fz = g.plane;
-    unsigned q = blockIdx.x * blockDim.x + threadIdx.x;
-    const int p = int(ctr->t & 1);
-    if (q < 2 * Fx) {
-        const int f = q < Fx ? 0 : 1;
-        q -= f * Fx;
-        const int y = int(q % unsigned(g.ny)), lz = int(q / unsigned(g.ny));
-        if (f == 0) ghost_fill_face<0>(P, p, 0, y, lz);
-        else ghost_fill_face<1>(P, p, g.nx - 1, y, lz);
-        return;
-    }
-    q -= 2 * Fx;
-    if (q < 2 * Fy) {
-        const int f = q < Fy ? 0 : 1;
-        q -= f * Fy;
-        const int x = int(q % unsigned(g.nx)), lz = int(q / unsigned(g.nx));
-        if (f == 0) ghost_fill_face<2>(P, p, x, 0, lz);
-        else ghost_fill_face<3>(P, p, x, g.ny - 1, lz);
-        return;
-    }
-    q -= 2 * Fy;
-    if (q < 2 * Fz) {
-        const int f = q < Fz ? 0 : 1;
-        q -= f * Fz;
-        const int x = int(q % unsigned(g.nx)), y = int(q / unsigned(g.nx));
-        if (f == 0) ghost_fill_face<4>(P, p, x, y, 0);
-        else ghost_fill_face<5>(P, p, x, y, g.nzl - 1);
-    }
-}
-
-// Entries: for faces f = 0..5 of the slab, direction slot j = 0..8 (slowest)
-// and the face's nodes (fastest, so consecutive threads walk rows).
-__global__ void __launch_bounds__(256) ghost_fill_dir_kernel(const __grid_constant__ FluidParams P) {
-    DevCounters* ctr = P.ctr;
-    if (blockIdx.x == 0 && threadIdx.x < 3) ctr->tile_ctr[threadIdx.x] = 0u;  // this step's tile queues
-    if (ctr->diverged) return;
-    const RegionGeo& g = P.g;
-    const unsigned Fx = unsigned(g.ny) * g.nzl, Fy = unsigned(g.nx) * g.nzl, Fz = g.plane;
     unsigned e = blockIdx.x * blockDim.x + threadIdx.x;
-    int f = 0;
-    unsigned F = Fx;
-    for (; f < 6; ++f) {
-        F = f < 2 ? Fx : (f < 4 ? Fy : Fz);
-        if (e < 9u * F) break;
-        e -= 9u * F;
-    }
-    if (f == 6) return;
-    const unsigned j = e / F, q = e - j * F;
-    const int axis = face_axis(f), side = face_side(f);
-    int x, y, lz, c[3];
-    const int ja = int(j % 3) - 1, jb = int(j / 3) - 1;  // cross9 order: lower axis fastest
-    if (axis == 0) {
-        const unsigned qq = g.div_ny.div(q);
-        y = int(q - qq * unsigned(g.ny)); lz = int(qq); x = side < 0 ? 0 : g.nx - 1;
-        c[0] = -side; c[1] = ja; c[2] = jb;
-    } else if (axis == 1) {
-        const unsigned qq = g.div_nx.div(q);
-        x = int(q - qq * unsigned(g.nx)); lz = int(qq); y = side < 0 ? 0 : g.ny - 1;
-        c[0] = ja; c[1] = -side; c[2] = jb;
-    } else {
-        const unsigned qq = g.div_nx.div(q);
-        x = int(q - qq * unsigned(g.nx)); y = int(qq); lz = side < 0 ? 0 : g.nzl - 1;
-        c[0] = ja; c[1] = jb; c[2] = -side;
-    }
-    const int i = tensor_dir((c[0] + 1) + 3 * (c[1] + 1) + 9 * (c[2] + 1));
     const int p = int(ctr->t & 1);
-    const float val = *pull_source(P, p, x, y, lz, i);
-    float* fin = P.p.f[p];
-    fin[g.gaddr((unsigned long long)((long long)g.sidx(x, y, lz) - g.soff(i)), i)] = val;
-    const int own = owner_face(g, x, y, g.gz0 + lz, i);
-    if (own != kNoOwner) P.p.slot[p ^ 1][own][g.slot_index(own, x, y, lz, i)] = val;
+    // face ranges of 9*F entries, j slowest inside a face
+    auto run = [&](auto FC, unsigned F) -> bool {
+        if (e >= 9u * F) {
+            e -= 9u * F;
+            return false;
+        }
+        unsigned j = 0, q = e;
+        while (q >= F) {
+            q -= F;
+            ++j;
+        }
+        ghost_fill_entry<decltype(FC)::value>(P, p, q, j);
+        return true;
+    };
+    if (run(IntC<0>{}, Fx) || run(IntC<1>{}, Fx) || run(IntC<2>{}, Fy) || run(IntC<3>{}, Fy) ||
+        run(IntC<4>{}, Fz) || run(IntC<5>{}, Fz))
+        return;
 }
 
 template <int KIND, int POLICY, bool STD>
@@ -927,15 +889,10 @@ void launch_fluid_form(const FluidParams& P, int part, int write_macro, cudaStre
 }  // namespace
 
 // part: 0 every node, 1 the two halo planes (edge), 2 the rest (bulk).
-void launch_ghost_fill(const FluidParams& P, cudaStream_t st) {
+void launch_ghost_fill(const FluidParams& P, cudaStream_t st, bool) {
     const RegionGeo& g = P.g;
-    static const bool per_node = [] {
-        const char* e = std::getenv("LBMG_FILL");
-        return e && std::string(e) == "node";
-    }();
-    const unsigned nodes = 2u * (unsigned(g.ny) * g.nzl + unsigned(g.nx) * g.nzl + g.plane);
-    if (per_node) ghost_fill_kernel<<<blocks_for(nodes, 256), 256, 0, st>>>(P);
-    else ghost_fill_dir_kernel<<<blocks_for(9ull * nodes, 256), 256, 0, st>>>(P);
+    const unsigned long long entries = 18ull * (unsigned(g.ny) * g.nzl + unsigned(g.nx) * g.nzl + g.plane);
+    ghost_fill_kernel<<<blocks_for(entries, 256), 256, 0, st>>>(P);
 }
 
 void launch_fluid(const FluidParams& P, int part, int write_macro, cudaStream_t st, bool fill) {

@@ -197,6 +197,10 @@ void Runner::compute_geo(Region& r) const {
         g.PX = unsigned(nx_) + 4u;
         g.PY = unsigned(ny_) + 1u;
         g.PP = g.PX * g.PY;
+        g.zwrap = g.per[2] && regions_.size() == 1 && !rank_mode_;
+        g.has_outflow = 0;
+        for (int f = 0; f < 6; ++f)
+            if (scene_.cfg.faces[f].condition == LBMG_OUTFLOW) g.has_outflow = 1;
         g.div_px = FastDiv(g.PX);
         g.div_py = FastDiv(g.PY);
         // a tile's windows reach off_max + 3 = PP + PX + 4 slots below its
@@ -398,6 +402,7 @@ void Runner::init_fields() {
         FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
         launch_init(P, ip, stream());
     }
+    fill_ghosts_full();
     CK(cudaGetLastError());
     // update_rigid_motion(t=0) for every solid (runner.cpp:104-106)
     if (has_solids_) {
@@ -461,6 +466,17 @@ void Runner::enqueue_fluid(bool write_macro, int part) {
         FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
         launch_fluid(P, part, write_macro, st);
     }
+}
+
+// Every ghost slot of the current step's input buffer (the fluid kernel only
+// pushes the next step's values; state set up outside the step loop needs
+// all of them).
+void Runner::fill_ghosts_full() {
+    for (auto& r : regions_)
+        if (r.geo.ghost) {
+            FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+            launch_ghost_fill(P, stream(), true);
+        }
 }
 
 // Single region on the ghost layout: ghost fill first, then one fused IB
@@ -703,6 +719,8 @@ void Runner::set_layout(int ell, size_t alpha) {
         }
     }
     (void)old;
+    fill_ghosts_full();
+    CK(cudaStreamSynchronize(stream()));
     for (auto& r : regions_)
         for (auto& d : r.solids) {
             const size_t n = d.n;

@@ -126,6 +126,7 @@ private:
     void enqueue_ib_pre();
     void enqueue_ib_mid();
     bool fused_ib() const;
+    void fill_ghosts_full();
     void enqueue_fluid(bool write_macro, int part);
     void invalidate_graphs();
     void finish_chunk(long t0, long requested);

@@ -121,6 +121,23 @@ def test_outflow_edge_semantics_parity():
     assert_fields_close(g, r)
 
 
+@pytest.mark.parametrize("faces", [
+    ("inlet", "outflow", "no-slip", "outflow", "outflow", "inlet"),
+    ("periodic", "periodic", "no-slip", "outflow", "inlet", "outflow"),
+    ("outflow", "inlet", "periodic", "periodic", "outflow", "no-slip"),
+    ("no-slip", "no-slip", "outflow", "inlet", "periodic", "periodic"),
+])
+@pytest.mark.parametrize("regions", [1, 2])
+def test_edge_semantics_parity_ghost_layout(faces, regions):
+    # nx % 4 == 0: the ghost-layer path (fill kernel + pushed bounce-back /
+    # inlet / wrap ghosts + stale outflow slots) against the reference
+    cfg = scenes.outflow_mix(12, 8, 10)
+    cfg.faces = scenes.faces(*faces, inlet=(0.03, 0.01, -0.01))
+    g, r, sg, sr = run_pair(cfg, 40, regions=regions, ref_regions=regions, chunks=4)
+    assert sg.ok and sr["ok"]
+    assert_fields_close(g, r)
+
+
 def test_open_channel_sphere_parity_small():
     cfg = scenes.sphere(64, 40, 40, center=(20, 20, 20), radius=6.0, subdiv=3, r=0.6)
     g, r, sg, sr = run_pair(cfg, 120, chunks=3)
