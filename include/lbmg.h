@@ -183,6 +183,22 @@ int lbmg_runner_dims(const lbmg_runner* r, int* nx, int* ny, int* nz);
 int lbmg_runner_region_count(const lbmg_runner* r);
 /* Runner::set_layout, runner.cpp:252-258. */
 int lbmg_runner_set_layout(lbmg_runner* r, int block_edge, size_t alpha);
+/* Kernel variants, the launch-split dimension of the tuner (replaces the
+ * fixed kSplitBoundary two-pass collision, collision.hpp:58): fluid 0 = the
+ * TMA-staged kernel on the ghost layout, 1 = register-direct kernels on the
+ * compact layout; ib 0 = fused single-region IB kernel, 1 = split pipeline.
+ * Results are identical up to fp32 atomic order in the IB scatter. */
+int lbmg_runner_set_variant(lbmg_runner* r, int fluid, int ib);
+int lbmg_runner_variant(const lbmg_runner* r, int* fluid, int* ib);
+/* measure_cost (autotune.cpp:29-36): set_layout(block_edge, alpha), advance
+ * warmup steps, then the mean device seconds per step of advance(n_steps)
+ * (CUDA events on the runner's stream); +inf when the run diverges.  The
+ * runner advances, like the reference's probe. */
+int lbmg_runner_measure_cost(lbmg_runner* r, int block_edge, size_t alpha, int warmup, int n_steps,
+                             double* seconds);
+/* Identity of the device layout a requested alpha maps to (equal keys =
+ * identical layouts, so a tuner can measure each once). */
+int lbmg_runner_layout_key(const lbmg_runner* r, size_t alpha, uint64_t* key);
 size_t lbmg_runner_alpha(const lbmg_runner* r);
 int lbmg_runner_block_edge(const lbmg_runner* r);
 

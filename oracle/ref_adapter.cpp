@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <algorithm>
+
 #include "lbm/autotune.hpp"
 #include "lbm/boundary.hpp"
 #include "lbm/collision.hpp"
@@ -446,6 +448,40 @@ int ref_gather_forces(size_t n, const double* pos, const double* force, const ui
             for (int a = 0; a < 3; ++a) g[3 * k + a] = r.g[k][a];
             loops[k] = r.loops[k];
         }
+    });
+}
+
+// TuneSpec::from_scene (autotune.cpp:9-27) of a runner's scene: ell range and
+// the alpha list (cap entries at most; returns the count).
+int ref_tune_spec(void* h, int n_steps, int warmup, int* ell_min, int* ell_max, size_t* alphas, size_t cap,
+                  size_t* n_alphas) {
+    return guard([&] {
+        auto* rr = static_cast<RefRunner*>(h);
+        const TuneSpec spec = TuneSpec::from_scene(rr->scene, n_steps, warmup);
+        *ell_min = spec.ell_min;
+        *ell_max = spec.ell_max;
+        *n_alphas = spec.alphas.size();
+        for (std::size_t k = 0; k < spec.alphas.size() && k < cap; ++k) alphas[k] = spec.alphas[k];
+    });
+}
+
+// search_with_cost (autotune.cpp:38-60) over an injected cost table
+// cost[(ell - ell_min) * n_alphas + k] (SPEC autotune example: fake cost fn).
+int ref_search_with_cost(int ell_min, int ell_max, const size_t* alphas, size_t n_alphas, const double* cost,
+                         int* ell, size_t* alpha, double* best) {
+    return guard([&] {
+        TuneSpec spec;
+        spec.ell_min = ell_min;
+        spec.ell_max = ell_max;
+        spec.alphas.assign(alphas, alphas + n_alphas);
+        std::vector<std::size_t> idx(alphas, alphas + n_alphas);
+        const TuneOutcome o = search_with_cost(spec, [&](int l, std::size_t a) {
+            std::size_t k = std::find(idx.begin(), idx.end(), a) - idx.begin();
+            return cost[std::size_t(l - ell_min) * n_alphas + k];
+        });
+        *ell = o.ell;
+        *alpha = o.alpha;
+        *best = o.cost;
     });
 }
 

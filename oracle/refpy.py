@@ -72,6 +72,8 @@ def ref_lib():
         "ref_kernel_support": (I, [D, I, I, I, C.POINTER(I), D]),
         "ref_stream_and_faces": (I, [CFG, D, D]),
         "ref_gather_forces": (I, [SZ, D, D, U8P, I, I, I, D, U32P]),
+        "ref_tune_spec": (I, [P, I, I, C.POINTER(I), C.POINTER(I), C.POINTER(SZ), SZ, C.POINTER(SZ)]),
+        "ref_search_with_cost": (I, [I, I, C.POINTER(SZ), SZ, D, C.POINTER(I), C.POINTER(SZ), D]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -200,6 +202,24 @@ class RefRunner:
         L.ref_scene_samples(self._h, solid, _dp(pos), _dp(ref), _u32(src), _dp(bbox), C.byref(ell), _dp(rep))
         return {"positions": pos, "reference_positions": ref, "source_id": src, "bbox_lo": bbox[:3],
                 "bbox_hi": bbox[3:], "block_edge": ell.value, "report": rep}
+
+
+def ref_tune_spec(runner: "RefRunner", n_steps=10, warmup=5):
+    L = ref_lib()
+    lo, hi, n = C.c_int(), C.c_int(), C.c_size_t()
+    buf = (C.c_size_t * 64)()
+    _check(L.ref_tune_spec(runner._h, n_steps, warmup, C.byref(lo), C.byref(hi), buf, 64, C.byref(n)))
+    return lo.value, hi.value, [int(buf[k]) for k in range(n.value)]
+
+
+def ref_search_with_cost(ell_min, ell_max, alphas, table):
+    L = ref_lib()
+    a = (C.c_size_t * len(alphas))(*alphas)
+    t = np.ascontiguousarray(table, dtype=np.float64)
+    ell, alpha, best = C.c_int(), C.c_size_t(), C.c_double()
+    _check(L.ref_search_with_cost(ell_min, ell_max, a, len(alphas), _dp(t), C.byref(ell), C.byref(alpha),
+                                  C.byref(best)))
+    return ell.value, alpha.value, best.value
 
 
 def ref_rates(cfg: SceneConfig):

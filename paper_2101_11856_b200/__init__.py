@@ -13,7 +13,11 @@ from .runner import (CudaError, Runner, Scene, StateError, StepStatus, TimingRow
                      collide_batch, device_count, lib, model_rates, morton3, reorder_permutation,
                      split_domain)
 
+from . import autotune
+from .autotune import TuneOutcome, TuneSpec
+
 __all__ = [
+    "autotune", "TuneOutcome", "TuneSpec",
     "ConfigError", "FaceSpec", "MeshConfig", "RigidMotion", "SceneConfig", "SolidConfig",
     "load_scene_config", "parse_scene_config", "CudaError", "Runner", "Scene", "StateError",
     "StepStatus", "TimingRow", "build_scene", "collide_batch", "device_count", "lib", "model_rates",

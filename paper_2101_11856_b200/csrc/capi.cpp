@@ -294,6 +294,26 @@ int lbmg_runner_set_layout(lbmg_runner* r, int block_edge, size_t alpha) {
     return guarded([&] { R(r).set_layout(block_edge, alpha); });
 }
 
+int lbmg_runner_set_variant(lbmg_runner* r, int fluid, int ib) {
+    return guarded([&] { R(r).set_variant(fluid, ib); });
+}
+
+int lbmg_runner_variant(const lbmg_runner* r, int* fluid, int* ib) {
+    return guarded([&] {
+        if (fluid) *fluid = R(r).fluid_variant();
+        if (ib) *ib = R(r).ib_variant();
+    });
+}
+
+int lbmg_runner_measure_cost(lbmg_runner* r, int block_edge, size_t alpha, int warmup, int n_steps,
+                             double* seconds) {
+    return guarded([&] { *seconds = R(r).measure_cost(block_edge, alpha, warmup, n_steps); });
+}
+
+int lbmg_runner_layout_key(const lbmg_runner* r, size_t alpha, uint64_t* key) {
+    return guarded([&] { *key = R(r).layout_key(alpha); });
+}
+
 size_t lbmg_runner_alpha(const lbmg_runner* r) { return r && r->impl ? r->impl->alpha() : 0; }
 int lbmg_runner_block_edge(const lbmg_runner* r) { return r && r->impl ? r->impl->block_edge() : 0; }
 

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <string>
 
 namespace lbmg {
@@ -189,7 +190,7 @@ void Runner::compute_geo(Region& r) const {
     g.div_nx = FastDiv(unsigned(nx_));
     g.div_ny = FastDiv(unsigned(ny_));
     g.ghost = 0;
-    if (nx_ % 4 == 0 && ghost_layout_enabled()) {
+    if (nx_ % 4 == 0 && ghost_layout_enabled() && variant_fluid_ == 0) {
         // ghost-layer layout (device_common.cuh): pitch nx+4, ny+1 rows,
         // planes -1..nzl, CSoA blocks of alpha >= 256 slots (one staged tile
         // writes one contiguous 27 KB block); alpha >= slots is SoA
@@ -486,7 +487,7 @@ bool Runner::fused_ib() const {
         const char* e = std::getenv("LBMG_IB_FUSED");
         return e && std::string(e) == "0";
     }();
-    return has_solids_ && !off && !rank_mode_ && regions_.size() == 1 && regions_[0].geo.ghost;
+    return has_solids_ && !off && variant_ib_ == 0 && !rank_mode_ && regions_.size() == 1 && regions_[0].geo.ghost;
 }
 
 void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
@@ -767,9 +768,52 @@ void Runner::set_layout(int ell, size_t alpha) {
     invalidate_graphs();
 }
 
+void Runner::set_variant(int fluid, int ib) {
+    if (fluid < 0 || fluid > 1 || ib < 0 || ib > 1) throw ConfigError("set_variant: fluid and ib variants are 0 or 1");
+    variant_ib_ = ib;
+    if (fluid != variant_fluid_) {
+        variant_fluid_ = fluid;
+        set_layout(ell_, layout_.alpha_req);  // re-lays the populations out (ghost <-> compact)
+    }
+    invalidate_graphs();
+}
+
+unsigned long long Runner::layout_key(size_t alpha) const {
+    Runner* self = const_cast<Runner*>(this);
+    const size_t keep = layout_.alpha_req;
+    self->layout_.alpha_req = alpha;
+    Region r = regions_.front();
+    compute_geo(r);
+    self->layout_.alpha_req = keep;
+    return (static_cast<unsigned long long>(r.geo.ghost) << 40) | (static_cast<unsigned long long>(r.geo.la) << 32) |
+           r.geo.A;
+}
+
+double Runner::measure_cost(int ell, size_t alpha, int warmup, int n_steps) {
+    if (n_steps < 1) throw ConfigError("tune: n_steps must be >= 1");
+    set_layout(ell, alpha);
+    if (warmup > 0 && !advance(warmup, nullptr).ok) return std::numeric_limits<double>::infinity();
+    if (!status_.ok) return std::numeric_limits<double>::infinity();
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, stream()));
+    const Status st = advance(n_steps, nullptr);
+    CK(cudaEventRecord(e1, stream()));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (!st.ok) return std::numeric_limits<double>::infinity();
+    return double(ms) * 1e-3 / n_steps;
+}
+
 std::unique_ptr<Runner> Runner::clone() const {
     auto c = std::make_unique<Runner>(scene_, rank_mode_ ? 1 : m_global_, device_, rank_mode_ ? m_global_ : 0,
                                       rank_);
+    c->variant_ib_ = variant_ib_;
+    if (variant_fluid_ != c->variant_fluid_) c->set_variant(variant_fluid_, variant_ib_);
     if (layout_.alpha_req != c->layout_.alpha_req || ell_ != c->ell_) c->set_layout(ell_, layout_.alpha_req);
     c->copy_state_from(*this);
     return c;

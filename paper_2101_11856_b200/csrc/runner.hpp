@@ -63,6 +63,19 @@ public:
     int region_count() const { return int(regions_.size()); }
     int global_regions() const { return m_global_; }
     void set_layout(int ell, size_t alpha);
+    // Kernel variants (the launch-split dimension of the tuner): fluid 0 =
+    // TMA-staged kernel on the ghost layout (needs nx % 4 == 0), 1 =
+    // register-direct kernels on the compact layout; ib 0 = fused single-region
+    // IB kernel, 1 = mark / band / spread / totals pipeline.
+    void set_variant(int fluid, int ib);
+    int fluid_variant() const { return variant_fluid_; }
+    int ib_variant() const { return variant_ib_; }
+    // Eq. 10 cost of one candidate (autotune.cpp:29-36): set_layout, warm-up,
+    // mean device seconds per step over n_steps (CUDA events around advance);
+    // +inf when the run diverges.
+    double measure_cost(int ell, size_t alpha, int warmup, int n_steps);
+    // identity of the device layout alpha maps to (ghost, log2 block, block)
+    unsigned long long layout_key(size_t alpha) const;
     size_t alpha() const { return layout_.alpha_req; }
     int block_edge() const { return ell_; }
     int nx() const { return nx_; }
@@ -142,6 +155,7 @@ private:
     std::vector<Region> regions_;
     Layout layout_;
     int ell_ = 1;
+    int variant_fluid_ = 0, variant_ib_ = 0;
     FaceTable faces_{};
     ModelConst model_{};
     bool has_solids_ = false;

@@ -71,6 +71,10 @@ def lib():
         "lbmg_runner_region_count": (I, [P]),
         "lbmg_runner_set_layout": (I, [P, I, SZ]),
         "lbmg_runner_alpha": (SZ, [P]),
+        "lbmg_runner_set_variant": (I, [P, I, I]),
+        "lbmg_runner_variant": (I, [P, C.POINTER(I), C.POINTER(I)]),
+        "lbmg_runner_measure_cost": (I, [P, I, SZ, I, I, C.POINTER(C.c_double)]),
+        "lbmg_runner_layout_key": (I, [P, SZ, C.POINTER(C.c_uint64)]),
         "lbmg_runner_block_edge": (I, [P]),
         "lbmg_runner_gather_rho": (I, [P, D]),
         "lbmg_runner_gather_u": (I, [P, D]),
@@ -270,6 +274,28 @@ class Runner:
 
     def alpha(self) -> int:
         return int(lib().lbmg_runner_alpha(self._h))
+
+    def set_variant(self, fluid: int, ib: int):
+        """Kernel variants (tuner launch-split dimension): fluid 0 = TMA-staged
+        ghost-layout kernel, 1 = register-direct compact kernels; ib 0 = fused
+        single-region IB kernel, 1 = split IB pipeline."""
+        _check(lib().lbmg_runner_set_variant(self._h, fluid, ib))
+
+    def variant(self):
+        f, i = C.c_int(), C.c_int()
+        _check(lib().lbmg_runner_variant(self._h, C.byref(f), C.byref(i)))
+        return f.value, i.value
+
+    def measure_cost(self, block_edge: int, alpha: int, warmup: int, n_steps: int) -> float:
+        """autotune.cpp:29-36 on the device: mean seconds per step (CUDA events), inf on divergence."""
+        out = C.c_double()
+        _check(lib().lbmg_runner_measure_cost(self._h, block_edge, alpha, warmup, n_steps, C.byref(out)))
+        return out.value
+
+    def layout_key(self, alpha: int) -> int:
+        k = C.c_uint64()
+        _check(lib().lbmg_runner_layout_key(self._h, alpha, C.byref(k)))
+        return k.value
 
     def block_edge(self) -> int:
         return int(lib().lbmg_runner_block_edge(self._h))
