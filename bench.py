@@ -268,6 +268,7 @@ def run_ours(args):
         runner.advance(min(args.steps, 20), timings=rows)
     fluid = [r.seconds for r in rows if r.phase == "fluid"]
     ib = [r.seconds for r in rows if r.phase == "ib"]
+    bnd = [r.seconds for r in rows if r.phase == "boundary"]
     fluid_s = statistics.mean(fluid) if fluid else None
     peak, peak_kind = measured_peaks()
     roofline = None
@@ -275,11 +276,16 @@ def run_ours(args):
         alg = ALG_BYTES_PER_LU * nodes_local
         achieved = alg / fluid_s / 1e9
         traffic = ncu_traffic(args.config)
+        step_bytes = alg + IB_BYTES_PER_SAMPLE * n_samples
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": traffic, "kernel": "fluid_kernel (fused stream+faces+moments+CM-MRT+forcing)",
-                    "alg_bytes_per_launch": alg, "kernel_ms": fluid_s * 1e3, "peak_kind": peak_kind,
+                    "traffic": traffic,
+                    "kernel": "fluid_ghost_kernel (TMA-staged pull-stream + moments + CM-MRT/ACM + forcing)",
+                    "alg_bytes_per_launch": alg, "alg_bytes_per_lu": ALG_BYTES_PER_LU,
+                    "kernel_ms": fluid_s * 1e3, "peak_kind": peak_kind,
+                    "boundary_ms": (statistics.mean(bnd) * 1e3) if bnd else 0.0,
                     "ib_ms": (statistics.mean(ib) * 1e3) if ib else 0.0,
-                    "step_share_fluid": fluid_s / (ms_per_step * 1e-3)}
+                    "step_share_fluid": fluid_s / (ms_per_step * 1e-3),
+                    "step_frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / peak}
 
     # end-to-end through the public API: per step one advance(1) call with its
     # host inputs (motion-table rows) and host result (status + reaction totals)

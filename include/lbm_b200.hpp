@@ -257,7 +257,7 @@ public:
         if (!timings) {
             detail::check(lbmg_runner_advance(h_, steps, &st, nullptr, 0, nullptr));
         } else {
-            std::vector<lbmg_timing_row> rows(std::size_t(steps > 0 ? steps : 1) * 3);
+            std::vector<lbmg_timing_row> rows(std::size_t(steps > 0 ? steps : 1) * 4);
             std::size_t n = 0;
             detail::check(lbmg_runner_advance(h_, steps, &st, rows.data(), rows.size(), &n));
             for (std::size_t k = 0; k < n; ++k) timings->push_back({rows[k].phase, rows[k].step, rows[k].seconds});

@@ -489,7 +489,6 @@ __device__ __forceinline__ void ghost_fill_entry(const FluidParams& P, int p, un
 
 __global__ void __launch_bounds__(256) ghost_fill_kernel(const __grid_constant__ FluidParams P) {
     DevCounters* ctr = P.ctr;
-    if (blockIdx.x == 0 && threadIdx.x < 3) ctr->tile_ctr[threadIdx.x] = 0u;  // this step's tile queues
     if (ctr->diverged) return;
     const RegionGeo& g = P.g;
     const unsigned Fx = unsigned(g.ny) * g.nzl, Fy = unsigned(g.nx) * g.nzl, Fz = g.plane;
@@ -521,7 +520,13 @@ __global__ void __launch_bounds__(kBulkThreads, 4)
     float* const stage0 = reinterpret_cast<float*>(smem_raw);
     uint64_t* const full = reinterpret_cast<uint64_t*>(smem_raw + kStages * kStageBytes);
     DevCounters* ctr = P.ctr;
-    if (ctr->diverged) return;  // CTA-uniform
+    if (ctr->diverged) {  // CTA-uniform; still counted for the queue rewind
+        if (threadIdx.x == 0 && atomicAdd(&ctr->tile_done[slot], 1u) == gridDim.x - 1) {
+            ctr->tile_ctr[slot] = 0u;
+            ctr->tile_done[slot] = 0u;
+        }
+        return;
+    }
     const RegionGeo& g = P.g;
     const int p = int(ctr->t & 1);
     const float* __restrict__ fin = P.p.f[p];
@@ -668,6 +673,16 @@ __global__ void __launch_bounds__(kBulkThreads, 4)
                 constexpr int i = decltype(I)::value;
                 *reinterpret_cast<float2*>(sd + cross9(i, 2) * g.plane + hp) = fs[i];
             });
+        }
+    }
+    // the last CTA out rewinds this launch's tile queue (all of its warps have
+    // stopped claiming tiles: barrier first), so every launch starts at 0
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(&ctr->tile_done[slot], 1u) == gridDim.x - 1) {
+            ctr->tile_ctr[slot] = 0u;
+            ctr->tile_done[slot] = 0u;
         }
     }
 }

@@ -490,14 +490,21 @@ bool Runner::fused_ib() const {
     return has_solids_ && !off && variant_ib_ == 0 && !rank_mode_ && regions_.size() == 1 && regions_[0].geo.ghost;
 }
 
+// One step on the runner's stream.  Timing events (advance with timings):
+// [0] boundary = ghost fill (the six face passes, wraps, halos) [1] ib [2]
+// fluid = the fused stream/moments/collision kernel [3] step end [4].
 void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
     cudaStream_t st = stream();
     if (ev) CK(cudaEventRecord((*ev)[0], st));
-    const bool fused = fused_ib();
-    if (fused) {
+    for (auto& r : regions_)
+        if (r.geo.ghost) {
+            FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+            launch_ghost_fill(P, st);
+        }
+    if (ev) CK(cudaEventRecord((*ev)[1], st));
+    if (fused_ib()) {
         Region& r = regions_[0];
         FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
-        launch_ghost_fill(P, st);
         const int ns = int(scene_.solids.size());
         for (int s = 0; s < ns; ++s)
             launch_ib_fused(P, r.solids[s], motion_tab_ + size_t(s) * (cap_ + 2) * kMotionRow, r.fused_partial,
@@ -506,18 +513,16 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
         enqueue_ib_pre();
         enqueue_ib_mid();
     }
-    if (ev) CK(cudaEventRecord((*ev)[1], st));
-    if (fused) {
-        Region& r = regions_[0];
+    if (ev) CK(cudaEventRecord((*ev)[2], st));
+    for (auto& r : regions_) {
         FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
         launch_fluid(P, 0, write_macro, st, false);
-    } else {
-        enqueue_fluid(write_macro, 0);
     }
+    if (ev) CK(cudaEventRecord((*ev)[3], st));
     if (has_solids_)
         for (auto& r : regions_) CK(cudaMemsetAsync(r.ptr.tflag, 0, r.geo.ns / 32 + 1, st));
     launch_step_end(ctr_, st);
-    if (ev) CK(cudaEventRecord((*ev)[2], st));
+    if (ev) CK(cudaEventRecord((*ev)[4], st));
 }
 
 Status Runner::advance(long steps, std::vector<Timing>* timings) {
@@ -532,14 +537,14 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
         long long t0d = t0;
         CK(cudaMemcpyAsync(&ctr_->chunk_t0, &t0d, sizeof t0d, cudaMemcpyHostToDevice, st));
         CK(cudaStreamSynchronize(st));
-        std::vector<std::array<cudaEvent_t, 3>> evs;
+        std::vector<std::array<cudaEvent_t, 5>> evs;
         for (long j = 0; j < chunk; ++j) {
             const bool last = done + j == steps - 1;
             if (timings) {
-                std::vector<cudaEvent_t> e(3);
+                std::vector<cudaEvent_t> e(5);
                 for (auto& x : e) CK(cudaEventCreate(&x));
                 enqueue_step(last, &e);
-                evs.push_back({e[0], e[1], e[2]});
+                evs.push_back({e[0], e[1], e[2], e[3], e[4]});
             } else {
                 cudaGraphExec_t& g = graph_[last ? 1 : 0];
                 if (!g) {
@@ -568,13 +573,13 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
         CK(cudaGetLastError());
         if (timings) {
             for (size_t j = 0; j < evs.size(); ++j) {
-                float ib = 0, fl = 0;
-                CK(cudaEventElapsedTime(&ib, evs[j][0], evs[j][1]));
-                CK(cudaEventElapsedTime(&fl, evs[j][1], evs[j][2]));
+                float seg[4] = {0, 0, 0, 0};
+                for (int q = 0; q < 4; ++q) CK(cudaEventElapsedTime(&seg[q], evs[j][q], evs[j][q + 1]));
                 const long step = t0 + long(j);
-                if (has_solids_) timings->push_back({"ib", step, ib * 1e-3});
-                timings->push_back({"fluid", step, fl * 1e-3});
-                timings->push_back({"total", step, (ib + fl) * 1e-3});
+                if (seg[0] > 0.f) timings->push_back({"boundary", step, seg[0] * 1e-3});
+                if (has_solids_) timings->push_back({"ib", step, seg[1] * 1e-3});
+                timings->push_back({"fluid", step, seg[2] * 1e-3});
+                timings->push_back({"total", step, (seg[0] + seg[1] + seg[2] + seg[3]) * 1e-3});
                 for (auto x : evs[j]) cudaEventDestroy(x);
             }
         }

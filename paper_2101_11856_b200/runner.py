@@ -245,7 +245,7 @@ class Runner:
         if timings is None:
             _check(lib().lbmg_runner_advance(self._h, steps, C.byref(st), None, 0, None))
         else:
-            cap = max(1, steps) * 3
+            cap = max(1, steps) * 4
             rows = (_abi.TimingRowC * cap)()
             n = C.c_size_t()
             _check(lib().lbmg_runner_advance(self._h, steps, C.byref(st), rows, cap, C.byref(n)))

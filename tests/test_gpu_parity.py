@@ -274,7 +274,7 @@ def test_timings_rows():
     g = lbm.Runner(lbm.build_scene(cfg))
     rows = []
     g.advance(3, timings=rows)
-    assert [r.phase for r in rows[:3]] == ["ib", "fluid", "total"]
+    assert [r.phase for r in rows[:4]] == ["boundary", "ib", "fluid", "total"]
     assert all(r.seconds > 0 for r in rows)
 
 
