@@ -1,19 +1,19 @@
 // The fused fluid step of one region (stream + six face passes + moments +
-// CM-MRT/ACM collision + forcing, runner.cpp:135-208), split in two kernels
-// so the hot one carries no boundary logic:
+// CM-MRT/ACM collision + forcing, runner.cpp:135-208).
 //
-//  fluid_bulk_kernel   nodes with 1<=x<=nx-2, 1<=y<=ny-2, 1<=lz<=nzl-2.
-//                      Two consecutive x-nodes per thread, packed fp32x2
-//                      arithmetic (FFMA2/FADD2/FMUL2), one 64-bit load and
-//                      store per direction per thread; x-shifted pulls take
-//                      the neighbour lane's half through a warp shuffle (one
-//                      extra scalar load at the warp edge).  All 27 loads are
-//                      independent and issued back to back.
-//  fluid_shell_kernel  every other node (the six boundary layers and the
-//                      planes next to a halo): per-direction ownership,
-//                      bounce-back / inlet / outflow (incl. the stale edge
-//                      read), halo sends, face slots.  Scalar, same collision
-//                      code (bit-identical per node to the bulk path).
+// Ghost-layer layout (RegionGeo::ghost):
+//  ghost_fill_kernel   the face passes, periodic wraps and z halos of this
+//                      step, written into the ghost slots the face nodes pull
+//                      from (+ the persistent face slots).
+//  fluid_ghost_kernel  every owned node: TMA-staged plain shifted pulls,
+//                      moments, packed (FFMA2) collision, forcing; persistent
+//                      CTAs on an in-order device tile queue.
+// Compact layout (nx % 4 != 0, or the register-direct tuner variant):
+//  fluid_bulk_kernel   interior nodes, two x-nodes per thread, LDG.64 + SHFL.
+//  fluid_shell_kernel  the boundary layers: per-direction ownership, bounce-
+//                      back / inlet / outflow (incl. the stale edge read),
+//                      halo sends, face slots.
+// All paths share collision.cuh and are bit-identical per node.
 #include <cuda_runtime.h>
 
 #include <algorithm>
