@@ -386,11 +386,17 @@ __global__ void __launch_bounds__(kBulkThreads, FORM == 2 ? 4 : 3) fluid_bulk_ke
 //                      while the CTA computes the current one (two nodes per
 //                      thread, packed FFMA2 collision, 64-bit stores).  Lanes on
 //                      ghost/pad slots compute but do not store.
-constexpr int kTile = 2 * kBulkThreads;  // storage slots per tile
-constexpr int kWin = kTile + 4;         // staged floats per direction
+// Tile geometry per CTA size T (threads): 2T storage slots per tile.
+template <int T>
+struct GhostTile {
+    static constexpr int kThreads = T;
+    static constexpr int kTile = 2 * T;               // storage slots per tile
+    static constexpr int kWin = kTile + 4;            // staged floats per direction
+    static constexpr unsigned kStageBytes = 27u * kWin * 4u;
+};
 constexpr int kStages = 2;
-constexpr unsigned kStageBytes = 27u * kWin * 4u;
-constexpr unsigned kStagedSmem = kStages * kStageBytes + 8u * kStages;
+template <int T>
+constexpr unsigned staged_smem() { return kStages * GhostTile<T>::kStageBytes + 8u * kStages; }
 
 // Window offset of slot 0 of a tile for direction i: tiles start at multiples
 // of 4 and PX, PP are multiples of 4, so (tile start - off_i) = -c_x (mod 4).
@@ -513,9 +519,12 @@ __global__ void __launch_bounds__(256) ghost_fill_kernel(const __grid_constant__
         return;
 }
 
-template <int KIND, int POLICY, bool STD>
-__global__ void __launch_bounds__(kBulkThreads, 4)
-    fluid_ghost_kernel(const __grid_constant__ FluidParams P, int z_a, int z_b, int slot, int write_macro, int dbg) {
+template <int KIND, int POLICY, bool STD, int T>
+__global__ void __launch_bounds__(T, 512 / T)
+    fluid_ghost_kernel(const __grid_constant__ FluidParams P, int z_a, int z_b, int slot, int write_macro, int dbg,
+                       int pf) {
+    constexpr int kTile = GhostTile<T>::kTile, kWin = GhostTile<T>::kWin;
+    constexpr unsigned kStageBytes = GhostTile<T>::kStageBytes;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* const stage0 = reinterpret_cast<float*>(smem_raw);
     uint64_t* const full = reinterpret_cast<uint64_t*>(smem_raw + kStages * kStageBytes);
@@ -587,6 +596,20 @@ __global__ void __launch_bounds__(kBulkThreads, 4)
         mbar_wait_parity(&full[s], (it / kStages) & 1u);
         const unsigned tile = stage_tile[s];
         if (tile >= ntiles) break;
+        // Tiles are claimed in order by all CTAs, so tile + pf will be claimed
+        // about pf / (stages * grid) tile periods from now: pull its windows
+        // into L2 already (deeper pipeline at no shared-memory cost; issued
+        // here, before the tile is read into registers)
+        if (pf > 0 && tid == 0 && tile + unsigned(pf) < ntiles) {
+            const long long k1 = (long long)org + (long long)(tile + unsigned(pf)) * kTile;
+            static_for<0, 27>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                const unsigned long long a1 = (unsigned long long)(k1 - g.soff(i) - win_shift(i));
+                const unsigned long long e1 = (a1 | g.amask) + 1ull;
+                const unsigned l1 = e1 - a1 < (unsigned long long)kWin ? unsigned(e1 - a1) : unsigned(kWin);
+                prefetch_l2(fin + g.gaddr(a1, i), l1 * 4u);
+            });
+        }
         const unsigned m = 2u * tid;
         const unsigned sl = org + tile * kTile + m;  // storage slot of the pair's first node
         const unsigned row = g.div_px.div(sl - g.base);
@@ -607,7 +630,7 @@ __global__ void __launch_bounds__(kBulkThreads, 4)
         __syncwarp();
         if ((tid & 31u) == 0) {
             __threadfence_block();  // this warp's reads of stage s are done
-            if (atomicAdd(&reads_done[s], 1u) == kBulkThreads / 32 - 1) {
+            if (atomicAdd(&reads_done[s], 1u) == T / 32 - 1) {
                 reads_done[s] = 0;
                 fence_proxy_async_smem();
                 refill(s);
@@ -813,21 +836,21 @@ namespace {
 
 thread_local bool t_fill = true;  // launch_fluid(..., fill): the ghost fill is part of this launch
 
-template <int KIND, int POLICY, bool STD>
-void launch_ghost_planes(const FluidParams& P, int z_a, int z_b, int slot, int write_macro, cudaStream_t st) {
-    if (z_b <= z_a) return;
+template <int KIND, int POLICY, bool STD, int T>
+void launch_ghost_planes_t(const FluidParams& P, int z_a, int z_b, int slot, int write_macro, cudaStream_t st) {
     const RegionGeo& g = P.g;
-    const unsigned ntiles = unsigned(z_b - z_a) * g.PP / kTile + 2;
+    constexpr unsigned smem = staged_smem<T>();
+    const unsigned ntiles = unsigned(z_b - z_a) * g.PP / GhostTile<T>::kTile + 2;
     static int grid_per_sm = -1, sms = 0;
-    auto kern = fluid_ghost_kernel<KIND, POLICY, STD>;
+    auto kern = fluid_ghost_kernel<KIND, POLICY, STD, T>;
     if (grid_per_sm < 0) {
-        CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kStagedSmem)));
+        CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         int dev = 0;
         CUDA_OK(cudaGetDevice(&dev));
         CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         int nb = 0;
-        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kBulkThreads, kStagedSmem));
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T, smem));
         grid_per_sm = nb > 0 ? nb : 1;
     }
     const unsigned grid = std::min<unsigned>(ntiles, unsigned(grid_per_sm * sms));
@@ -835,7 +858,30 @@ void launch_ghost_planes(const FluidParams& P, int z_a, int z_b, int slot, int w
         const char* e = std::getenv("LBMG_GHOST_DBG");
         return e ? std::atoi(e) : 0;
     }();
-    kern<<<grid, kBulkThreads, kStagedSmem, st>>>(P, z_a, z_b, slot, write_macro, dbg);
+    static const int pf_periods = [] {  // L2 prefetch distance in tile periods (0: off, measured best)
+        const char* e = std::getenv("LBMG_L2_PREFETCH");
+        return e ? std::atoi(e) : 0;
+    }();
+    kern<<<grid, T, smem, st>>>(P, z_a, z_b, slot, write_macro, dbg, pf_periods * kStages * int(grid));
+}
+
+// CTA size of the staged kernel (LBMG_GHOST_THREADS, default 512 = 1024-slot
+// tiles, one CTA of 16 warps per SM, 2 x 111 KB stages: measured fastest,
+// C3 4.92 ms vs 5.31 (256) vs 6.00 (128)); a tile must fit one Eq. 9 block.
+template <int KIND, int POLICY, bool STD>
+void launch_ghost_planes(const FluidParams& P, int z_a, int z_b, int slot, int write_macro, cudaStream_t st) {
+    if (z_b <= z_a) return;
+    static const int threads = [] {
+        const char* e = std::getenv("LBMG_GHOST_THREADS");
+        return e ? std::atoi(e) : 512;
+    }();
+    const unsigned block = P.g.amask + 1u;  // Eq. 9 block (slots); SoA: 2^31
+    if (threads >= 512 && block >= 1024u)
+        launch_ghost_planes_t<KIND, POLICY, STD, 512>(P, z_a, z_b, slot, write_macro, st);
+    else if (threads >= 256 && block >= 512u)
+        launch_ghost_planes_t<KIND, POLICY, STD, 256>(P, z_a, z_b, slot, write_macro, st);
+    else
+        launch_ghost_planes_t<KIND, POLICY, STD, 128>(P, z_a, z_b, slot, write_macro, st);
 }
 
 // part 0: every plane; 1: ghost fill + the slab's boundary planes (which feed

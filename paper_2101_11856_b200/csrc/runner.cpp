@@ -204,10 +204,11 @@ void Runner::compute_geo(Region& r) const {
             if (scene_.cfg.faces[f].condition == LBMG_OUTFLOW) g.has_outflow = 1;
         g.div_px = FastDiv(g.PX);
         g.div_py = FastDiv(g.PY);
-        // a tile's windows reach off_max + 3 = PP + PX + 4 slots below its
-        // first slot and kWin - 1 - off_min above its last one
-        g.base = round_up(g.PX + 264u, 256u);
-        const unsigned slots = round_up(g.base + unsigned(g.nzl + 2) * g.PP + g.PX + 1024u, 256u);
+        // a tile (<= 1024 slots, aligned down from the first owned plane) reads
+        // windows reaching off_max + 3 = PP + PX + 4 slots below its first slot
+        // and kWin - 1 - off_min above its last one
+        g.base = round_up(g.PX + 1040u, 256u);
+        const unsigned slots = round_up(g.base + unsigned(g.nzl + 2) * g.PP + g.PX + 2080u, 256u);
         size_t areq = layout_.alpha_req;
         if (const char* e = std::getenv("LBMG_GHOST_ALPHA")) areq = std::strtoull(e, nullptr, 10);  // layout probes
         // alpha below one 256-slot tile (incl. the reference default 1) has no

@@ -60,4 +60,9 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
         : "memory");
 }
 
+// global -> L2 bulk prefetch (no destination, no completion tracking)
+__device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 }  // namespace lbmg
