@@ -301,9 +301,9 @@ __global__ void ib_motion_once_kernel(IbSolidDev S, const double* row, int nx, i
 // reaction totals (ib.cpp:491-501: per-block FP64 partials, the last block
 // sums them in block order -> deterministic) and, for moving solids, the
 // rigid motion to t+1 (ib.cpp:456-489).
-constexpr int kFusedWarps = 8;
+constexpr int kFusedWarps = 4;
 
-__global__ void __launch_bounds__(kFusedWarps * 32)
+__global__ void __launch_bounds__(kFusedWarps * 32, 8)
     ib_fused_kernel(const __grid_constant__ FluidParams P, IbSolidDev S, const double* table, double* partial,
                     unsigned* done, double* out_base, int stride, int moving) {
     __shared__ double red[kFusedWarps][6];

@@ -116,11 +116,40 @@ Runner::Runner(const lbmg_scene& scene, int regions, int device, int world, int 
     }
     ell_ = c.block_edge;
     layout_.alpha_req = c.alpha;
+    // The fused IB kernel reads f* of its support nodes as plain pulls; if no
+    // support node can lie on a domain face, none of those pulls touches a
+    // ghost slot and the ghost fill may run concurrently with the IB kernel.
+    // Static solids: their sample positions; moving ones: the sphere of their
+    // largest reference radius around a fixed centre (no linear motion).
+    ib_overlap_ok_ = has_solids_;
+    for (const auto& s : scene_.solids) {
+        V3 lo{1e300, 1e300, 1e300}, hi{-1e300, -1e300, -1e300};
+        if (s.moving) {
+            if (dot(s.linear_velocity, s.linear_velocity) != 0.0) ib_overlap_ok_ = false;
+            double r2 = 0.0;
+            for (const auto& q : s.samples.reference_positions) r2 = std::max(r2, dot(q, q));
+            const double r = std::sqrt(r2) + 1e-6;
+            lo = s.center + V3{-r, -r, -r};
+            hi = s.center + V3{r, r, r};
+        } else {
+            for (const auto& q : s.samples.positions)
+                for (int a = 0; a < 3; ++a) {
+                    lo[a] = std::min(lo[a], q[a]);
+                    hi[a] = std::max(hi[a], q[a]);
+                }
+        }
+        const int n[3] = {nx_, ny_, nz_};
+        for (int a = 0; a < 3; ++a)  // support nodes floor(p) .. floor(p)+1 strictly inside
+            if (!(std::floor(lo[a]) >= 1.0 && std::floor(hi[a]) + 1.0 <= double(n[a] - 2))) ib_overlap_ok_ = false;
+    }
 
     device_ = device;
     CK(cudaSetDevice(device));
     CK(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, device));
     CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming));
 
     const int first = rank_mode_ ? rank_ : 0;
     const int count = rank_mode_ ? 1 : m_global_;
@@ -151,6 +180,9 @@ Runner::~Runner() {
     for (void* p : allocs_) cudaFree(p);
     allocs_.clear();
     if (stream_) cudaStreamDestroy(stream_);
+    if (side_) cudaStreamDestroy(side_);
+    if (fork_) cudaEventDestroy(fork_);
+    if (join_) cudaEventDestroy(join_);
 }
 
 void Runner::invalidate_graphs() {
@@ -481,6 +513,14 @@ void Runner::fill_ghosts_full() {
         }
 }
 
+bool Runner::overlap_off() {
+    static const bool off = [] {
+        const char* e = std::getenv("LBMG_IB_OVERLAP");
+        return e && std::string(e) == "0";
+    }();
+    return off;
+}
+
 // Single region on the ghost layout: ghost fill first, then one fused IB
 // kernel per solid (no band list, no seams), then the fluid kernel.
 bool Runner::fused_ib() const {
@@ -497,11 +537,21 @@ bool Runner::fused_ib() const {
 void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
     cudaStream_t st = stream();
     if (ev) CK(cudaEventRecord((*ev)[0], st));
+    // ghost fill || fused IB when no IB support node can touch a ghost slot
+    // (a fork/join inside the captured graph); timed runs keep them serial
+    const bool overlap = !ev && fused_ib() && ib_overlap_ok_ && !overlap_off();
+    cudaStream_t fst = st;
+    if (overlap) {
+        CK(cudaEventRecord(fork_, st));
+        CK(cudaStreamWaitEvent(side_, fork_, 0));
+        fst = side_;
+    }
     for (auto& r : regions_)
         if (r.geo.ghost) {
             FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
-            launch_ghost_fill(P, st);
+            launch_ghost_fill(P, fst);
         }
+    if (overlap) CK(cudaEventRecord(join_, side_));
     if (ev) CK(cudaEventRecord((*ev)[1], st));
     if (fused_ib()) {
         Region& r = regions_[0];
@@ -514,6 +564,7 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
         enqueue_ib_pre();
         enqueue_ib_mid();
     }
+    if (overlap) CK(cudaStreamWaitEvent(st, join_, 0));
     if (ev) CK(cudaEventRecord((*ev)[2], st));
     for (auto& r : regions_) {
         FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};

@@ -139,6 +139,7 @@ private:
     void enqueue_ib_pre();
     void enqueue_ib_mid();
     bool fused_ib() const;
+    static bool overlap_off();
     void fill_ghosts_full();
     void enqueue_fluid(bool write_macro, int part);
     void invalidate_graphs();
@@ -170,6 +171,9 @@ private:
 
     cudaStream_t stream_ = nullptr;
     cudaStream_t ext_stream_ = nullptr;
+    cudaStream_t side_ = nullptr;             // ghost fill concurrent with the fused IB kernel
+    cudaEvent_t fork_ = nullptr, join_ = nullptr;
+    bool ib_overlap_ok_ = false;
     cudaGraphExec_t graph_[2] = {nullptr, nullptr};
 
     long t_ = 0;

@@ -81,3 +81,24 @@ def outflow_mix(nx=10, ny=8, nz=7) -> SceneConfig:
     cfg.faces = faces("inlet", "outflow", "no-slip", "outflow", "outflow", "inlet", inlet=(0.03, 0.01, -0.01))
     cfg.init_velocity = (0.02, 0.0, 0.0)
     return cfg
+
+
+def city(nx=64, ny=32, nz=48, n_boxes=4, seed=7, r=0.7) -> SceneConfig:
+    """C4 twin: seeded synthetic "city" of box solids on a no-slip ground,
+    x- inlet 0.05, x+ outflow (Poisson r=0.7, since r=0.5
+    boxes diverge)."""
+    import numpy as np
+    cfg = acm(SceneConfig(nx=nx, ny=ny, nz=nz, viscosity=0.02))
+    cfg.faces = faces("inlet", "outflow", "no-slip", "no-slip", "no-slip", "no-slip")
+    cfg.init_velocity = (0.05, 0.0, 0.0)
+    rng = np.random.default_rng(seed)
+    cfg.solids = []
+    for _ in range(n_boxes):
+        w, d = rng.uniform(4, 8, size=2)
+        h = rng.uniform(6, 0.6 * ny)
+        x0 = rng.uniform(0.25 * nx, 0.75 * nx - w)
+        z0 = rng.uniform(6, nz - 6 - d)
+        cfg.solids.append(SolidConfig(MeshConfig(type="box", lo=(x0, 1.2, z0), hi=(x0 + w, 1.2 + h, z0 + d)),
+                                      poisson_radius=r))
+    cfg.block_edge = 2
+    return cfg

@@ -98,6 +98,38 @@ def test_cavity_parity():
     assert_fields_close(g, r)
 
 
+def test_c1_cavity_64_matches_reference_anchors():
+    # configs[0] at full size: the reference's own t=100 / t=1000 anchors
+    # (tests/golden/c1_anchor.npz, made by tests/golden/make_golden.py)
+    import pathlib
+    gold = np.load(pathlib.Path(__file__).parent / "golden" / "c1_anchor.npz")
+    g = lbm.Runner(lbm.build_scene(scenes.cavity(n=64)))
+    for t in (100, 1000):
+        st = g.advance(t - g.step_count())
+        assert st.ok
+        rho, u = g.gather_rho(), g.gather_u()
+        assert abs(rho.sum() - gold[f"mass_{t}"]) / gold[f"mass_{t}"] <= 1e-7
+        ke = 0.5 * (rho * (u ** 2).sum(axis=1)).sum()
+        assert abs(ke - gold[f"ke_{t}"]) / gold[f"ke_{t}"] <= 1e-4
+        umax = np.sqrt((u ** 2).sum(axis=1)).max()
+        assert abs(umax - gold[f"umax_{t}"]) / gold[f"umax_{t}"] <= 1e-4
+        assert rel_l2(rho.reshape(64, 64, 64)[32], gold[f"rho_slice_{t}"]) <= RHO_TOL
+        assert rel_l2(u.reshape(64, 64, 64, 3)[:, 32], gold[f"u_slice_{t}"]) <= U_TOL
+
+
+def test_city_twin_parity():
+    # configs[3] twin: several box solids on the ground, inlet/outflow
+    cfg = scenes.city()
+    g, r, sg, sr = run_pair(cfg, 60, chunks=2)
+    assert sg.ok and sr["ok"]
+    assert_fields_close(g, r, f_tol=5e-5)
+    tg, tr = g.totals_log(), r.totals_log()
+    assert np.abs(tg - tr).max() <= 1e-3 * np.abs(tr).max() + 1e-6
+    for s in range(len(cfg.solids)):
+        a, b = g.samples(0, s), r.samples(0, s)
+        assert np.array_equal(a["source_id"], b["source_id"]) and np.array_equal(a["flagged"], b["flagged"])
+
+
 def test_taylor_green_parity_and_decay():
     cfg = scenes.taylor_green(nx=32, ny=32, nz=4)
     g, r, sg, sr = run_pair(cfg, 400, chunks=4)
