@@ -300,9 +300,11 @@ def run_ours(args):
         dt = time.perf_counter() - t0
         ns = len(cfg.solids)
         e2e = {"value": nodes_global * k_e2e / dt / 1e6, "unit": "MLUPS",
-               "h2d_bytes_per_step": 8 + 2 * ns * 18 * 8, "d2h_bytes_per_step": 40 + ns * 6 * 8,
-               "how": "advance(1) per step through the C ABI from pinned-free host buffers; includes the "
-                      "per-step motion-table upload and status/totals download", "steps": k_e2e}
+               "h2d_bytes_per_step": 8 + 2 * ns * 18 * 8, "d2h_bytes_per_step": 64 + ns * 6 * 8,
+               "how": "one Runner.advance(1) call per step through the C ABI, host wall clock: each call "
+                      "uploads that step's inputs (chunk start + rigid-motion rows) from pinned host memory "
+                      "and downloads its results (step counters/status + reaction totals), one stream sync",
+               "steps": k_e2e}
         del rho_probe, st
 
     line = None

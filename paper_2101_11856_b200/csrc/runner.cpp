@@ -169,14 +169,22 @@ Runner::Runner(const lbmg_scene& scene, int regions, int device, int world, int 
         motion_tab_ = static_cast<double*>(dalloc(sizeof(double) * (cap_ + 2) * ns * kMotionRow));
         totals_dev_ = static_cast<double*>(dalloc(sizeof(double) * cap_ * regions_.size() * ns * 6));
     }
+    {
+        const size_t ns = scene_.solids.size();
+        CK(cudaMallocHost(&pinned_up_, sizeof(double) * (1 + (cap_ + 2) * std::max<size_t>(ns, 1) * kMotionRow)));
+        pinned_down_bytes_ = sizeof(DevCounters) + sizeof(double) * cap_ * regions_.size() * std::max<size_t>(ns, 1) * 6;
+        CK(cudaMallocHost(&pinned_down_, pinned_down_bytes_));
+    }
     upload_solids();
     init_fields();
-    if (rank_mode_ && has_solids_) fill_motion_table(0, cap_ + 1);
+    if (rank_mode_ && has_solids_) fill_motion_table(0, cap_ + 1, true);
     CK(cudaStreamSynchronize(stream_));
 }
 
 Runner::~Runner() {
     invalidate_graphs();
+    if (pinned_up_) cudaFreeHost(pinned_up_);
+    if (pinned_down_) cudaFreeHost(pinned_down_);
     for (void* p : allocs_) cudaFree(p);
     allocs_.clear();
     if (stream_) cudaStreamDestroy(stream_);
@@ -240,7 +248,8 @@ void Runner::compute_geo(Region& r) const {
         // windows reaching off_max + 3 = PP + PX + 4 slots below its first slot
         // and kWin - 1 - off_min above its last one
         g.base = round_up(g.PX + 1040u, 256u);
-        const unsigned slots = round_up(g.base + unsigned(g.nzl + 2) * g.PP + g.PX + 2080u, 256u);
+        unsigned slots = round_up(g.base + unsigned(g.nzl + 2) * g.PP + g.PX + 2080u, 256u);
+        if (const char* e = std::getenv("LBMG_A_PAD")) slots += 256u * unsigned(std::atoi(e));  // layout probe
         size_t areq = layout_.alpha_req;
         if (const char* e = std::getenv("LBMG_GHOST_ALPHA")) areq = std::strtoull(e, nullptr, 10);  // layout probes
         // alpha below one 256-slot tile (incl. the reference default 1) has no
@@ -410,17 +419,19 @@ void Runner::motion_row(int solid, long t, double* row) const {
     }
 }
 
-void Runner::fill_motion_table(long t0, long rows) {
+// Motion rows of steps t0 .. t0+rows-1, solid-major ([solid][step][row]: the
+// kernels index (t - chunk_t0) * kMotionRow within a per-solid view), staged
+// in pinned memory and uploaded asynchronously on the runner's stream (the
+// caller synchronises once per advance chunk, after the step graphs).
+void Runner::fill_motion_table(long t0, long rows, bool sync) {
     const size_t ns = scene_.solids.size();
-    std::vector<double> tab(size_t(rows) * ns * kMotionRow);
-    // layout: [step][solid][row]; kernels index (t - t0) * kMotionRow within a
-    // per-solid view, so store solid-major: [solid][step][row]
+    double* tab = pinned_up_ + 1;
     for (size_t s = 0; s < ns; ++s)
         for (long j = 0; j < rows; ++j) motion_row(int(s), t0 + j, &tab[(s * (cap_ + 2) + j) * kMotionRow]);
     for (size_t s = 0; s < ns; ++s)
         CK(cudaMemcpyAsync(motion_tab_ + s * (cap_ + 2) * kMotionRow, &tab[s * (cap_ + 2) * kMotionRow],
                            sizeof(double) * rows * kMotionRow, cudaMemcpyHostToDevice, stream()));
-    CK(cudaStreamSynchronize(stream()));
+    if (sync) CK(cudaStreamSynchronize(stream()));
 }
 
 void Runner::init_fields() {
@@ -585,10 +596,10 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
     while (done < steps) {
         const long chunk = std::min(cap_, steps - done);
         const long t0 = t_;
-        if (has_solids_) fill_motion_table(t0, chunk + 1);
-        long long t0d = t0;
-        CK(cudaMemcpyAsync(&ctr_->chunk_t0, &t0d, sizeof t0d, cudaMemcpyHostToDevice, st));
-        CK(cudaStreamSynchronize(st));
+        // inputs of the chunk (pinned, async, ordered before the step graphs)
+        if (has_solids_) fill_motion_table(t0, chunk + 1, false);
+        *reinterpret_cast<long long*>(pinned_up_) = t0;
+        CK(cudaMemcpyAsync(&ctr_->chunk_t0, pinned_up_, sizeof(long long), cudaMemcpyHostToDevice, st));
         std::vector<std::array<cudaEvent_t, 5>> evs;
         for (long j = 0; j < chunk; ++j) {
             const bool last = done + j == steps - 1;
@@ -621,8 +632,15 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
                 CK(cudaGraphLaunch(g, st));
             }
         }
+        // results of the chunk (counters + reaction totals), one sync
+        CK(cudaMemcpyAsync(pinned_down_, ctr_, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
+        if (has_solids_)
+            CK(cudaMemcpyAsync(pinned_down_ + sizeof(DevCounters), totals_dev_,
+                               sizeof(double) * size_t(chunk) * regions_.size() * scene_.solids.size() * 6,
+                               cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         CK(cudaGetLastError());
+        downloaded_ = true;
         if (timings) {
             for (size_t j = 0; j < evs.size(); ++j) {
                 float seg[4] = {0, 0, 0, 0};
@@ -643,13 +661,19 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
 }
 
 void Runner::finish_chunk(long t0, long) {
+    // advance() downloads counters + totals asynchronously with its final
+    // sync; other callers (rank mode) read them here
+    const bool pre = downloaded_;
+    downloaded_ = false;
     DevCounters h{};
-    CK(cudaMemcpy(&h, ctr_, sizeof h, cudaMemcpyDeviceToHost));
+    if (pre) std::memcpy(&h, pinned_down_, sizeof h);
+    else CK(cudaMemcpy(&h, ctr_, sizeof h, cudaMemcpyDeviceToHost));
     const long completed = long(h.t) - t0;
     if (has_solids_ && completed > 0) {
         const size_t ns = scene_.solids.size(), m = regions_.size();
         std::vector<double> tot(size_t(completed) * m * ns * 6);
-        CK(cudaMemcpy(tot.data(), totals_dev_, sizeof(double) * tot.size(), cudaMemcpyDeviceToHost));
+        if (pre) std::memcpy(tot.data(), pinned_down_ + sizeof(DevCounters), sizeof(double) * tot.size());
+        else CK(cudaMemcpy(tot.data(), totals_dev_, sizeof(double) * tot.size(), cudaMemcpyDeviceToHost));
         for (long j = 0; j < completed; ++j) {
             std::array<double, 6> sum{};
             for (size_t r = 0; r < m; ++r)
@@ -969,7 +993,7 @@ Status Runner::sync_external() {
     finish_chunk(ext_chunk_t0_, 0);
     ext_chunk_t0_ = t_;
     if (has_solids_) {
-        fill_motion_table(t_, cap_ + 1);
+        fill_motion_table(t_, cap_ + 1, true);
         long long t0d = t_;
         CK(cudaMemcpy(&ctr_->chunk_t0, &t0d, sizeof t0d, cudaMemcpyHostToDevice));
     }

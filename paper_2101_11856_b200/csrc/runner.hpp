@@ -133,7 +133,7 @@ private:
     void link_halos();
     void init_fields();
     void upload_solids();
-    void fill_motion_table(long t0, long rows);
+    void fill_motion_table(long t0, long rows, bool sync);
     void motion_row(int solid, long t, double* row) const;
     void enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev);
     void enqueue_ib_pre();
@@ -174,6 +174,10 @@ private:
     cudaStream_t side_ = nullptr;             // ghost fill concurrent with the fused IB kernel
     cudaEvent_t fork_ = nullptr, join_ = nullptr;
     bool ib_overlap_ok_ = false;
+    double* pinned_up_ = nullptr;      // chunk_t0 + motion rows (host -> device)
+    char* pinned_down_ = nullptr;      // counters + totals (device -> host)
+    size_t pinned_down_bytes_ = 0;
+    bool downloaded_ = false;
     cudaGraphExec_t graph_[2] = {nullptr, nullptr};
 
     long t_ = 0;
