@@ -208,6 +208,17 @@ int lbmg_runner_block_edge(const lbmg_runner* r);
 int lbmg_runner_gather_rho(const lbmg_runner* r, double* out);
 int lbmg_runner_gather_u(const lbmg_runner* r, double* out);
 int lbmg_runner_gather_f(const lbmg_runner* r, double* out);
+/* Asynchronous rho* and u* snapshot, the driver's snapshot path (driver.cpp:45-59)
+ * without stalling the step loop: _begin enqueues the canonical-AoS FP64
+ * conversion and the D2H copy into pinned memory on a copy stream and
+ * returns; later advance() calls continue (they wait for it only before
+ * rho/u are rewritten); _wait blocks and copies out (rho: N doubles, u: 3N),
+ * returning the step the snapshot was taken at. */
+int lbmg_runner_snapshot_begin(lbmg_runner* r);
+int lbmg_runner_snapshot_wait(lbmg_runner* r, double* rho, double* u, long* step);
+/* dump_field in canonical order (io.cpp:34-55, canonical = true): the LBF1
+ * file the reference's load_field (io.cpp:57-87) reads. */
+int lbmg_dump_field(const char* path, int nx, int ny, int nz, int beta, const double* aos);
 int lbmg_runner_slab(const lbmg_runner* r, int* z0, int* z1);
 
 /* Runner::totals_log, runner.hpp:52: 6 doubles (force, torque) per step. */

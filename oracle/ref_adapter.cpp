@@ -15,6 +15,7 @@
 #include <algorithm>
 
 #include "lbm/autotune.hpp"
+#include "lbm/io.hpp"
 #include "lbm/boundary.hpp"
 #include "lbm/collision.hpp"
 #include "lbm/decomp.hpp"
@@ -482,6 +483,34 @@ int ref_search_with_cost(int ell_min, int ell_max, const size_t* alphas, size_t 
         *ell = o.ell;
         *alpha = o.alpha;
         *best = o.cost;
+    });
+}
+
+// io.cpp:34-87: dump_field (canonical) and load_field of the reference.
+int ref_dump_field(const char* path, int nx, int ny, int nz, int beta, const double* aos) {
+    return guard([&] {
+        GridDims d;
+        d.nx = nx;
+        d.ny = ny;
+        d.nz = nz;
+        FieldStore fs(LayoutParams::make(1, std::size_t(beta), d.n_nodes()));
+        for (std::size_t k = 0; k < d.n_nodes(); ++k)
+            for (int i = 0; i < beta; ++i) fs.set(k, std::size_t(i), aos[k * beta + i]);
+        dump_field(fs, d, path, true);
+    });
+}
+
+int ref_load_field(const char* path, int* dims, int* beta, double* out, size_t cap) {
+    return guard([&] {
+        const LoadedField lf = load_field(path);
+        dims[0] = lf.dims.nx;
+        dims[1] = lf.dims.ny;
+        dims[2] = lf.dims.nz;
+        *beta = int(lf.field.beta());
+        const std::size_t n = lf.field.n_nodes();
+        for (std::size_t k = 0; k < n; ++k)
+            for (std::size_t i = 0; i < lf.field.beta(); ++i)
+                if (k * lf.field.beta() + i < cap) out[k * lf.field.beta() + i] = lf.field.get(k, i);
     });
 }
 

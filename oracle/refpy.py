@@ -74,6 +74,8 @@ def ref_lib():
         "ref_gather_forces": (I, [SZ, D, D, U8P, I, I, I, D, U32P]),
         "ref_tune_spec": (I, [P, I, I, C.POINTER(I), C.POINTER(I), C.POINTER(SZ), SZ, C.POINTER(SZ)]),
         "ref_search_with_cost": (I, [I, I, C.POINTER(SZ), SZ, D, C.POINTER(I), C.POINTER(SZ), D]),
+        "ref_dump_field": (I, [C.c_char_p, I, I, I, I, D]),
+        "ref_load_field": (I, [C.c_char_p, C.POINTER(I), C.POINTER(I), D, SZ]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -220,6 +222,20 @@ def ref_search_with_cost(ell_min, ell_max, alphas, table):
     _check(L.ref_search_with_cost(ell_min, ell_max, a, len(alphas), _dp(t), C.byref(ell), C.byref(alpha),
                                   C.byref(best)))
     return ell.value, alpha.value, best.value
+
+
+def ref_dump_field(path, dims, field):
+    a = np.ascontiguousarray(field, dtype=np.float64)
+    nx, ny, nz = dims
+    _check(ref_lib().ref_dump_field(str(path).encode(), nx, ny, nz, a.size // (nx * ny * nz), _dp(a)))
+
+
+def ref_load_field(path, cap):
+    d = (C.c_int * 3)()
+    b = C.c_int()
+    out = np.zeros(cap)
+    _check(ref_lib().ref_load_field(str(path).encode(), d, C.byref(b), _dp(out), cap))
+    return (d[0], d[1], d[2]), b.value, out
 
 
 def ref_rates(cfg: SceneConfig):

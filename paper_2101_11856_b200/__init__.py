@@ -10,7 +10,7 @@
 from .scene import (ConfigError, FaceSpec, MeshConfig, RigidMotion, SceneConfig, SolidConfig,
                     load_scene_config, parse_scene_config)
 from .runner import (CudaError, Runner, Scene, StateError, StepStatus, TimingRow, build_scene,
-                     collide_batch, device_count, lib, model_rates, morton3, reorder_permutation,
+                     collide_batch, device_count, dump_field, lib, model_rates, morton3, reorder_permutation,
                      split_domain)
 
 from . import autotune
@@ -20,6 +20,6 @@ __all__ = [
     "autotune", "TuneOutcome", "TuneSpec",
     "ConfigError", "FaceSpec", "MeshConfig", "RigidMotion", "SceneConfig", "SolidConfig",
     "load_scene_config", "parse_scene_config", "CudaError", "Runner", "Scene", "StateError",
-    "StepStatus", "TimingRow", "build_scene", "collide_batch", "device_count", "lib", "model_rates",
+    "StepStatus", "TimingRow", "build_scene", "collide_batch", "device_count", "dump_field", "lib", "model_rates",
     "morton3", "reorder_permutation", "split_domain",
 ]

@@ -27,6 +27,9 @@ int guarded(F&& f) {
     } catch (const OomError& e) {
         g_err = e.what();
         return LBMG_ERR_OOM;
+    } catch (const IoError& e) {
+        g_err = e.what();
+        return LBMG_ERR_IO;
     } catch (const CudaError& e) {
         g_err = e.what();
         return LBMG_ERR_CUDA;
@@ -323,6 +326,37 @@ int lbmg_runner_gather_rho(const lbmg_runner* r, double* out) {
 int lbmg_runner_gather_u(const lbmg_runner* r, double* out) {
     return guarded([&] { R(r).gather(1, out); });
 }
+int lbmg_runner_snapshot_begin(lbmg_runner* r) {
+    return guarded([&] { R(r).snapshot_begin(); });
+}
+
+int lbmg_runner_snapshot_wait(lbmg_runner* r, double* rho, double* u, long* step) {
+    return guarded([&] {
+        const long t = R(r).snapshot_wait(rho, u);
+        if (step) *step = t;
+    });
+}
+
+// LBF1 field dump, canonical order (io.cpp:34-55 with canonical = true):
+// magic, endian probe, nx, ny, nz, beta (u32), alpha = 0 (u64), width (u32),
+// n_nodes (u64), then n_nodes * beta doubles node-major.
+int lbmg_dump_field(const char* path, int nx, int ny, int nz, int beta, const double* aos) {
+    return guarded([&] {
+        std::FILE* f = std::fopen(path, "wb");
+        if (!f) throw IoError(std::string("cannot write field dump: ") + path);
+        const char magic[4] = {'L', 'B', 'F', '1'};
+        const uint32_t probe = 0x01020304u, dims[4] = {uint32_t(nx), uint32_t(ny), uint32_t(nz), uint32_t(beta)};
+        const uint64_t alpha = 0, n = uint64_t(nx) * uint64_t(ny) * uint64_t(nz);
+        const uint32_t width = sizeof(double);
+        bool ok = std::fwrite(magic, 1, 4, f) == 4 && std::fwrite(&probe, 4, 1, f) == 1 &&
+                  std::fwrite(dims, 4, 4, f) == 4 && std::fwrite(&alpha, 8, 1, f) == 1 &&
+                  std::fwrite(&width, 4, 1, f) == 1 && std::fwrite(&n, 8, 1, f) == 1 &&
+                  std::fwrite(aos, sizeof(double), n * uint64_t(beta), f) == n * uint64_t(beta);
+        ok = (std::fclose(f) == 0) && ok;
+        if (!ok) throw IoError(std::string("short write: ") + path);
+    });
+}
+
 int lbmg_runner_gather_f(const lbmg_runner* r, double* out) {
     return guarded([&] { R(r).gather(2, out); });
 }

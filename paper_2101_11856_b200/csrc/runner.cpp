@@ -183,6 +183,11 @@ Runner::Runner(const lbmg_scene& scene, int regions, int device, int world, int 
 
 Runner::~Runner() {
     invalidate_graphs();
+    if (snap_pending_ && snap_done_) cudaEventSynchronize(snap_done_);
+    if (snap_host_) cudaFreeHost(snap_host_);
+    if (copy_) cudaStreamDestroy(copy_);
+    if (snap_ready_) cudaEventDestroy(snap_ready_);
+    if (snap_done_) cudaEventDestroy(snap_done_);
     if (pinned_up_) cudaFreeHost(pinned_up_);
     if (pinned_down_) cudaFreeHost(pinned_down_);
     for (void* p : allocs_) cudaFree(p);
@@ -596,6 +601,9 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
     while (done < steps) {
         const long chunk = std::min(cap_, steps - done);
         const long t0 = t_;
+        // an in-flight snapshot reads rho/u: the split IB pipeline rewrites
+        // them at band nodes every step, the fluid kernel on the last step
+        if (snap_pending_ && has_solids_ && !fused_ib()) CK(cudaStreamWaitEvent(st, snap_done_, 0));
         // inputs of the chunk (pinned, async, ordered before the step graphs)
         if (has_solids_) fill_motion_table(t0, chunk + 1, false);
         *reinterpret_cast<long long*>(pinned_up_) = t0;
@@ -603,6 +611,7 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
         std::vector<std::array<cudaEvent_t, 5>> evs;
         for (long j = 0; j < chunk; ++j) {
             const bool last = done + j == steps - 1;
+            if (last && snap_pending_) CK(cudaStreamWaitEvent(st, snap_done_, 0));
             if (timings) {
                 std::vector<cudaEvent_t> e(5);
                 for (auto& x : e) CK(cudaEventCreate(&x));
@@ -740,6 +749,44 @@ void Runner::gather(int what, double* out) const {
         throw;
     }
     cudaFree(stage);
+}
+
+void Runner::snapshot_begin() {
+    CK(cudaSetDevice(device_));
+    if (snap_pending_) CK(cudaEventSynchronize(snap_done_));
+    size_t n = 0;
+    for (const auto& r : regions_) n += r.geo.n;
+    if (!snap_dev_) {
+        snap_dev_ = static_cast<double*>(dalloc(sizeof(double) * 4 * n, false));
+        CK(cudaMallocHost(&snap_host_, sizeof(double) * 4 * n));
+        CK(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&snap_ready_, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&snap_done_, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(snap_ready_, stream()));
+    CK(cudaStreamWaitEvent(copy_, snap_ready_, 0));
+    const size_t base_plane = size_t(regions_.front().z0) * regions_.front().geo.plane;
+    for (const auto& r : regions_) {
+        FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+        const size_t off = size_t(r.z0) * r.geo.plane - base_plane;
+        launch_read_macro(P, 0, r.geo.n, snap_dev_ + off, snap_dev_ + n + 3 * off, copy_);
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(snap_host_, snap_dev_, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, copy_));
+    CK(cudaEventRecord(snap_done_, copy_));
+    snap_pending_ = true;
+    snap_step_ = t_;
+}
+
+long Runner::snapshot_wait(double* rho, double* u) {
+    if (!snap_pending_ && !snap_host_) throw StateError("snapshot_wait: no snapshot was started");
+    CK(cudaEventSynchronize(snap_done_));
+    snap_pending_ = false;
+    size_t n = 0;
+    for (const auto& r : regions_) n += r.geo.n;
+    if (rho) std::memcpy(rho, snap_host_, sizeof(double) * n);
+    if (u) std::memcpy(u, snap_host_ + n, sizeof(double) * 3 * n);
+    return snap_step_;
 }
 
 size_t Runner::sample_count(int region, int solid) const {

@@ -21,6 +21,9 @@ struct CudaError : std::runtime_error {
 struct OomError : std::runtime_error {
     explicit OomError(const std::string& m) : std::runtime_error(m) {}
 };
+struct IoError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
 struct StateError : std::runtime_error {
     explicit StateError(const std::string& m) : std::runtime_error(m) {}
 };
@@ -84,6 +87,11 @@ public:
     void slab(int* z0, int* z1) const;
 
     void gather(int what, double* out) const;  // 0 rho, 1 u, 2 f
+    // Asynchronous rho*/u* snapshot (driver.cpp:45-59 without stalling the
+    // step loop): device conversion + D2H into pinned memory on a copy
+    // stream; the next advance only waits for it before rho/u are rewritten.
+    void snapshot_begin();
+    long snapshot_wait(double* rho, double* u);  // returns the snapshot's step
     const std::vector<std::array<double, 6>>& totals_log() const { return totals_; }
     size_t sample_count(int region, int solid) const;
     void samples(int region, int solid, double* pos, double* ub, double* force, double* sampled,
@@ -178,6 +186,12 @@ private:
     char* pinned_down_ = nullptr;      // counters + totals (device -> host)
     size_t pinned_down_bytes_ = 0;
     bool downloaded_ = false;
+    cudaStream_t copy_ = nullptr;
+    cudaEvent_t snap_ready_ = nullptr, snap_done_ = nullptr;
+    double* snap_dev_ = nullptr;   // rho (n) then u (3n), canonical order of this runner's slabs
+    double* snap_host_ = nullptr;  // pinned
+    bool snap_pending_ = false;
+    long snap_step_ = 0;
     cudaGraphExec_t graph_[2] = {nullptr, nullptr};
 
     long t_ = 0;

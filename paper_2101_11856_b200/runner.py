@@ -79,6 +79,9 @@ def lib():
         "lbmg_runner_gather_rho": (I, [P, D]),
         "lbmg_runner_gather_u": (I, [P, D]),
         "lbmg_runner_gather_f": (I, [P, D]),
+        "lbmg_runner_snapshot_begin": (I, [P]),
+        "lbmg_runner_snapshot_wait": (I, [P, D, D, C.POINTER(C.c_long)]),
+        "lbmg_dump_field": (I, [C.c_char_p, I, I, I, I, D]),
         "lbmg_runner_slab": (I, [P, C.POINTER(I), C.POINTER(I)]),
         "lbmg_runner_totals_count": (SZ, [P]),
         "lbmg_runner_totals": (I, [P, D, SZ]),
@@ -122,6 +125,16 @@ def _u32(a: np.ndarray):
 
 def _u8(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_uint8))
+
+
+def dump_field(path, dims, field: np.ndarray):
+    """LBF1 canonical field dump (io.cpp:34-55), readable by the reference's load_field."""
+    a = np.ascontiguousarray(field, dtype=np.float64)
+    nx, ny, nz = dims
+    beta = a.size // (nx * ny * nz)
+    if beta * nx * ny * nz != a.size:
+        raise ConfigError("dump_field: field size does not match dims")
+    _check(lib().lbmg_dump_field(str(path).encode(), nx, ny, nz, beta, _dp(a)))
 
 
 def device_count() -> int:
@@ -334,6 +347,20 @@ class Runner:
         _check(lib().lbmg_runner_gather_f(self._h, _dp(out)))
         return out
 
+
+    def snapshot_begin(self):
+        """Start an asynchronous rho*/u* snapshot of the current step (returns at once)."""
+        _check(lib().lbmg_runner_snapshot_begin(self._h))
+
+    def snapshot_wait(self):
+        """(step, rho[N], u[N,3]) of the snapshot started by snapshot_begin."""
+        nx, ny, nz = self.dims()
+        z0, z1 = self.slab()
+        n = nx * ny * (z1 - z0)
+        rho, u = np.empty(n), np.empty((n, 3))
+        t = C.c_long()
+        _check(lib().lbmg_runner_snapshot_wait(self._h, _dp(rho), _dp(u), C.byref(t)))
+        return t.value, rho, u
     def totals_log(self) -> np.ndarray:
         n = lib().lbmg_runner_totals_count(self._h)
         out = np.zeros((n, 6))
