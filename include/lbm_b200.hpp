@@ -9,6 +9,9 @@
 #pragma once
 
 #include <array>
+#include <cmath>
+#include <functional>
+#include <limits>
 #include <cstdint>
 #include <optional>
 #include <stdexcept>
@@ -302,6 +305,30 @@ public:
         return c;
     }
 
+    // Kernel variants (the tuner's launch-split dimension, lbmg.h).
+    void set_variant(int fluid, int ib) { detail::check(lbmg_runner_set_variant(h_, fluid, ib)); }
+    std::array<int, 2> variant() const {
+        std::array<int, 2> v{};
+        detail::check(lbmg_runner_variant(h_, &v[0], &v[1]));
+        return v;
+    }
+    std::uint64_t layout_key(std::size_t alpha) const {
+        std::uint64_t k = 0;
+        detail::check(lbmg_runner_layout_key(h_, alpha, &k));
+        return k;
+    }
+
+    // Asynchronous rho*, u* snapshot (driver.cpp:45-59 without the stall).
+    void snapshot_begin() { detail::check(lbmg_runner_snapshot_begin(h_)); }
+    long snapshot_wait(FieldStore& rho, FieldStore& u) {
+        const GridDims d = dims();
+        rho = FieldStore(d.n_nodes(), 1);
+        u = FieldStore(d.n_nodes(), 3);
+        long t = 0;
+        detail::check(lbmg_runner_snapshot_wait(h_, rho.data(), u.data(), &t));
+        return t;
+    }
+
     lbmg_runner* handle() { return h_; }
 
 private:
@@ -315,5 +342,88 @@ private:
     }
     lbmg_runner* h_ = nullptr;
 };
+
+// dump_field (io.hpp:19-20, canonical = true): LBF1 file readable by load_field.
+inline void dump_field(const FieldStore& field, const GridDims& dims, const std::string& path) {
+    detail::check(lbmg_dump_field(path.c_str(), dims.nx, dims.ny, dims.nz, int(field.beta()), field.data()));
+}
+
+// ---- auto-tuner (autotune.hpp; Eq. 10), device-timed costs -------------------
+
+struct TuneSpec {  // autotune.hpp:18-35 (+ the kernel-variant dimension)
+    int ell_min = 1;
+    int ell_max = 1;
+    std::vector<std::size_t> alphas;
+    int n_steps = 10;
+    int warmup = 5;
+    std::vector<std::array<int, 2>> variants{{0, 0}};
+    std::size_t candidate_count() const {
+        return std::size_t(ell_max - ell_min + 1) * alphas.size() * variants.size();
+    }
+};
+
+struct TuneRow {
+    int ell;
+    std::size_t alpha;
+    double seconds;
+    std::array<int, 2> variant;
+};
+
+struct TuneOutcome {  // autotune.hpp:37-42
+    int ell = 0;
+    std::size_t alpha = 0;
+    double cost = std::numeric_limits<double>::infinity();
+    std::array<int, 2> variant{0, 0};
+    std::vector<TuneRow> rows;
+};
+
+// measure_cost (autotune.cpp:29-36): mean device seconds per step, inf on divergence.
+inline double measure_cost(Runner& runner, int ell, std::size_t alpha, const TuneSpec& spec) {
+    double sec = 0.0;
+    detail::check(lbmg_runner_measure_cost(runner.handle(), ell, alpha, spec.warmup, spec.n_steps, &sec));
+    return sec;
+}
+
+using CostFn = std::function<double(int ell, std::size_t alpha, std::array<int, 2> variant)>;
+
+// search_with_cost (autotune.cpp:38-60): ascending enumeration, strict <.
+inline TuneOutcome search_with_cost(const TuneSpec& spec, const CostFn& cost) {
+    TuneOutcome out;
+    for (const auto& v : spec.variants)
+        for (int ell = spec.ell_min; ell <= spec.ell_max; ++ell)
+            for (std::size_t a : spec.alphas) {
+                const double c = cost(ell, a, v);
+                out.rows.push_back({ell, a, c, v});
+                if (c < out.cost) {
+                    out.cost = c;
+                    out.ell = ell;
+                    out.alpha = a;
+                    out.variant = v;
+                }
+            }
+    if (!std::isfinite(out.cost)) throw ConfigError("tune: every candidate was invalid");
+    return out;
+}
+
+// search (autotune.cpp:62-70): on a clone; equal device layouts measured once.
+inline TuneOutcome search(const Runner& base, const TuneSpec& spec) {
+    Runner probe = base.clone();
+    struct Seen {
+        std::array<int, 2> v;
+        int ell;
+        std::uint64_t key;
+        double cost;
+    };
+    std::vector<Seen> seen;
+    return search_with_cost(spec, [&](int ell, std::size_t alpha, std::array<int, 2> v) {
+        if (probe.variant() != v) probe.set_variant(v[0], v[1]);
+        const std::uint64_t key = probe.layout_key(alpha);
+        for (const auto& s : seen)
+            if (s.v == v && s.ell == ell && s.key == key) return s.cost;
+        const double c = measure_cost(probe, ell, alpha, spec);
+        seen.push_back({v, ell, key, c});
+        return c;
+    });
+}
 
 }  // namespace lbm

@@ -35,3 +35,29 @@ def test_cpp_example_runs(tmp_path):
     r.advance(20)
     mass = float(out.split("mass=")[1])
     assert abs(mass - r.gather_rho().sum()) < 1e-6
+
+
+def _build_example(tmp_path, name):
+    exe = tmp_path / name
+    lib = ROOT / "paper_2101_11856_b200" / "_build"
+    subprocess.run(["g++", "-std=c++17", "-Wall", "-Werror", f"-I{ROOT / 'include'}",
+                    str(ROOT / "examples" / f"{name}.cpp"), f"-L{lib}", "-llbmg", f"-Wl,-rpath,{lib}", "-o",
+                    str(exe)], check=True)
+    return exe
+
+
+def test_cpp_tune_snapshot_example_compiles(tmp_path):
+    assert _build_example(tmp_path, "tune_and_snapshot").exists()
+
+
+@pytest.mark.gpu
+def test_cpp_tune_snapshot_example_runs(tmp_path):
+    exe = _build_example(tmp_path, "tune_and_snapshot")
+    res = subprocess.run([str(exe), str(tmp_path)], capture_output=True, text=True)
+    assert res.returncode == 0, res.stderr
+    assert "tuned rows=6" in res.stdout and "last_snapshot=30 steps=30" in res.stdout
+    import numpy as np
+    from oracle import refpy
+    for t in (10, 20, 30):
+        dims, beta, rho = refpy.ref_load_field(tmp_path / f"rho_{t}.lbf", 32 * 24 * 24)
+        assert dims == (32, 24, 24) and beta == 1 and abs(rho.mean() - 1.0) < 1e-2
