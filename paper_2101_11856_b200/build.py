@@ -62,7 +62,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
                 if verbose and log:
                     print(f"[{src}]\n{log}", file=sys.stderr)
     if todo or not LIB.exists() or any(_obj(s).stat().st_mtime > LIB.stat().st_mtime for s in SOURCES):
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *[str(_obj(s)) for s in SOURCES]]
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *[str(_obj(s)) for s in SOURCES], "-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

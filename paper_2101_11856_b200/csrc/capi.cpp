@@ -2,7 +2,11 @@
 // each entry point maps them to an LBMG_ERR_* code + lbmg_last_error().
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdio>
+#include <exception>
+#include <thread>
+#include <vector>
 #include <cstring>
 #include <string>
 
@@ -109,25 +113,46 @@ int lbmg_scene_build(const lbmg_scene_config* cfg, lbmg_scene** out) {
             s->cfg = *cfg;
             s->solid_cfgs.assign(cfg->solids, cfg->solids + cfg->n_solids);
             s->cfg.solids = s->solid_cfgs.empty() ? nullptr : s->solid_cfgs.data();
-            uint64_t seed = cfg->seed;
-            for (const auto& sc : s->solid_cfgs) {
-                SolidInstance inst;
-                inst.cfg = sc;
-                const TriMesh mesh = build_mesh(sc.mesh);
-                inst.samples = sample_surface(mesh, sc.poisson_radius, seed++, sc.sampling, &inst.report);
-                if (sc.has_motion) {
-                    inst.moving = true;
-                    inst.linear_velocity = v3(sc.linear_velocity);
-                    inst.angular_velocity = v3(sc.angular_velocity);
-                    inst.center = v3(sc.center);
-                    for (size_t k = 0; k < inst.samples.size(); ++k)
-                        inst.samples.reference_positions[k] = inst.samples.positions[k] - inst.center;
-                } else {
-                    inst.samples.reference_positions = inst.samples.positions;
+            // build_scene (scene.cpp:341-366): solid i is sampled with seed
+            // cfg.seed + i, independently of the others -> the solids of a
+            // large scene (C4: ~3.7 M samples over many boxes) are sampled on
+            // all host cores, bit-identical to the sequential order.
+            const size_t ns = s->solid_cfgs.size();
+            std::vector<SolidInstance> built(ns);
+            std::vector<std::exception_ptr> errs(ns);
+            std::atomic<size_t> next{0};
+            auto work = [&] {
+                for (size_t i = next++; i < ns; i = next++) {
+                    try {
+                        const auto& sc = s->solid_cfgs[i];
+                        SolidInstance& inst = built[i];
+                        inst.cfg = sc;
+                        const TriMesh mesh = build_mesh(sc.mesh);
+                        inst.samples = sample_surface(mesh, sc.poisson_radius, cfg->seed + i, sc.sampling, &inst.report);
+                        if (sc.has_motion) {
+                            inst.moving = true;
+                            inst.linear_velocity = v3(sc.linear_velocity);
+                            inst.angular_velocity = v3(sc.angular_velocity);
+                            inst.center = v3(sc.center);
+                            for (size_t k = 0; k < inst.samples.size(); ++k)
+                                inst.samples.reference_positions[k] = inst.samples.positions[k] - inst.center;
+                        } else {
+                            inst.samples.reference_positions = inst.samples.positions;
+                        }
+                        reorder_samples(inst.samples, cfg->block_edge);
+                    } catch (...) {
+                        errs[i] = std::current_exception();
+                    }
                 }
-                reorder_samples(inst.samples, cfg->block_edge);
-                s->solids.push_back(std::move(inst));
-            }
+            };
+            const size_t nt = std::min<size_t>(ns, std::max(1u, std::thread::hardware_concurrency()));
+            std::vector<std::thread> pool;
+            for (size_t t = 1; t < nt; ++t) pool.emplace_back(work);
+            work();
+            for (auto& t : pool) t.join();
+            for (auto& e : errs)
+                if (e) std::rethrow_exception(e);
+            for (auto& inst : built) s->solids.push_back(std::move(inst));
         } catch (...) {
             delete s;
             throw;

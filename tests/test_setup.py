@@ -90,6 +90,8 @@ SCENES = {
     "sphere_small_elim": lambda: _elim(scenes.sphere(48, 32, 32, center=(16, 16, 16), radius=6.0, subdiv=3, r=0.6)),
     "fin_comb_moving": lambda: scenes.rotating_fins(),
     "boxes": lambda: _boxes(),
+    # many solids: sampled on all host cores, must equal the sequential order
+    "city_12": lambda: scenes.city(96, 40, 64, n_boxes=12, seed=11, r=0.7),
 }
 
 
