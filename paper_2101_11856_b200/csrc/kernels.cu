@@ -302,99 +302,103 @@ __global__ void ib_motion_once_kernel(IbSolidDev S, const double* row, int nx, i
 // sums them in block order -> deterministic) and, for moving solids, the
 // rigid motion to t+1 (ib.cpp:456-489).
 constexpr int kFusedWarps = 4;
+constexpr int kFusedSamples = 2 * kFusedWarps;  // two samples per warp (16 lanes each)
 
 __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     ib_fused_kernel(const __grid_constant__ FluidParams P, IbSolidDev S, const double* table, double* partial,
                     unsigned* done, double* out_base, int stride, int moving) {
-    __shared__ double red[kFusedWarps][6];
+    __shared__ double red[kFusedSamples][6];
     __shared__ bool last;
     DevCounters* ctr = P.ctr;
     if (ctr->diverged) return;
     const RegionGeo& g = P.g;
-    const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const unsigned s = blockIdx.x * kFusedWarps + warp;
-    const int corner = int(lane >> 2), sub = int(lane & 3u);
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned slot = threadIdx.x >> 4;  // sample slot in the block
+    const unsigned s = blockIdx.x * kFusedSamples + slot;
+    const unsigned hl = lane & 15u;          // lane within the sample's half warp
+    const int corner = int(hl >> 1), sub = int(hl & 1u);
     const double* row = table + (ctr->t - ctr->chunk_t0) * kMotionRow;
     double tot[6] = {0, 0, 0, 0, 0, 0};
-    if (s < S.n) {
-        const double pos[3] = {S.pos[3 * s], S.pos[3 * s + 1], S.pos[3 * s + 2]};
-        const double ub[3] = {S.ub[3 * s], S.ub[3 * s + 1], S.ub[3 * s + 2]};  // (issued early)
-        const Support ks = kernel_support(pos, g.nx, g.ny, g.NZ);
-        if (lane == 0) S.flagged[s] = ks.inside ? 0 : 1;
-        double us[3] = {0.0, 0.0, 0.0}, fg[3] = {0.0, 0.0, 0.0};
-        if (ks.inside) {  // (single region: every support lies in the slab)
-            const int ox = corner & 1, oy = (corner >> 1) & 1, oz = corner >> 2;
-            const int x = ks.base[0] + ox, y = ks.base[1] + oy, lz = ks.base[2] + oz - g.gz0;
-            const float* fin = P.p.f[ctr->t & 1];
-            const long long sl = g.sidx(x, y, lz);
-            float v[7];
+    const bool have = s < S.n;
+    const unsigned si = have ? s : 0u;
+    const double pos[3] = {S.pos[3 * si], S.pos[3 * si + 1], S.pos[3 * si + 2]};
+    const double ub[3] = {S.ub[3 * si], S.ub[3 * si + 1], S.ub[3 * si + 2]};  // (issued early)
+    const Support ks = kernel_support(pos, g.nx, g.ny, g.NZ);
+    if (have && hl == 0) S.flagged[s] = ks.inside ? 0 : 1;
+    const bool act = have && ks.inside;  // (single region: every support lies in the slab)
+    // every lane runs the gather (shuffles need the full warp); inactive
+    // halves read node (0,0,0) and discard the result
+    const int ox = corner & 1, oy = (corner >> 1) & 1, oz = corner >> 2;
+    const int x = act ? ks.base[0] + ox : 0, y = act ? ks.base[1] + oy : 0;
+    const int lz = act ? ks.base[2] + oz - g.gz0 : 0;
+    const float* fin = P.p.f[ctr->t & 1];
+    const long long sl = g.sidx(x, y, lz);
+    float v[14];
 #pragma unroll
-            for (int j = 0; j < 7; ++j) {  // all seven loads in flight at once
-                const int i = sub + 4 * j;
-                v[j] = i < 27 ? __ldcg(&fin[g.gaddr((unsigned long long)(sl - g.soff(i)), i)]) : 0.f;
-            }
-            float r = 0.f, jx = 0.f, jy = 0.f, jz = 0.f;
+    for (int j = 0; j < 14; ++j) {  // all fourteen loads in flight at once
+        const int i = sub + 2 * j;
+        v[j] = i < 27 ? __ldcg(&fin[g.gaddr((unsigned long long)(sl - g.soff(i)), i)]) : 0.f;
+    }
+    float r = 0.f, jx = 0.f, jy = 0.f, jz = 0.f;
 #pragma unroll
-            for (int j = 0; j < 7; ++j) {
-                const int i = sub + 4 * j;
-                r += v[j];
-                jx += float(cx(i)) * v[j];
-                jy += float(cy(i)) * v[j];
-                jz += float(cz(i)) * v[j];
-            }
+    for (int j = 0; j < 14; ++j) {
+        const int i = sub + 2 * j;
+        r += v[j];
+        jx += float(cx(i)) * v[j];
+        jy += float(cy(i)) * v[j];
+        jz += float(cz(i)) * v[j];
+    }
+    r += __shfl_xor_sync(0xffffffffu, r, 1);
+    jx += __shfl_xor_sync(0xffffffffu, jx, 1);
+    jy += __shfl_xor_sync(0xffffffffu, jy, 1);
+    jz += __shfl_xor_sync(0xffffffffu, jz, 1);
+    const float rho = 1.0f + r;
+    const float inv = 1.0f / rho;
+    const double wx = ox ? ks.w[0][1] : ks.w[0][0], wy = oy ? ks.w[1][1] : ks.w[1][0];
+    const double wz = oz ? ks.w[2][1] : ks.w[2][0];
+    const double w = __dmul_rn(__dmul_rn(wx, wy), wz);
+    double c4[4] = {sub == 0 ? w * double(jx * inv) : 0.0, sub == 0 ? w * double(jy * inv) : 0.0,
+                    sub == 0 ? w * double(jz * inv) : 0.0, sub == 0 ? w * double(rho) : 0.0};
 #pragma unroll
-            for (int o = 1; o < 4; o <<= 1) {
-                r += __shfl_xor_sync(0xffffffffu, r, o);
-                jx += __shfl_xor_sync(0xffffffffu, jx, o);
-                jy += __shfl_xor_sync(0xffffffffu, jy, o);
-                jz += __shfl_xor_sync(0xffffffffu, jz, o);
-            }
-            const float rho = 1.0f + r;
-            const float inv = 1.0f / rho;
-            const double wx = ox ? ks.w[0][1] : ks.w[0][0], wy = oy ? ks.w[1][1] : ks.w[1][0];
-            const double wz = oz ? ks.w[2][1] : ks.w[2][0];
-            const double w = __dmul_rn(__dmul_rn(wx, wy), wz);
-            double c4[4] = {sub == 0 ? w * double(jx * inv) : 0.0, sub == 0 ? w * double(jy * inv) : 0.0,
-                            sub == 0 ? w * double(jz * inv) : 0.0, sub == 0 ? w * double(rho) : 0.0};
+    for (int o = 2; o < 16; o <<= 1)
 #pragma unroll
-            for (int o = 4; o < 32; o <<= 1)
-#pragma unroll
-                for (int a = 0; a < 4; ++a) c4[a] += __shfl_xor_sync(0xffffffffu, c4[a], o);
-            for (int a = 0; a < 3; ++a) {
-                us[a] = c4[a];
-                fg[a] = c4[3] * (ub[a] - us[a]);
-            }
-            if (sub == 0) {  // scatter of this corner (owned: single region)
-                const unsigned k = g.node(x, y, lz);
-                atomicAdd(&P.p.gib[k], float(w * fg[0]));
-                atomicAdd(&P.p.gib[k + g.ns], float(w * fg[1]));
-                atomicAdd(&P.p.gib[k + 2u * g.ns], float(w * fg[2]));
-                P.p.tflag[k >> 5] = 1;
-            }
+        for (int a = 0; a < 4; ++a) c4[a] += __shfl_xor_sync(0xffffffffu, c4[a], o);
+    double us[3] = {0.0, 0.0, 0.0}, fg[3] = {0.0, 0.0, 0.0};
+    if (act) {
+        for (int a = 0; a < 3; ++a) {
+            us[a] = c4[a];
+            fg[a] = c4[3] * (ub[a] - us[a]);
         }
-        if (lane == 0) {
-            for (int a = 0; a < 3; ++a) {
-                S.sampled[3 * s + a] = us[a];
-                S.force[3 * s + a] = fg[a];
-            }
-            if (pos[2] >= double(g.gz0) && pos[2] < double(g.gz0 + g.nzl)) {
-                const double rr[3] = {pos[0] - row[0], pos[1] - row[1], pos[2] - row[2]};
-                tot[0] = -fg[0];
-                tot[1] = -fg[1];
-                tot[2] = -fg[2];
-                tot[3] = -(rr[1] * fg[2] - rr[2] * fg[1]);
-                tot[4] = -(rr[2] * fg[0] - rr[0] * fg[2]);
-                tot[5] = -(rr[0] * fg[1] - rr[1] * fg[0]);
-            }
-            if (moving) motion_apply(row + kMotionRow, S, s, g.nx, g.ny, g.NZ);
+        if (sub == 0) {  // scatter of this corner (owned: single region)
+            const unsigned k = g.node(x, y, lz);
+            atomicAdd(&P.p.gib[k], float(w * fg[0]));
+            atomicAdd(&P.p.gib[k + g.ns], float(w * fg[1]));
+            atomicAdd(&P.p.gib[k + 2u * g.ns], float(w * fg[2]));
+            P.p.tflag[k >> 5] = 1;
         }
     }
-    if (lane == 0)
-        for (int a = 0; a < 6; ++a) red[warp][a] = tot[a];
+    if (have && hl == 0) {
+        for (int a = 0; a < 3; ++a) {
+            S.sampled[3 * s + a] = us[a];
+            S.force[3 * s + a] = fg[a];
+        }
+        if (pos[2] >= double(g.gz0) && pos[2] < double(g.gz0 + g.nzl)) {
+            const double rr[3] = {pos[0] - row[0], pos[1] - row[1], pos[2] - row[2]};
+            tot[0] = -fg[0];
+            tot[1] = -fg[1];
+            tot[2] = -fg[2];
+            tot[3] = -(rr[1] * fg[2] - rr[2] * fg[1]);
+            tot[4] = -(rr[2] * fg[0] - rr[0] * fg[2]);
+            tot[5] = -(rr[0] * fg[1] - rr[1] * fg[0]);
+        }
+        if (moving) motion_apply(row + kMotionRow, S, s, g.nx, g.ny, g.NZ);
+    }
+    if (hl == 0)
+        for (int a = 0; a < 6; ++a) red[slot][a] = tot[a];
     __syncthreads();
     if (threadIdx.x < 6) {
         double acc = 0.0;
-        for (int w = 0; w < kFusedWarps; ++w) acc += red[w][threadIdx.x];
+        for (int w = 0; w < kFusedSamples; ++w) acc += red[w][threadIdx.x];
         partial[blockIdx.x * 6 + threadIdx.x] = acc;
         __threadfence();
     }
@@ -560,7 +564,7 @@ void launch_ib_spread(const FluidParams& P, const IbSolidDev& S, cudaStream_t st
     else ib_spread_kernel<false><<<blocks_for(S.n, kSpreadThreads), kSpreadThreads, 0, st>>>(P, S);
 }
 
-int fused_blocks(size_t n) { return int((n + kFusedWarps - 1) / kFusedWarps); }
+int fused_blocks(size_t n) { return int((n + kFusedSamples - 1) / kFusedSamples); }
 void launch_ib_fused(const FluidParams& P, const IbSolidDev& S, const double* table, double* partial, unsigned* done,
                      double* out_base, int stride, bool moving, cudaStream_t st) {
     if (S.n == 0) return;
