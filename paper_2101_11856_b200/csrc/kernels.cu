@@ -302,7 +302,10 @@ __global__ void ib_motion_once_kernel(IbSolidDev S, const double* row, int nx, i
 // sums them in block order -> deterministic) and, for moving solids, the
 // rigid motion to t+1 (ib.cpp:456-489).
 constexpr int kFusedWarps = 4;
-constexpr int kFusedSamples = 2 * kFusedWarps;  // two samples per warp (16 lanes each)
+constexpr int kLanesPerSample = 8;                               // 8 corners x (lanes / 8) sub-lanes
+constexpr int kSubs = kLanesPerSample / 8;
+constexpr int kLoads = (27 + kSubs - 1) / kSubs;
+constexpr int kFusedSamples = kFusedWarps * 32 / kLanesPerSample;
 
 __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     ib_fused_kernel(const __grid_constant__ FluidParams P, IbSolidDev S, const double* table, double* partial,
@@ -313,10 +316,10 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     if (ctr->diverged) return;
     const RegionGeo& g = P.g;
     const unsigned lane = threadIdx.x & 31u;
-    const unsigned slot = threadIdx.x >> 4;  // sample slot in the block
+    const unsigned slot = threadIdx.x / kLanesPerSample;  // sample slot in the block
     const unsigned s = blockIdx.x * kFusedSamples + slot;
-    const unsigned hl = lane & 15u;          // lane within the sample's half warp
-    const int corner = int(hl >> 1), sub = int(hl & 1u);
+    const unsigned hl = lane % kLanesPerSample;          // lane within the sample's group
+    const int corner = int(hl / kSubs), sub = int(hl % kSubs);
     const double* row = table + (ctr->t - ctr->chunk_t0) * kMotionRow;
     double tot[6] = {0, 0, 0, 0, 0, 0};
     const bool have = s < S.n;
@@ -333,25 +336,28 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     const int lz = act ? ks.base[2] + oz - g.gz0 : 0;
     const float* fin = P.p.f[ctr->t & 1];
     const long long sl = g.sidx(x, y, lz);
-    float v[14];
+    float v[kLoads];
 #pragma unroll
-    for (int j = 0; j < 14; ++j) {  // all fourteen loads in flight at once
-        const int i = sub + 2 * j;
+    for (int j = 0; j < kLoads; ++j) {  // all loads in flight at once
+        const int i = sub + kSubs * j;
         v[j] = i < 27 ? __ldcg(&fin[g.gaddr((unsigned long long)(sl - g.soff(i)), i)]) : 0.f;
     }
     float r = 0.f, jx = 0.f, jy = 0.f, jz = 0.f;
 #pragma unroll
-    for (int j = 0; j < 14; ++j) {
-        const int i = sub + 2 * j;
+    for (int j = 0; j < kLoads; ++j) {
+        const int i = sub + kSubs * j;
         r += v[j];
         jx += float(cx(i)) * v[j];
         jy += float(cy(i)) * v[j];
         jz += float(cz(i)) * v[j];
     }
-    r += __shfl_xor_sync(0xffffffffu, r, 1);
-    jx += __shfl_xor_sync(0xffffffffu, jx, 1);
-    jy += __shfl_xor_sync(0xffffffffu, jy, 1);
-    jz += __shfl_xor_sync(0xffffffffu, jz, 1);
+#pragma unroll
+    for (int o = 1; o < kSubs; o <<= 1) {
+        r += __shfl_xor_sync(0xffffffffu, r, o);
+        jx += __shfl_xor_sync(0xffffffffu, jx, o);
+        jy += __shfl_xor_sync(0xffffffffu, jy, o);
+        jz += __shfl_xor_sync(0xffffffffu, jz, o);
+    }
     const float rho = 1.0f + r;
     const float inv = 1.0f / rho;
     const double wx = ox ? ks.w[0][1] : ks.w[0][0], wy = oy ? ks.w[1][1] : ks.w[1][0];
@@ -360,7 +366,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     double c4[4] = {sub == 0 ? w * double(jx * inv) : 0.0, sub == 0 ? w * double(jy * inv) : 0.0,
                     sub == 0 ? w * double(jz * inv) : 0.0, sub == 0 ? w * double(rho) : 0.0};
 #pragma unroll
-    for (int o = 2; o < 16; o <<= 1)
+    for (int o = kSubs; o < kLanesPerSample; o <<= 1)
 #pragma unroll
         for (int a = 0; a < 4; ++a) c4[a] += __shfl_xor_sync(0xffffffffu, c4[a], o);
     double us[3] = {0.0, 0.0, 0.0}, fg[3] = {0.0, 0.0, 0.0};
