@@ -446,15 +446,10 @@ __device__ __forceinline__ const float* pull_source(const FluidParams& P, int p,
 // bounce-back (f*_i = f_{i'}(N), boundary.cpp:98-100), inlet
 // (feq(1, u_in)_i), periodic wrap / z halo (plain pull) — the outflow chain
 // through pull_source().
-template <int F, int J>
-__device__ __forceinline__ void ghost_fill_entry(const FluidParams& P, int p, unsigned q) {
+template <int F>
+__device__ __forceinline__ void ghost_fill_entry(const FluidParams& P, int p, unsigned q, unsigned j) {
     const RegionGeo& g = P.g;
     constexpr int A = face_axis(F), S = face_side(F);
-    // the direction crossing face F with the other two components from J
-    // (cross9 order, lower axis fastest): everything below folds at compile time
-    constexpr int ja = J % 3 - 1, jb = J / 3 - 1;
-    constexpr int c0 = A == 0 ? -S : ja, c1 = A == 0 ? ja : (A == 1 ? -S : jb), c2 = A == 2 ? -S : jb;
-    constexpr int i = tensor_dir((c0 + 1) + 3 * (c1 + 1) + 9 * (c2 + 1));
     int x, y, lz;
     if constexpr (A == 0) {
         const unsigned qq = g.div_ny.div(q);
@@ -472,42 +467,30 @@ __device__ __forceinline__ void ghost_fill_entry(const FluidParams& P, int p, un
             lz = S < 0 ? 0 : g.nzl - 1;
         }
     }
-    const int own = owner_face_c<i>(g, x, y, g.gz0 + lz);
+    const int ja = int(j % 3u) - 1, jb = int(j / 3u) - 1;
+    const int c0 = A == 0 ? -S : ja, c1 = A == 0 ? ja : (A == 1 ? -S : jb), c2 = A == 2 ? -S : jb;
+    const int i = tensor_dir((c0 + 1) + 3 * (c1 + 1) + 9 * (c2 + 1));
+    const int own = owner_face(g, x, y, g.gz0 + lz, i);
     const unsigned sn = g.sidx(x, y, lz);
     float* fin = P.p.f[p];
     float val;
     if (own == kNoOwner) {  // periodic wrap in x/y, z halo
         int sx = x - c0, sy = y - c1;
-        if constexpr (c0 != 0) sx += sx < 0 ? g.nx : (sx >= g.nx ? -g.nx : 0);
-        if constexpr (c1 != 0) sy += sy < 0 ? g.ny : (sy >= g.ny ? -g.ny : 0);
+        sx += sx < 0 ? g.nx : (sx >= g.nx ? -g.nx : 0);
+        sy += sy < 0 ? g.ny : (sy >= g.ny ? -g.ny : 0);
         const int lzs = lz - c2;
         const unsigned hp = cross9(i, 2) * g.plane + unsigned(sy) * g.nx + unsigned(sx);
-        if (c2 == 1 && lzs < 0) val = P.p.recv_lo[p][hp];
-        else if (c2 == -1 && lzs >= g.nzl) val = P.p.recv_hi[p][hp];
+        if (lzs < 0) val = P.p.recv_lo[p][hp];
+        else if (lzs >= g.nzl) val = P.p.recv_hi[p][hp];
         else val = fin[g.gaddr(g.sidx(sx, sy, lzs), i)];
     } else {
         const int cond = P.faces.cond[own];
-        if (cond == kNoSlip) val = fin[g.gaddr(sn, opposite(i))];
+        if (cond == kNoSlip) val = fin[g.gaddr(sn, 27 - i)];
         else if (cond == kInlet) val = P.faces.inlet[own][i];
         else val = *pull_source(P, p, x, y, lz, i);
         P.p.slot[p ^ 1][own][g.slot_index(own, x, y, lz, i)] = val;
     }
     fin[g.gaddr((unsigned long long)((long long)sn - g.soff(i)), i)] = val;
-}
-
-template <int F>
-__device__ __forceinline__ void ghost_fill_face(const FluidParams& P, int p, unsigned q, unsigned j) {
-    switch (j) {
-        case 0: ghost_fill_entry<F, 0>(P, p, q); break;
-        case 1: ghost_fill_entry<F, 1>(P, p, q); break;
-        case 2: ghost_fill_entry<F, 2>(P, p, q); break;
-        case 3: ghost_fill_entry<F, 3>(P, p, q); break;
-        case 4: ghost_fill_entry<F, 4>(P, p, q); break;
-        case 5: ghost_fill_entry<F, 5>(P, p, q); break;
-        case 6: ghost_fill_entry<F, 6>(P, p, q); break;
-        case 7: ghost_fill_entry<F, 7>(P, p, q); break;
-        default: ghost_fill_entry<F, 8>(P, p, q); break;
-    }
 }
 
 // grid: x over a face's nodes, y = face * 9 + direction slot (block-uniform)
@@ -522,12 +505,12 @@ __global__ void __launch_bounds__(256) ghost_fill_kernel(const __grid_constant__
     if (q >= F) return;
     const int p = int(ctr->t & 1);
     switch (f) {
-        case 0: ghost_fill_face<0>(P, p, q, j); break;
-        case 1: ghost_fill_face<1>(P, p, q, j); break;
-        case 2: ghost_fill_face<2>(P, p, q, j); break;
-        case 3: ghost_fill_face<3>(P, p, q, j); break;
-        case 4: ghost_fill_face<4>(P, p, q, j); break;
-        default: ghost_fill_face<5>(P, p, q, j); break;
+        case 0: ghost_fill_entry<0>(P, p, q, j); break;
+        case 1: ghost_fill_entry<1>(P, p, q, j); break;
+        case 2: ghost_fill_entry<2>(P, p, q, j); break;
+        case 3: ghost_fill_entry<3>(P, p, q, j); break;
+        case 4: ghost_fill_entry<4>(P, p, q, j); break;
+        default: ghost_fill_entry<5>(P, p, q, j); break;
     }
 }
 
