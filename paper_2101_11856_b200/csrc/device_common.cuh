@@ -151,7 +151,7 @@ struct RegionPtrs {
     float* rho;
     float* u;    // 3 planes of ns
     float* gib;  // 3 planes of ns, or null without solids
-    unsigned char* tflag;
+    unsigned* tflag;   // per 32 nodes: step + 1 when the IB scattered into gib this step (epoch, never cleared)
     const float* mrecv_lo;  // (rho,u) of the ghost planes, 4*plane
     const float* mrecv_hi;
     float* msend_lo;

@@ -41,7 +41,11 @@ inline unsigned long long f_alloc_floats(const RegionGeo& g) {
 bool ghost_layout_enabled();
 
 // part: 0 every node, 1 the two halo planes (edge), 2 everything else (bulk)
-void launch_fluid(const FluidParams& P, int part, int write_macro, cudaStream_t st, bool fill = true);
+// end_step: the (single, part 0, ghost-layout) fluid launch also ends the
+// step (t += 1 in its last CTA); returns whether it did, else the caller
+// launches step_end_kernel.
+bool launch_fluid(const FluidParams& P, int part, int write_macro, cudaStream_t st, bool fill = true,
+                  bool end_step = false);
 void launch_macro(const FluidParams& P, int parity, cudaStream_t st);
 void launch_ib_mark(const FluidParams& P, const IbSolidDev& S, unsigned* stamp, unsigned* band,
                     cudaStream_t st);

@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(128) fluid_shell_kernel(const FluidParams P, u
     else shell_decode(g, s, x, y, lz);
     const unsigned k = g.node(x, y, lz);
     const int p = int(ctr->t & 1);
+    const unsigned epoch = unsigned(ctr->t) + 1u;  // IB force flags of this step
     const StepView v = make_view(P, p);
 
     float fs[27];
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(128) fluid_shell_kernel(const FluidParams P, u
         P.p.u[k + 2u * g.ns] = mc.uz;
     }
     float gx = P.m.body[0], gy = P.m.body[1], gz = P.m.body[2];
-    if (P.p.tflag != nullptr && P.p.tflag[k >> 5]) {
+    if (P.p.tflag != nullptr && P.p.tflag[k >> 5] == epoch) {
         float* gib = P.p.gib;
         gx = __fadd_rn(gx, gib[k]);
         gy = __fadd_rn(gy, gib[k + g.ns]);
@@ -284,6 +285,7 @@ __global__ void __launch_bounds__(kBulkThreads, FORM == 2 ? 4 : 3) fluid_bulk_ke
     const unsigned kl = (v0 || v1) ? k : g.plane + unsigned(g.nx) + 2u;
 
     const int p = int(ctr->t & 1);
+    const unsigned epoch = unsigned(ctr->t) + 1u;  // IB force flags of this step
     const float* __restrict__ fin = P.p.f[p];
     float2 fs[27];
     static_for<0, 27>([&](auto I) {
@@ -331,7 +333,7 @@ __global__ void __launch_bounds__(kBulkThreads, FORM == 2 ? 4 : 3) fluid_bulk_ke
     float2 gx = make_float2(P.m.body[0], P.m.body[0]);
     float2 gy = make_float2(P.m.body[1], P.m.body[1]);
     float2 gz = make_float2(P.m.body[2], P.m.body[2]);
-    if (P.p.tflag != nullptr && P.p.tflag[k >> 5]) {
+    if (P.p.tflag != nullptr && P.p.tflag[k >> 5] == epoch) {
         float* gib = P.p.gib;
         float2 a = *reinterpret_cast<const float2*>(gib + k);
         float2 b = *reinterpret_cast<const float2*>(gib + k + g.ns);
@@ -517,7 +519,7 @@ __global__ void __launch_bounds__(256) ghost_fill_kernel(const __grid_constant__
 template <int KIND, int POLICY, bool STD, int T>
 __global__ void __launch_bounds__(T, 512 / T)
     fluid_ghost_kernel(const __grid_constant__ FluidParams P, int z_a, int z_b, int slot, int write_macro, int dbg,
-                       int pf) {
+                       int pf, int end_step) {
     constexpr int kTile = GhostTile<T>::kTile, kWin = GhostTile<T>::kWin;
     constexpr unsigned kStageBytes = GhostTile<T>::kStageBytes;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -533,6 +535,7 @@ __global__ void __launch_bounds__(T, 512 / T)
     }
     const RegionGeo& g = P.g;
     const int p = int(ctr->t & 1);
+    const unsigned epoch = unsigned(ctr->t) + 1u;  // IB force flags of this step
     const float* __restrict__ fin = P.p.f[p];
     float* __restrict__ fout = P.p.f[p ^ 1];
     const unsigned tid = threadIdx.x;
@@ -659,7 +662,7 @@ __global__ void __launch_bounds__(T, 512 / T)
         float2 gx = make_float2(P.m.body[0], P.m.body[0]);
         float2 gy = make_float2(P.m.body[1], P.m.body[1]);
         float2 gz = make_float2(P.m.body[2], P.m.body[2]);
-        if (P.p.tflag != nullptr && P.p.tflag[k >> 5]) {
+        if (P.p.tflag != nullptr && P.p.tflag[k >> 5] == epoch) {
             float* gib = P.p.gib;
             gx = __fadd2_rn(gx, *reinterpret_cast<const float2*>(gib + k));
             gy = __fadd2_rn(gy, *reinterpret_cast<const float2*>(gib + k + g.ns));
@@ -701,6 +704,8 @@ __global__ void __launch_bounds__(T, 512 / T)
         if (atomicAdd(&ctr->tile_done[slot], 1u) == gridDim.x - 1) {
             ctr->tile_ctr[slot] = 0u;
             ctr->tile_done[slot] = 0u;
+            __threadfence();
+            if (end_step && !ctr->diverged) ctr->t += 1;  // step_end_kernel folded in
         }
     }
 }
@@ -830,9 +835,11 @@ bool ghost_layout_enabled() {
 namespace {
 
 thread_local bool t_fill = true;  // launch_fluid(..., fill): the ghost fill is part of this launch
+thread_local bool t_end = false;  // launch_fluid(..., end_step): the fluid kernel also ends the step
 
 template <int KIND, int POLICY, bool STD, int T>
-void launch_ghost_planes_t(const FluidParams& P, int z_a, int z_b, int slot, int write_macro, cudaStream_t st) {
+void launch_ghost_planes_t(const FluidParams& P, int z_a, int z_b, int slot, int write_macro, cudaStream_t st,
+                           int end_step) {
     const RegionGeo& g = P.g;
     constexpr unsigned smem = staged_smem<T>();
     const unsigned ntiles = unsigned(z_b - z_a) * g.PP / GhostTile<T>::kTile + 2;
@@ -857,14 +864,15 @@ void launch_ghost_planes_t(const FluidParams& P, int z_a, int z_b, int slot, int
         const char* e = std::getenv("LBMG_L2_PREFETCH");
         return e ? std::atoi(e) : 0;
     }();
-    kern<<<grid, T, smem, st>>>(P, z_a, z_b, slot, write_macro, dbg, pf_periods * kStages * int(grid));
+    kern<<<grid, T, smem, st>>>(P, z_a, z_b, slot, write_macro, dbg, pf_periods * kStages * int(grid), end_step);
 }
 
 // CTA size of the staged kernel (LBMG_GHOST_THREADS, default 512 = 1024-slot
 // tiles, one CTA of 16 warps per SM, 2 x 111 KB stages: measured fastest,
 // C3 4.92 ms vs 5.31 (256) vs 6.00 (128)); a tile must fit one Eq. 9 block.
 template <int KIND, int POLICY, bool STD>
-void launch_ghost_planes(const FluidParams& P, int z_a, int z_b, int slot, int write_macro, cudaStream_t st) {
+void launch_ghost_planes(const FluidParams& P, int z_a, int z_b, int slot, int write_macro, cudaStream_t st,
+                         int end_step = 0) {
     if (z_b <= z_a) return;
     static const int threads = [] {
         const char* e = std::getenv("LBMG_GHOST_THREADS");
@@ -872,11 +880,11 @@ void launch_ghost_planes(const FluidParams& P, int z_a, int z_b, int slot, int w
     }();
     const unsigned block = P.g.amask + 1u;  // Eq. 9 block (slots); SoA: 2^31
     if (threads >= 512 && block >= 1024u)
-        launch_ghost_planes_t<KIND, POLICY, STD, 512>(P, z_a, z_b, slot, write_macro, st);
+        launch_ghost_planes_t<KIND, POLICY, STD, 512>(P, z_a, z_b, slot, write_macro, st, end_step);
     else if (threads >= 256 && block >= 512u)
-        launch_ghost_planes_t<KIND, POLICY, STD, 256>(P, z_a, z_b, slot, write_macro, st);
+        launch_ghost_planes_t<KIND, POLICY, STD, 256>(P, z_a, z_b, slot, write_macro, st, end_step);
     else
-        launch_ghost_planes_t<KIND, POLICY, STD, 128>(P, z_a, z_b, slot, write_macro, st);
+        launch_ghost_planes_t<KIND, POLICY, STD, 128>(P, z_a, z_b, slot, write_macro, st, end_step);
 }
 
 // part 0: every plane; 1: ghost fill + the slab's boundary planes (which feed
@@ -886,7 +894,7 @@ void launch_fluid_ghost(const FluidParams& P, int part, int write_macro, cudaStr
     const RegionGeo& g = P.g;
     if ((part == 0 || part == 1) && t_fill) launch_ghost_fill(P, st);
     if (part == 0) {
-        launch_ghost_planes<KIND, POLICY, STD>(P, 0, g.nzl, 0, write_macro, st);
+        launch_ghost_planes<KIND, POLICY, STD>(P, 0, g.nzl, 0, write_macro, st, t_end ? 1 : 0);
     } else if (part == 1) {
         launch_ghost_planes<KIND, POLICY, STD>(P, 0, 1, 0, write_macro, st);
         if (g.nzl > 1) launch_ghost_planes<KIND, POLICY, STD>(P, g.nzl - 1, g.nzl, 1, write_macro, st);
@@ -951,13 +959,15 @@ void launch_ghost_fill(const FluidParams& P, cudaStream_t st, bool) {
     ghost_fill_kernel<<<dim3(blocks_for(fmax, 256), 54), 256, 0, st>>>(P);
 }
 
-void launch_fluid(const FluidParams& P, int part, int write_macro, cudaStream_t st, bool fill) {
+bool launch_fluid(const FluidParams& P, int part, int write_macro, cudaStream_t st, bool fill, bool end_step) {
     t_fill = fill;
+    t_end = end_step && part == 0 && P.g.ghost && fluid_form() == 2;
     switch (fluid_form()) {
         case 0: launch_fluid_form<0>(P, part, write_macro, st); break;
         case 1: launch_fluid_form<1>(P, part, write_macro, st); break;
         default: launch_fluid_form<2>(P, part, write_macro, st); break;
     }
+    return t_end;
 }
 
 void launch_macro(const FluidParams& P, int parity, cudaStream_t st) {

@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kSpreadThreads) ib_spread_kernel(const FluidPa
                             atomicAdd(&P.p.gib[key], float(w * fg[0]));
                             atomicAdd(&P.p.gib[key + g.ns], float(w * fg[1]));
                             atomicAdd(&P.p.gib[key + 2u * g.ns], float(w * fg[2]));
-                            P.p.tflag[key >> 5] = 1;
+                            P.p.tflag[key >> 5] = unsigned(P.ctr->t) + 1u;
                             continue;
                         }
                         unsigned h = (key * 2654435761u) & (kHashSlots - 1);
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kSpreadThreads) ib_spread_kernel(const FluidPa
         atomicAdd(&P.p.gib[key], hval[0][j]);
         atomicAdd(&P.p.gib[key + g.ns], hval[1][j]);
         atomicAdd(&P.p.gib[key + 2u * g.ns], hval[2][j]);
-        P.p.tflag[key >> 5] = 1;
+        P.p.tflag[key >> 5] = unsigned(P.ctr->t) + 1u;
     }
 }
 
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
             atomicAdd(&P.p.gib[k], float(w * fg[0]));
             atomicAdd(&P.p.gib[k + g.ns], float(w * fg[1]));
             atomicAdd(&P.p.gib[k + 2u * g.ns], float(w * fg[2]));
-            P.p.tflag[k >> 5] = 1;
+            P.p.tflag[k >> 5] = unsigned(P.ctr->t) + 1u;
         }
     }
     if (have && hl == 0) {

@@ -290,7 +290,7 @@ void Runner::build_regions(int) {
         r.ptr.u = static_cast<float*>(dalloc(sizeof(float) * 3ull * g.ns));
         if (has_solids_) {
             r.ptr.gib = static_cast<float*>(dalloc(sizeof(float) * 3ull * g.ns));
-            r.ptr.tflag = static_cast<unsigned char*>(dalloc(g.ns / 32 + 1));
+            r.ptr.tflag = static_cast<unsigned*>(dalloc(sizeof(unsigned) * (g.ns / 32 + 1)));
             r.stamp = static_cast<unsigned*>(dalloc(sizeof(unsigned) * g.ns));
             const size_t cap = std::max<size_t>(1, std::min<size_t>(g.n, 8 * total_samples_));
             r.band = static_cast<unsigned*>(dalloc(sizeof(unsigned) * cap));
@@ -582,14 +582,13 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
     }
     if (overlap) CK(cudaStreamWaitEvent(st, join_, 0));
     if (ev) CK(cudaEventRecord((*ev)[2], st));
+    bool ended = false;
     for (auto& r : regions_) {
         FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
-        launch_fluid(P, 0, write_macro, st, false);
+        ended = launch_fluid(P, 0, write_macro, st, false, regions_.size() == 1);
     }
     if (ev) CK(cudaEventRecord((*ev)[3], st));
-    if (has_solids_)
-        for (auto& r : regions_) CK(cudaMemsetAsync(r.ptr.tflag, 0, r.geo.ns / 32 + 1, st));
-    launch_step_end(ctr_, st);
+    if (!ended) launch_step_end(ctr_, st);
     if (ev) CK(cudaEventRecord((*ev)[4], st));
 }
 
@@ -1026,8 +1025,6 @@ void Runner::phase(int ph, int write_macro) {
         case LBMG_PHASE_FLUID_EDGE: enqueue_fluid(write_macro != 0, 1); break;
         case LBMG_PHASE_FLUID_BULK: enqueue_fluid(write_macro != 0, 2); break;
         case LBMG_PHASE_END:
-            if (has_solids_)
-                for (auto& r : regions_) CK(cudaMemsetAsync(r.ptr.tflag, 0, r.geo.ns / 32 + 1, stream()));
             launch_step_end(ctr_, stream());
             break;
         default: throw StateError("unknown phase");
