@@ -617,6 +617,10 @@ __global__ void __launch_bounds__(T, 512 / T)
         const int x = col - 2, y = r - 1, lz = int(pl) - 1;
         // pairs are all-ghost or all-owned (nx, PX even)
         const bool valid = sl >= sb && sl < se && x >= 0 && x < g.nx && y >= 0;
+        // IB force flag of the pair's 32-node group, loaded early (consumed
+        // after the moments, so its latency hides behind the shared-memory reads)
+        const unsigned kf = valid ? (unsigned(lz) * g.ny + unsigned(y)) * g.nx + unsigned(x) : 0u;
+        const unsigned tflag_word = P.p.tflag != nullptr ? __ldcg(&P.p.tflag[kf >> 5]) : 0u;
         float2 fs[27];
         static_for<0, 27>([&](auto I) {
             constexpr int i = decltype(I)::value;
@@ -662,7 +666,7 @@ __global__ void __launch_bounds__(T, 512 / T)
         float2 gx = make_float2(P.m.body[0], P.m.body[0]);
         float2 gy = make_float2(P.m.body[1], P.m.body[1]);
         float2 gz = make_float2(P.m.body[2], P.m.body[2]);
-        if (P.p.tflag != nullptr && P.p.tflag[k >> 5] == epoch) {
+        if (tflag_word == epoch) {
             float* gib = P.p.gib;
             gx = __fadd2_rn(gx, *reinterpret_cast<const float2*>(gib + k));
             gy = __fadd2_rn(gy, *reinterpret_cast<const float2*>(gib + k + g.ns));
