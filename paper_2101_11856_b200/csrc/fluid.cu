@@ -549,14 +549,16 @@ __global__ void __launch_bounds__(T, 512 / T)
     // stay open across CTAs and the window edges two neighbouring tiles share
     // are fetched once and hit in L2 for the other.
     unsigned* const next_tile = &ctr->tile_ctr[slot];
-    __shared__ unsigned stage_tile[kStages];
+    // tile id per (stage, phase parity): the refill for phase k+1 writes the
+    // other parity slot than the one phase-k readers use (no WAR hazard)
+    __shared__ unsigned stage_tile[kStages][2];
     __shared__ unsigned reads_done[kStages];
 
     // claim the next tile into stage s (elected thread); past the end the
     // stage's phase completes empty so the consumers see the end marker
-    auto refill = [&](int s) {
+    auto refill = [&](int s, unsigned phase) {
         const unsigned tile = atomicAdd(next_tile, 1u);
-        stage_tile[s] = tile;
+        stage_tile[s][phase & 1u] = tile;
         if (tile >= ntiles) {
             mbar_arrive(&full[s]);
             return;
@@ -586,13 +588,13 @@ __global__ void __launch_bounds__(T, 512 / T)
     }
     __syncthreads();
     if (tid == 0)
-        for (int s = 0; s < kStages; ++s) refill(s);
+        for (int s = 0; s < kStages; ++s) refill(s, 0u);
 
     for (unsigned it = 0;; ++it) {
         const int s = int(it % kStages);
         const float* const st = stage0 + s * (kStageBytes / 4);
         mbar_wait_parity(&full[s], (it / kStages) & 1u);
-        const unsigned tile = stage_tile[s];
+        const unsigned tile = stage_tile[s][(it / kStages) & 1u];
         if (tile >= ntiles) break;
         // Tiles are claimed in order by all CTAs, so tile + pf will be claimed
         // about pf / (stages * grid) tile periods from now: pull its windows
@@ -634,8 +636,9 @@ __global__ void __launch_bounds__(T, 512 / T)
             __threadfence_block();  // this warp's reads of stage s are done
             if (atomicAdd(&reads_done[s], 1u) == T / 32 - 1) {
                 reads_done[s] = 0;
+                __threadfence_block();  // (acquire: every warp's reads of stage s precede the refill)
                 fence_proxy_async_smem();
-                refill(s);
+                refill(s, it / kStages + 1u);
             }
         }
         if (!valid) continue;
