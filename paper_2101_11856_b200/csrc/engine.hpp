@@ -17,6 +17,16 @@ struct IbSolidDev {
     double* sampled;  // n*3
     unsigned* source;
     unsigned char* flagged;
+    // deterministic accumulation (ib_accumulation = deterministic): one
+    // record per (sample, support corner) = (owned node | ~0u, w * g_s);
+    // sorted by node (stable: sample order), summed per node in FP64
+    unsigned* rec_key = nullptr;   // 8n
+    unsigned* rec_idx = nullptr;   // 8n
+    double* rec_val = nullptr;     // 3 * 8n
+    unsigned* key_sorted = nullptr;
+    unsigned* idx_sorted = nullptr;
+    void* sort_temp = nullptr;
+    size_t sort_temp_bytes = 0;
 };
 
 // Motion table row per step: center(t)[3], R(t)[9], v[3], omega[3].
@@ -51,12 +61,16 @@ void launch_ib_mark(const FluidParams& P, const IbSolidDev& S, unsigned* stamp, 
                     cudaStream_t st);
 void launch_ib_band(const FluidParams& P, const unsigned* band, int sm_count, cudaStream_t st);
 void launch_macro_pack(const FluidParams& P, cudaStream_t st);
-void launch_ib_spread(const FluidParams& P, const IbSolidDev& S, cudaStream_t st);
+void launch_ib_spread(const FluidParams& P, const IbSolidDev& S, cudaStream_t st, bool deterministic = false);
+// deterministic accumulation: CUB temp bytes for 8n records; the sort +
+// fixed-order per-node FP64 sum into g (after the spread / fused kernel)
+size_t ib_det_temp_bytes(unsigned n_samples);
+void launch_ib_det_reduce(const FluidParams& P, const IbSolidDev& S, cudaStream_t st);
 int totals_blocks(size_t n);
 // single-region ghost-layout IB step (interp + penalty + scatter + totals + motion), after launch_ghost_fill
 int fused_blocks(size_t n);
 void launch_ib_fused(const FluidParams& P, const IbSolidDev& S, const double* table, double* partial, unsigned* done,
-                     double* out_base, int stride, bool moving, cudaStream_t st);
+                     double* out_base, int stride, bool moving, cudaStream_t st, bool deterministic = false);
 // ghost slots of this step: full = every entry (after init / relayout),
 // otherwise only what the previous fluid step did not push
 void launch_ghost_fill(const FluidParams& P, cudaStream_t st, bool full = false);

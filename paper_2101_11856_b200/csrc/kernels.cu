@@ -16,6 +16,8 @@
 //   step_end     t += 1 unless diverged
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -107,7 +109,7 @@ __global__ void ib_mark_kernel(const FluidParams P, IbSolidDev S, unsigned* stam
 constexpr int kSpreadThreads = 128;
 constexpr int kHashSlots = 2048;  // >= 2 * 8 * kSpreadThreads (load <= 0.5), power of two
 
-template <bool SMEM>
+template <bool SMEM, bool DET = false>
 __global__ void __launch_bounds__(kSpreadThreads) ib_spread_kernel(const FluidParams P, IbSolidDev S) {
     __shared__ unsigned hkey[SMEM ? kHashSlots : 1];
     __shared__ float hval[3][SMEM ? kHashSlots : 1];
@@ -163,7 +165,18 @@ __global__ void __launch_bounds__(kSpreadThreads) ib_spread_kernel(const FluidPa
             S.sampled[3 * s + a] = us[a];
             S.force[3 * s + a] = fg[a];
         }
-        if (active) {
+        if constexpr (DET) {  // one (owned node | ~0u, w g_s) record per corner, sample-major
+            for (int c = 0; c < 8; ++c) {
+                const int ox = c & 1, oy = (c >> 1) & 1, oz = c >> 2;
+                const int gz = ks.base[2] + oz;
+                const unsigned rec = s * 8u + unsigned(c);
+                const bool own = active && gz >= z0 && gz < z1;
+                S.rec_key[rec] = own ? g.node(ks.base[0] + ox, ks.base[1] + oy, gz - g.gz0) : ~0u;
+                S.rec_idx[rec] = rec;
+                const double w = __dmul_rn(__dmul_rn(ks.w[0][ox], ks.w[1][oy]), ks.w[2][oz]);
+                for (int a = 0; a < 3; ++a) S.rec_val[3 * rec + a] = own ? w * fg[a] : 0.0;
+            }
+        } else if (active) {
             for (int oz = 0; oz < 2; ++oz) {
                 const int gz = ks.base[2] + oz;
                 if (gz < z0 || gz >= z1) continue;
@@ -309,7 +322,7 @@ constexpr int kFusedSamples = kFusedWarps * 32 / kLanesPerSample;
 
 __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     ib_fused_kernel(const __grid_constant__ FluidParams P, IbSolidDev S, const double* table, double* partial,
-                    unsigned* done, double* out_base, int stride, int moving) {
+                    unsigned* done, double* out_base, int stride, int moving, int det) {
     __shared__ double red[kFusedSamples][6];
     __shared__ bool last;
     DevCounters* ctr = P.ctr;
@@ -375,13 +388,22 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
             us[a] = c4[a];
             fg[a] = c4[3] * (ub[a] - us[a]);
         }
-        if (sub == 0) {  // scatter of this corner (owned: single region)
+        if (sub == 0 && det) {  // deterministic: a (node, contribution) record per corner
+            const unsigned rec = s * 8u + unsigned(corner);
+            S.rec_key[rec] = g.node(x, y, lz);
+            S.rec_idx[rec] = rec;
+            for (int a = 0; a < 3; ++a) S.rec_val[3 * rec + a] = w * fg[a];
+        } else if (sub == 0) {  // scatter of this corner (owned: single region)
             const unsigned k = g.node(x, y, lz);
             atomicAdd(&P.p.gib[k], float(w * fg[0]));
             atomicAdd(&P.p.gib[k + g.ns], float(w * fg[1]));
             atomicAdd(&P.p.gib[k + 2u * g.ns], float(w * fg[2]));
             P.p.tflag[k >> 5] = unsigned(P.ctr->t) + 1u;
         }
+    }
+    if (det && have && !act && sub == 0) {  // inactive sample: empty records
+        S.rec_key[s * 8u + unsigned(corner)] = ~0u;
+        S.rec_idx[s * 8u + unsigned(corner)] = s * 8u + unsigned(corner);
     }
     if (have && hl == 0) {
         for (int a = 0; a < 3; ++a) {
@@ -560,8 +582,52 @@ void launch_ib_mark(const FluidParams& P, const IbSolidDev& S, unsigned* stamp, 
 
 
 
-void launch_ib_spread(const FluidParams& P, const IbSolidDev& S, cudaStream_t st) {
+// Deterministic accumulation: stable radix sort of the records by node (ties
+// keep record = sample order), then one thread per node segment sums its
+// contributions in that order in FP64 and adds the fp32 result to g.  The
+// sum no longer depends on atomic timing, so runs are bitwise reproducible
+// and independent of the region count (SPEC criterion 9; ib.cpp:407-453
+// groups by colour instead — same contract, different fixed order).
+__global__ void ib_det_segment_kernel(const FluidParams P, IbSolidDev S, unsigned n_rec) {
+    const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_rec || P.ctr->diverged) return;
+    const unsigned k = S.key_sorted[i];
+    if (k == ~0u || (i > 0 && S.key_sorted[i - 1] == k)) return;
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (unsigned j = i; j < n_rec && S.key_sorted[j] == k; ++j) {
+        const unsigned r = S.idx_sorted[j];
+        for (int a = 0; a < 3; ++a) acc[a] += S.rec_val[3 * r + a];
+    }
+    const RegionGeo& g = P.g;
+    P.p.gib[k] += float(acc[0]);
+    P.p.gib[k + g.ns] += float(acc[1]);
+    P.p.gib[k + 2u * g.ns] += float(acc[2]);
+    P.p.tflag[k >> 5] = unsigned(P.ctr->t) + 1u;
+}
+
+size_t ib_det_temp_bytes(unsigned n_samples) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const unsigned*)nullptr, (unsigned*)nullptr,
+                                    (const unsigned*)nullptr, (unsigned*)nullptr, int(8u * n_samples));
+    return bytes;
+}
+
+void launch_ib_det_reduce(const FluidParams& P, const IbSolidDev& S, cudaStream_t st) {
     if (S.n == 0) return;
+    const unsigned n_rec = 8u * S.n;
+    size_t bytes = S.sort_temp_bytes;
+    cub::DeviceRadixSort::SortPairs(S.sort_temp, bytes, S.rec_key, S.key_sorted, S.rec_idx, S.idx_sorted,
+                                    int(n_rec), 0, 32, st);
+    ib_det_segment_kernel<<<blocks_for(n_rec, 256), 256, 0, st>>>(P, S, n_rec);
+}
+
+void launch_ib_spread(const FluidParams& P, const IbSolidDev& S, cudaStream_t st, bool deterministic) {
+    if (S.n == 0) return;
+    if (deterministic) {
+        ib_spread_kernel<false, true><<<blocks_for(S.n, kSpreadThreads), kSpreadThreads, 0, st>>>(P, S);
+        launch_ib_det_reduce(P, S, st);
+        return;
+    }
     static const bool smem = [] {
         const char* e = std::getenv("LBMG_IB_SPREAD");
         return e && std::string(e) == "smem";
@@ -572,10 +638,11 @@ void launch_ib_spread(const FluidParams& P, const IbSolidDev& S, cudaStream_t st
 
 int fused_blocks(size_t n) { return int((n + kFusedSamples - 1) / kFusedSamples); }
 void launch_ib_fused(const FluidParams& P, const IbSolidDev& S, const double* table, double* partial, unsigned* done,
-                     double* out_base, int stride, bool moving, cudaStream_t st) {
+                     double* out_base, int stride, bool moving, cudaStream_t st, bool deterministic) {
     if (S.n == 0) return;
     ib_fused_kernel<<<fused_blocks(S.n), kFusedWarps * 32, 0, st>>>(P, S, table, partial, done, out_base, stride,
-                                                                     moving ? 1 : 0);
+                                                                     moving ? 1 : 0, deterministic ? 1 : 0);
+    if (deterministic) launch_ib_det_reduce(P, S, st);
 }
 int totals_blocks(size_t n) {
     size_t b = (n + kTotThreads - 1) / kTotThreads;

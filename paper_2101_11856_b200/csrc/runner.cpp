@@ -375,6 +375,15 @@ void Runner::upload_solids() {
             d.sampled = static_cast<double*>(dalloc(sizeof(double) * 3 * n));
             d.source = static_cast<unsigned*>(dalloc(sizeof(unsigned) * n));
             d.flagged = static_cast<unsigned char*>(dalloc(n));
+            if (scene_.cfg.ib_mode == LBMG_IB_DETERMINISTIC && n) {
+                d.rec_key = static_cast<unsigned*>(dalloc(sizeof(unsigned) * 8 * n));
+                d.rec_idx = static_cast<unsigned*>(dalloc(sizeof(unsigned) * 8 * n));
+                d.key_sorted = static_cast<unsigned*>(dalloc(sizeof(unsigned) * 8 * n));
+                d.idx_sorted = static_cast<unsigned*>(dalloc(sizeof(unsigned) * 8 * n));
+                d.rec_val = static_cast<double*>(dalloc(sizeof(double) * 24 * n));
+                d.sort_temp_bytes = ib_det_temp_bytes(unsigned(n));
+                d.sort_temp = dalloc(d.sort_temp_bytes);
+            }
             std::vector<double> pos(3 * n), ref(3 * n);
             for (size_t k = 0; k < n; ++k)
                 for (int a = 0; a < 3; ++a) {
@@ -493,7 +502,7 @@ void Runner::enqueue_ib_mid() {
     const int m = int(regions_.size());
     for (auto& r : regions_) {
         FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
-        for (auto& s : r.solids) launch_ib_spread(P, s, st);
+        for (auto& s : r.solids) launch_ib_spread(P, s, st, scene_.cfg.ib_mode == LBMG_IB_DETERMINISTIC);
     }
     for (int ri = 0; ri < m; ++ri) {
         Region& r = regions_[ri];
@@ -575,7 +584,8 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
         const int ns = int(scene_.solids.size());
         for (int s = 0; s < ns; ++s)
             launch_ib_fused(P, r.solids[s], motion_tab_ + size_t(s) * (cap_ + 2) * kMotionRow, r.fused_partial,
-                            r.fused_done, totals_dev_ + size_t(s) * 6, ns * 6, moving_[s] != 0, st);
+                            r.fused_done, totals_dev_ + size_t(s) * 6, ns * 6, moving_[s] != 0, st,
+                            scene_.cfg.ib_mode == LBMG_IB_DETERMINISTIC);
     } else if (has_solids_) {
         enqueue_ib_pre();
         enqueue_ib_mid();

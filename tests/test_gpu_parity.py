@@ -186,6 +186,39 @@ def test_open_channel_sphere_parity_small():
     assert np.abs(a["penalty_force"] - b["penalty_force"]).max() <= 1e-3 * np.abs(b["penalty_force"]).max()
 
 
+def _det_sphere():
+    cfg = scenes.sphere(48, 32, 32, center=(16, 16, 16), radius=5.0, subdiv=3, r=0.6)
+    cfg.ib_mode = "deterministic"
+    return cfg
+
+
+def test_deterministic_ib_is_reproducible_and_matches_reference():
+    cfg = _det_sphere()
+    outs = []
+    for _ in range(2):
+        g = lbm.Runner(lbm.build_scene(cfg))
+        g.advance(30)
+        outs.append((g.gather_f(), g.totals_log()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    g, r, sg, sr = run_pair(cfg, 30)
+    assert sg.ok and sr["ok"]
+    assert_fields_close(g, r, f_tol=2e-5)
+
+
+def test_deterministic_ib_region_count_bitwise():
+    # SPEC criterion 9 with solids: the split IB pipeline on every region count
+    # (per-node FP64 sums in sample order, no atomics) -> bit-identical fields
+    cfg = _det_sphere()
+    outs = []
+    for m in (1, 2, 3):
+        g = lbm.Runner(lbm.build_scene(cfg), regions=m)
+        g.set_variant(0, 1)
+        g.advance(25)
+        outs.append(g.gather_f())
+    for o in outs[1:]:
+        assert np.array_equal(outs[0], o)
+
+
 def test_moving_solid_parity():
     cfg = scenes.rotating_fins(96, 48, 48)
     cfg.solids[0].mesh.origin = (38, 16, 16)
