@@ -642,6 +642,21 @@ __global__ void __launch_bounds__(T, 512 / T)
             }
         }
         if (!valid) continue;
+        const unsigned k = (unsigned(lz) * g.ny + unsigned(y)) * g.nx + unsigned(x);  // compact node index
+        // body force + this step's IB force (loads issued before the moments:
+        // their latency hides behind them; consumed at the end of collide)
+        float2 gx = make_float2(P.m.body[0], P.m.body[0]);
+        float2 gy = make_float2(P.m.body[1], P.m.body[1]);
+        float2 gz = make_float2(P.m.body[2], P.m.body[2]);
+        if (tflag_word == epoch) {
+            float* gib = P.p.gib;
+            gx = __fadd2_rn(gx, __ldcg(reinterpret_cast<const float2*>(gib + k)));
+            gy = __fadd2_rn(gy, __ldcg(reinterpret_cast<const float2*>(gib + k + g.ns)));
+            gz = __fadd2_rn(gz, __ldcg(reinterpret_cast<const float2*>(gib + k + 2u * g.ns)));
+            *reinterpret_cast<float2*>(gib + k) = make_float2(0.f, 0.f);
+            *reinterpret_cast<float2*>(gib + k + g.ns) = make_float2(0.f, 0.f);
+            *reinterpret_cast<float2*>(gib + k + 2u * g.ns) = make_float2(0.f, 0.f);
+        }
         if (dbg & 3) {  // bandwidth probes: 1 = staged loads only, 2 = loads + stores (no collision)
             if ((dbg & 3) == 2)
                 static_for<0, 27>([&](auto I) {
@@ -653,7 +668,6 @@ __global__ void __launch_bounds__(T, 512 / T)
             continue;
         }
 
-        const unsigned k = (unsigned(lz) * g.ny + unsigned(y)) * g.nx + unsigned(x);  // compact node index
         const MacroV<float2> mc = moments_v<float2>(fs);
         if (mc.bad[0] || mc.bad[1]) {
             flag_divergence(ctr);
@@ -665,18 +679,6 @@ __global__ void __launch_bounds__(T, 512 / T)
             *reinterpret_cast<float2*>(P.p.u + k) = mc.ux;
             *reinterpret_cast<float2*>(P.p.u + k + g.ns) = mc.uy;
             *reinterpret_cast<float2*>(P.p.u + k + 2u * g.ns) = mc.uz;
-        }
-        float2 gx = make_float2(P.m.body[0], P.m.body[0]);
-        float2 gy = make_float2(P.m.body[1], P.m.body[1]);
-        float2 gz = make_float2(P.m.body[2], P.m.body[2]);
-        if (tflag_word == epoch) {
-            float* gib = P.p.gib;
-            gx = __fadd2_rn(gx, *reinterpret_cast<const float2*>(gib + k));
-            gy = __fadd2_rn(gy, *reinterpret_cast<const float2*>(gib + k + g.ns));
-            gz = __fadd2_rn(gz, *reinterpret_cast<const float2*>(gib + k + 2u * g.ns));
-            *reinterpret_cast<float2*>(gib + k) = make_float2(0.f, 0.f);
-            *reinterpret_cast<float2*>(gib + k + g.ns) = make_float2(0.f, 0.f);
-            *reinterpret_cast<float2*>(gib + k + 2u * g.ns) = make_float2(0.f, 0.f);
         }
         const bool any_force = gx.x != 0.f || gx.y != 0.f || gy.x != 0.f || gy.y != 0.f || gz.x != 0.f || gz.y != 0.f;
         NoStash<float2> stash;
