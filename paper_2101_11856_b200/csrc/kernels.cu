@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
             S.rec_key[rec] = g.node(x, y, lz);
             S.rec_idx[rec] = rec;
             for (int a = 0; a < 3; ++a) S.rec_val[3 * rec + a] = w * fg[a];
-        } else if (sub == 0) {  // scatter of this corner (owned: single region)
+        } else if (sub == 0 && !(moving & 2)) {  // scatter of this corner (owned: single region)
             const unsigned k = g.node(x, y, lz);
             atomicAdd(&P.p.gib[k], float(w * fg[0]));
             atomicAdd(&P.p.gib[k + g.ns], float(w * fg[1]));
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
             tot[4] = -(rr[2] * fg[0] - rr[0] * fg[2]);
             tot[5] = -(rr[0] * fg[1] - rr[1] * fg[0]);
         }
-        if (moving) motion_apply(row + kMotionRow, S, s, g.nx, g.ny, g.NZ);
+        if (moving & 1) motion_apply(row + kMotionRow, S, s, g.nx, g.ny, g.NZ);
     }
     if (hl == 0)
         for (int a = 0; a < 6; ++a) red[slot][a] = tot[a];
@@ -640,8 +640,12 @@ int fused_blocks(size_t n) { return int((n + kFusedSamples - 1) / kFusedSamples)
 void launch_ib_fused(const FluidParams& P, const IbSolidDev& S, const double* table, double* partial, unsigned* done,
                      double* out_base, int stride, bool moving, cudaStream_t st, bool deterministic) {
     if (S.n == 0) return;
+    static const int probe = [] {  // timing probe: LBMG_IB_NOSCATTER=1 skips the scatter into g
+        const char* e = std::getenv("LBMG_IB_NOSCATTER");
+        return e && std::atoi(e) ? 2 : 0;
+    }();
     ib_fused_kernel<<<fused_blocks(S.n), kFusedWarps * 32, 0, st>>>(P, S, table, partial, done, out_base, stride,
-                                                                     moving ? 1 : 0, deterministic ? 1 : 0);
+                                                                     (moving ? 1 : 0) | probe, deterministic ? 1 : 0);
     if (deterministic) launch_ib_det_reduce(P, S, st);
 }
 int totals_blocks(size_t n) {
