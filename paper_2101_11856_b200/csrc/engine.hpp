@@ -69,8 +69,23 @@ void launch_ib_det_reduce(const FluidParams& P, const IbSolidDev& S, cudaStream_
 int totals_blocks(size_t n);
 // single-region ghost-layout IB step (interp + penalty + scatter + totals + motion), after launch_ghost_fill
 int fused_blocks(size_t n);
-void launch_ib_fused(const FluidParams& P, const IbSolidDev& S, const double* table, double* partial, unsigned* done,
-                     double* out_base, int stride, bool moving, cudaStream_t st, bool deterministic = false);
+// every solid in one launch (device descriptors); totals row of solid k at
+// out_base[(t - chunk_t0) * out_stride + 6k]
+struct IbBatch {
+    const IbSolidDev* solids;      // device copy, n_solids
+    const unsigned* block_start;   // n_solids + 1 prefix of fused_blocks(n_k)
+    const int* moving;             // n_solids
+    unsigned n_solids;
+    const double* table;           // motion rows, table_stride doubles per solid
+    size_t table_stride;
+    double* partial;               // 6 per block
+    unsigned* done;                // n_solids counters
+    double* out_base;
+    int out_stride;
+    int probe;
+};
+void launch_ib_fused(const FluidParams& P, IbBatch B, unsigned total_blocks, const IbSolidDev* host_solids,
+                     cudaStream_t st, bool deterministic = false);
 // ghost slots of this step: full = every entry (after init / relayout),
 // otherwise only what the previous fluid step did not push
 void launch_ghost_fill(const FluidParams& P, cudaStream_t st, bool full = false);

@@ -320,17 +320,33 @@ constexpr int kSubs = kLanesPerSample / 8;
 constexpr int kLoads = (27 + kSubs - 1) / kSubs;
 constexpr int kFusedSamples = kFusedWarps * 32 / kLanesPerSample;
 
+// All solids of the scene in ONE launch: blocks [block_start[k], block_start[k+1])
+// belong to solid k (per-solid totals reductions keep their own counters).
 __global__ void __launch_bounds__(kFusedWarps * 32, 8)
-    ib_fused_kernel(const __grid_constant__ FluidParams P, IbSolidDev S, const double* table, double* partial,
-                    unsigned* done, double* out_base, int stride, int moving, int det) {
+    ib_fused_kernel(const __grid_constant__ FluidParams P, IbBatch B, int det) {
     __shared__ double red[kFusedSamples][6];
     __shared__ bool last;
     DevCounters* ctr = P.ctr;
     if (ctr->diverged) return;
     const RegionGeo& g = P.g;
+    unsigned lo = 0, hi = B.n_solids;
+    while (hi - lo > 1) {
+        const unsigned mid = (lo + hi) >> 1;
+        if (B.block_start[mid] <= blockIdx.x) lo = mid;
+        else hi = mid;
+    }
+    const unsigned solid = lo;
+    const IbSolidDev S = B.solids[solid];
+    const double* table = B.table + size_t(solid) * B.table_stride;
+    const int moving = B.moving[solid] | B.probe;
+    const unsigned b0 = B.block_start[solid], nblk = B.block_start[solid + 1] - b0;
+    double* partial = B.partial + size_t(b0) * 6;
+    unsigned* done = B.done + solid;
+    double* out_base = B.out_base + 6 * solid;
+    const int stride = B.out_stride;
     const unsigned lane = threadIdx.x & 31u;
     const unsigned slot = threadIdx.x / kLanesPerSample;  // sample slot in the block
-    const unsigned s = blockIdx.x * kFusedSamples + slot;
+    const unsigned s = (blockIdx.x - b0) * kFusedSamples + slot;
     const unsigned hl = lane % kLanesPerSample;          // lane within the sample's group
     const int corner = int(hl / kSubs), sub = int(hl % kSubs);
     const double* row = table + (ctr->t - ctr->chunk_t0) * kMotionRow;
@@ -427,11 +443,11 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     if (threadIdx.x < 6) {
         double acc = 0.0;
         for (int w = 0; w < kFusedSamples; ++w) acc += red[w][threadIdx.x];
-        partial[blockIdx.x * 6 + threadIdx.x] = acc;
+        partial[(blockIdx.x - b0) * 6 + threadIdx.x] = acc;
         __threadfence();
     }
     __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == nblk - 1;
     __syncthreads();
     if (!last) return;
     __threadfence();
@@ -439,7 +455,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     // then a shared-memory tree (independent of which block finished last)
     __shared__ double tree[6][kFusedWarps * 32];
     double acc[6] = {0, 0, 0, 0, 0, 0};
-    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+    for (unsigned b = threadIdx.x; b < nblk; b += blockDim.x)
         for (int a = 0; a < 6; ++a) acc[a] += __ldcg(&partial[b * 6 + a]);
     for (int a = 0; a < 6; ++a) tree[a][threadIdx.x] = acc[a];
     __syncthreads();
@@ -637,16 +653,17 @@ void launch_ib_spread(const FluidParams& P, const IbSolidDev& S, cudaStream_t st
 }
 
 int fused_blocks(size_t n) { return int((n + kFusedSamples - 1) / kFusedSamples); }
-void launch_ib_fused(const FluidParams& P, const IbSolidDev& S, const double* table, double* partial, unsigned* done,
-                     double* out_base, int stride, bool moving, cudaStream_t st, bool deterministic) {
-    if (S.n == 0) return;
+void launch_ib_fused(const FluidParams& P, IbBatch B, unsigned total_blocks, const IbSolidDev* host_solids,
+                     cudaStream_t st, bool deterministic) {
+    if (total_blocks == 0) return;
     static const int probe = [] {  // timing probe: LBMG_IB_NOSCATTER=1 skips the scatter into g
         const char* e = std::getenv("LBMG_IB_NOSCATTER");
         return e && std::atoi(e) ? 2 : 0;
     }();
-    ib_fused_kernel<<<fused_blocks(S.n), kFusedWarps * 32, 0, st>>>(P, S, table, partial, done, out_base, stride,
-                                                                     (moving ? 1 : 0) | probe, deterministic ? 1 : 0);
-    if (deterministic) launch_ib_det_reduce(P, S, st);
+    B.probe = probe;
+    ib_fused_kernel<<<total_blocks, kFusedWarps * 32, 0, st>>>(P, B, deterministic ? 1 : 0);
+    if (deterministic)
+        for (unsigned k = 0; k < B.n_solids; ++k) launch_ib_det_reduce(P, host_solids[k], st);
 }
 int totals_blocks(size_t n) {
     size_t b = (n + kTotThreads - 1) / kTotThreads;

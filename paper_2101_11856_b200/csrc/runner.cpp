@@ -296,10 +296,10 @@ void Runner::build_regions(int) {
             r.band = static_cast<unsigned*>(dalloc(sizeof(unsigned) * cap));
             r.ptr.band_count = static_cast<unsigned*>(dalloc(sizeof(unsigned)));
             r.partial = static_cast<double*>(dalloc(sizeof(double) * 6 * 256));
-            size_t nmax = 1;
-            for (const auto& so : scene_.solids) nmax = std::max(nmax, so.samples.size());
-            r.fused_partial = static_cast<double*>(dalloc(sizeof(double) * 6 * size_t(fused_blocks(nmax))));
-            r.fused_done = static_cast<unsigned*>(dalloc(sizeof(unsigned)));
+            size_t blocks = 1;
+            for (const auto& so : scene_.solids) blocks += size_t(fused_blocks(so.samples.size()));
+            r.fused_partial = static_cast<double*>(dalloc(sizeof(double) * 6 * blocks));
+            r.fused_done = static_cast<unsigned*>(dalloc(sizeof(unsigned) * scene_.solids.size()));
         }
         for (int f = 0; f < 6; ++f) {
             const int a = face_axis(f);
@@ -397,6 +397,23 @@ void Runner::upload_solids() {
                               cudaMemcpyHostToDevice));
             }
             r.solids.push_back(d);
+        }
+        // the fused IB kernel's batch: every solid in one launch
+        const size_t ns = r.solids.size();
+        if (ns) {
+            std::vector<unsigned> start(ns + 1, 0);
+            std::vector<int> mv(ns);
+            for (size_t k = 0; k < ns; ++k) {
+                start[k + 1] = start[k] + unsigned(fused_blocks(r.solids[k].n));
+                mv[k] = moving_[k] ? 1 : 0;
+            }
+            r.batch_solids = static_cast<IbSolidDev*>(dalloc(sizeof(IbSolidDev) * ns));
+            r.batch_start = static_cast<unsigned*>(dalloc(sizeof(unsigned) * (ns + 1)));
+            r.batch_moving = static_cast<int*>(dalloc(sizeof(int) * ns));
+            CK(cudaMemcpy(r.batch_solids, r.solids.data(), sizeof(IbSolidDev) * ns, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(r.batch_start, start.data(), sizeof(unsigned) * (ns + 1), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(r.batch_moving, mv.data(), sizeof(int) * ns, cudaMemcpyHostToDevice));
+            r.batch_blocks = start[ns];
         }
     }
 }
@@ -582,10 +599,18 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
         Region& r = regions_[0];
         FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
         const int ns = int(scene_.solids.size());
-        for (int s = 0; s < ns; ++s)
-            launch_ib_fused(P, r.solids[s], motion_tab_ + size_t(s) * (cap_ + 2) * kMotionRow, r.fused_partial,
-                            r.fused_done, totals_dev_ + size_t(s) * 6, ns * 6, moving_[s] != 0, st,
-                            scene_.cfg.ib_mode == LBMG_IB_DETERMINISTIC);
+        IbBatch B{};
+        B.solids = r.batch_solids;
+        B.block_start = r.batch_start;
+        B.moving = r.batch_moving;
+        B.n_solids = unsigned(ns);
+        B.table = motion_tab_;
+        B.table_stride = size_t(cap_ + 2) * kMotionRow;
+        B.partial = r.fused_partial;
+        B.done = r.fused_done;
+        B.out_base = totals_dev_;
+        B.out_stride = ns * 6;
+        launch_ib_fused(P, B, r.batch_blocks, r.solids.data(), st, scene_.cfg.ib_mode == LBMG_IB_DETERMINISTIC);
     } else if (has_solids_) {
         enqueue_ib_pre();
         enqueue_ib_mid();
