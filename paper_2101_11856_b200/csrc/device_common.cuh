@@ -7,7 +7,7 @@
 //               paper's CSoA layout (Eq. 9, layout.hpp:41-52) with group
 //               alpha = 2^la; alpha >= n_pad is plain SoA.  A/B by step parity.
 //   rho, u      fp32 rho* and u* (u as 3 SoA planes of stride ns)
-//   gib, tflag  fp32 IB force density (3 SoA planes) + one byte per 32 nodes
+//   gib, tflag  fp32 IB force density (3 SoA planes) + one epoch byte per node
 //   slot[2][6]  per-face persistent f* of the 9 populations each face
 //               reconstructs (needed for the stale outflow-edge read,
 //               SURVEY App. A.3), A/B by parity
@@ -151,7 +151,11 @@ struct RegionPtrs {
     float* rho;
     float* u;    // 3 planes of ns
     float* gib;  // 3 planes of ns, or null without solids
-    unsigned* tflag;   // per 32 nodes: step + 1 when the IB scattered into gib this step (epoch, never cleared)
+    // per node: ib_epoch(step) (1..255, never the zero of a fresh buffer) when the IB scattered into gib at that
+    // step.  Never cleared: a stale byte that happens to match only makes the
+    // fluid kernel add a gib it already zeroed (+0), so only the true band
+    // nodes of this step pay the gib loads.
+    unsigned char* tflag;
     const float* mrecv_lo;  // (rho,u) of the ghost planes, 4*plane
     const float* mrecv_hi;
     float* msend_lo;
@@ -168,6 +172,9 @@ struct DevCounters {
     unsigned tile_ctr[4];      // tile queues of the staged fluid launches of a step
     unsigned tile_done[4];     // CTAs finished per queue (the last one rewinds it)
 };
+
+// IB force-flag epoch of step t: 1..255 (a zeroed flag byte never matches)
+LBMG_HD unsigned char ib_epoch(long long t) { return (unsigned char)(1 + t % 255); }
 
 struct FluidParams {
     RegionGeo g;

@@ -136,6 +136,13 @@ __device__ __forceinline__ void gather_node(const FluidParams& P, const StepView
     }
 }
 
+// Sticky Mach warning (|u|^2 >= 0.16, collision.hpp:55): once set, further
+// nodes only read it (L2), so a flow with many fast nodes does not serialise
+// every thread on one atomic address.
+__device__ __forceinline__ void raise_mach(DevCounters* ctr) {
+    if (__ldcg(&ctr->mach) == 0u) atomicOr(&ctr->mach, 1u);
+}
+
 __device__ __forceinline__ void flag_divergence(DevCounters* ctr) {
     if (atomicExch(&ctr->diverged, 1u) == 0u) ctr->diverged_step = ctr->t;
 }
@@ -194,7 +201,7 @@ __global__ void __launch_bounds__(128) fluid_shell_kernel(const FluidParams P, u
     else shell_decode(g, s, x, y, lz);
     const unsigned k = g.node(x, y, lz);
     const int p = int(ctr->t & 1);
-    const unsigned epoch = unsigned(ctr->t) + 1u;  // IB force flags of this step
+    const unsigned char epoch = ib_epoch(ctr->t);  // IB force flags of this step
     const StepView v = make_view(P, p);
 
     float fs[27];
@@ -204,7 +211,7 @@ __global__ void __launch_bounds__(128) fluid_shell_kernel(const FluidParams P, u
         flag_divergence(ctr);
         return;
     }
-    if (mc.mach[0]) atomicOr(&ctr->mach, 1u);
+    if (mc.mach[0]) raise_mach(ctr);
     if (write_macro) {
         P.p.rho[k] = mc.rho;
         P.p.u[k] = mc.ux;
@@ -212,7 +219,7 @@ __global__ void __launch_bounds__(128) fluid_shell_kernel(const FluidParams P, u
         P.p.u[k + 2u * g.ns] = mc.uz;
     }
     float gx = P.m.body[0], gy = P.m.body[1], gz = P.m.body[2];
-    if (P.p.tflag != nullptr && P.p.tflag[k >> 5] == epoch) {
+    if (P.p.tflag != nullptr && P.p.tflag[k] == epoch) {
         float* gib = P.p.gib;
         gx = __fadd_rn(gx, gib[k]);
         gy = __fadd_rn(gy, gib[k + g.ns]);
@@ -285,7 +292,7 @@ __global__ void __launch_bounds__(kBulkThreads, FORM == 2 ? 4 : 3) fluid_bulk_ke
     const unsigned kl = (v0 || v1) ? k : g.plane + unsigned(g.nx) + 2u;
 
     const int p = int(ctr->t & 1);
-    const unsigned epoch = unsigned(ctr->t) + 1u;  // IB force flags of this step
+    const unsigned char epoch = ib_epoch(ctr->t);  // IB force flags of this step
     const float* __restrict__ fin = P.p.f[p];
     float2 fs[27];
     static_for<0, 27>([&](auto I) {
@@ -312,7 +319,7 @@ __global__ void __launch_bounds__(kBulkThreads, FORM == 2 ? 4 : 3) fluid_bulk_ke
         flag_divergence(ctr);
         return;
     }
-    if ((v0 && mc.mach[0]) || (v1 && mc.mach[1])) atomicOr(&ctr->mach, 1u);
+    if ((v0 && mc.mach[0]) || (v1 && mc.mach[1])) raise_mach(ctr);
     const bool both = v0 && v1;
     if (write_macro) {
         const float2 r = mc.rho, ux = mc.ux, uy = mc.uy, uz = mc.uz;
@@ -333,7 +340,7 @@ __global__ void __launch_bounds__(kBulkThreads, FORM == 2 ? 4 : 3) fluid_bulk_ke
     float2 gx = make_float2(P.m.body[0], P.m.body[0]);
     float2 gy = make_float2(P.m.body[1], P.m.body[1]);
     float2 gz = make_float2(P.m.body[2], P.m.body[2]);
-    if (P.p.tflag != nullptr && P.p.tflag[k >> 5] == epoch) {
+    if (P.p.tflag != nullptr && (P.p.tflag[k] == epoch || P.p.tflag[k + 1] == epoch)) {
         float* gib = P.p.gib;
         float2 a = *reinterpret_cast<const float2*>(gib + k);
         float2 b = *reinterpret_cast<const float2*>(gib + k + g.ns);
@@ -535,7 +542,7 @@ __global__ void __launch_bounds__(T, 512 / T)
     }
     const RegionGeo& g = P.g;
     const int p = int(ctr->t & 1);
-    const unsigned epoch = unsigned(ctr->t) + 1u;  // IB force flags of this step
+    const unsigned char epoch = ib_epoch(ctr->t);  // IB force flags of this step
     const float* __restrict__ fin = P.p.f[p];
     float* __restrict__ fout = P.p.f[p ^ 1];
     const unsigned tid = threadIdx.x;
@@ -622,7 +629,8 @@ __global__ void __launch_bounds__(T, 512 / T)
         // IB force flag of the pair's 32-node group, loaded early (consumed
         // after the moments, so its latency hides behind the shared-memory reads)
         const unsigned kf = valid ? (unsigned(lz) * g.ny + unsigned(y)) * g.nx + unsigned(x) : 0u;
-        const unsigned tflag_word = P.p.tflag != nullptr ? __ldcg(&P.p.tflag[kf >> 5]) : 0u;
+        const unsigned tflag2 =
+            P.p.tflag != nullptr ? __ldcg(reinterpret_cast<const unsigned short*>(P.p.tflag + kf)) : 0u;
         float2 fs[27];
         static_for<0, 27>([&](auto I) {
             constexpr int i = decltype(I)::value;
@@ -648,7 +656,7 @@ __global__ void __launch_bounds__(T, 512 / T)
         float2 gx = make_float2(P.m.body[0], P.m.body[0]);
         float2 gy = make_float2(P.m.body[1], P.m.body[1]);
         float2 gz = make_float2(P.m.body[2], P.m.body[2]);
-        if (tflag_word == epoch) {
+        if (P.p.tflag != nullptr && ((tflag2 & 0xffu) == epoch || (tflag2 >> 8) == epoch)) {
             float* gib = P.p.gib;
             gx = __fadd2_rn(gx, __ldcg(reinterpret_cast<const float2*>(gib + k)));
             gy = __fadd2_rn(gy, __ldcg(reinterpret_cast<const float2*>(gib + k + g.ns)));
@@ -673,7 +681,7 @@ __global__ void __launch_bounds__(T, 512 / T)
             flag_divergence(ctr);
             continue;
         }
-        if (mc.mach[0] || mc.mach[1]) atomicOr(&ctr->mach, 1u);
+        if (mc.mach[0] || mc.mach[1]) raise_mach(ctr);
         if (write_macro) {
             *reinterpret_cast<float2*>(P.p.rho + k) = mc.rho;
             *reinterpret_cast<float2*>(P.p.u + k) = mc.ux;

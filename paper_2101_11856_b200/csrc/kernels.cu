@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kSpreadThreads) ib_spread_kernel(const FluidPa
                             atomicAdd(&P.p.gib[key], float(w * fg[0]));
                             atomicAdd(&P.p.gib[key + g.ns], float(w * fg[1]));
                             atomicAdd(&P.p.gib[key + 2u * g.ns], float(w * fg[2]));
-                            P.p.tflag[key >> 5] = unsigned(P.ctr->t) + 1u;
+                            P.p.tflag[key] = ib_epoch(P.ctr->t);
                             continue;
                         }
                         unsigned h = (key * 2654435761u) & (kHashSlots - 1);
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(kSpreadThreads) ib_spread_kernel(const FluidPa
         atomicAdd(&P.p.gib[key], hval[0][j]);
         atomicAdd(&P.p.gib[key + g.ns], hval[1][j]);
         atomicAdd(&P.p.gib[key + 2u * g.ns], hval[2][j]);
-        P.p.tflag[key >> 5] = unsigned(P.ctr->t) + 1u;
+        P.p.tflag[key] = ib_epoch(P.ctr->t);
     }
 }
 
@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
             atomicAdd(&P.p.gib[k], float(w * fg[0]));
             atomicAdd(&P.p.gib[k + g.ns], float(w * fg[1]));
             atomicAdd(&P.p.gib[k + 2u * g.ns], float(w * fg[2]));
-            P.p.tflag[k >> 5] = unsigned(P.ctr->t) + 1u;
+            if (!(moving & 4)) P.p.tflag[k] = ib_epoch(P.ctr->t);
         }
     }
     if (det && have && !act && sub == 0) {  // inactive sample: empty records
@@ -618,7 +618,7 @@ __global__ void ib_det_segment_kernel(const FluidParams P, IbSolidDev S, unsigne
     P.p.gib[k] += float(acc[0]);
     P.p.gib[k + g.ns] += float(acc[1]);
     P.p.gib[k + 2u * g.ns] += float(acc[2]);
-    P.p.tflag[k >> 5] = unsigned(P.ctr->t) + 1u;
+    P.p.tflag[k] = ib_epoch(P.ctr->t);
 }
 
 size_t ib_det_temp_bytes(unsigned n_samples) {
@@ -657,8 +657,8 @@ void launch_ib_fused(const FluidParams& P, IbBatch B, unsigned total_blocks, con
                      cudaStream_t st, bool deterministic) {
     if (total_blocks == 0) return;
     static const int probe = [] {  // timing probe: LBMG_IB_NOSCATTER=1 skips the scatter into g
-        const char* e = std::getenv("LBMG_IB_NOSCATTER");
-        return e && std::atoi(e) ? 2 : 0;
+        const char* e = std::getenv("LBMG_IB_NOSCATTER");  // 1: no scatter, 2: scatter without force flags
+        return e ? (std::atoi(e) == 1 ? 2 : (std::atoi(e) == 2 ? 4 : 0)) : 0;
     }();
     B.probe = probe;
     ib_fused_kernel<<<total_blocks, kFusedWarps * 32, 0, st>>>(P, B, deterministic ? 1 : 0);

@@ -290,7 +290,7 @@ void Runner::build_regions(int) {
         r.ptr.u = static_cast<float*>(dalloc(sizeof(float) * 3ull * g.ns));
         if (has_solids_) {
             r.ptr.gib = static_cast<float*>(dalloc(sizeof(float) * 3ull * g.ns));
-            r.ptr.tflag = static_cast<unsigned*>(dalloc(sizeof(unsigned) * (g.ns / 32 + 1)));
+            r.ptr.tflag = static_cast<unsigned char*>(dalloc(g.ns + 64));
             r.stamp = static_cast<unsigned*>(dalloc(sizeof(unsigned) * g.ns));
             const size_t cap = std::max<size_t>(1, std::min<size_t>(g.n, 8 * total_samples_));
             r.band = static_cast<unsigned*>(dalloc(sizeof(unsigned) * cap));
