@@ -643,7 +643,33 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
         *reinterpret_cast<long long*>(pinned_up_) = t0;
         CK(cudaMemcpyAsync(&ctr_->chunk_t0, pinned_up_, sizeof(long long), cudaMemcpyHostToDevice, st));
         std::vector<std::array<cudaEvent_t, 5>> evs;
-        for (long j = 0; j < chunk; ++j) {
+        // graphs: [0] one step, [1] the last step (writes rho*/u*), [2] kMultiSteps
+        // steps (fewer graph launches and inter-graph gaps)
+        auto graph_for = [&](int which) -> cudaGraphExec_t {
+            cudaGraphExec_t& g = graph_[which];
+            if (!g) {
+                cudaGraph_t graph;
+                CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+                const int n = which == 2 ? kMultiSteps : 1;
+                for (int q = 0; q < n; ++q) enqueue_step(which == 1, nullptr);
+                CK(cudaStreamEndCapture(st, &graph));
+                size_t nn = 0;
+                CK(cudaGraphGetNodes(graph, nullptr, &nn));
+                std::vector<cudaGraphNode_t> nodes(nn);
+                CK(cudaGraphGetNodes(graph, nodes.data(), &nn));
+                long kernels = 0;
+                for (auto nd : nodes) {
+                    cudaGraphNodeType ty;
+                    CK(cudaGraphNodeGetType(nd, &ty));
+                    if (ty == cudaGraphNodeTypeKernel) ++kernels;
+                }
+                if (which != 2) kernels_per_step_ = kernels;
+                CK(cudaGraphInstantiate(&g, graph, 0));
+                CK(cudaGraphDestroy(graph));
+            }
+            return g;
+        };
+        for (long j = 0; j < chunk;) {
             const bool last = done + j == steps - 1;
             if (last && snap_pending_) CK(cudaStreamWaitEvent(st, snap_done_, 0));
             if (timings) {
@@ -651,28 +677,13 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
                 for (auto& x : e) CK(cudaEventCreate(&x));
                 enqueue_step(last, &e);
                 evs.push_back({e[0], e[1], e[2], e[3], e[4]});
+                ++j;
+            } else if (!last && j + kMultiSteps < chunk && done + j + kMultiSteps < steps) {
+                CK(cudaGraphLaunch(graph_for(2), st));
+                j += kMultiSteps;
             } else {
-                cudaGraphExec_t& g = graph_[last ? 1 : 0];
-                if (!g) {
-                    cudaGraph_t graph;
-                    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-                    enqueue_step(last, nullptr);
-                    CK(cudaStreamEndCapture(st, &graph));
-                    size_t nn = 0;
-                    CK(cudaGraphGetNodes(graph, nullptr, &nn));
-                    std::vector<cudaGraphNode_t> nodes(nn);
-                    CK(cudaGraphGetNodes(graph, nodes.data(), &nn));
-                    long kernels = 0;
-                    for (auto nd : nodes) {
-                        cudaGraphNodeType ty;
-                        CK(cudaGraphNodeGetType(nd, &ty));
-                        if (ty == cudaGraphNodeTypeKernel) ++kernels;
-                    }
-                    kernels_per_step_ = kernels;
-                    CK(cudaGraphInstantiate(&g, graph, 0));
-                    CK(cudaGraphDestroy(graph));
-                }
-                CK(cudaGraphLaunch(g, st));
+                CK(cudaGraphLaunch(graph_for(last ? 1 : 0), st));
+                ++j;
             }
         }
         // results of the chunk (counters + reaction totals), one sync

@@ -196,7 +196,8 @@ private:
     double* snap_host_ = nullptr;  // pinned
     bool snap_pending_ = false;
     long snap_step_ = 0;
-    cudaGraphExec_t graph_[2] = {nullptr, nullptr};
+    static constexpr int kMultiSteps = 8;
+    cudaGraphExec_t graph_[3] = {nullptr, nullptr, nullptr};
 
     long t_ = 0;
     Status status_;
