@@ -76,6 +76,7 @@ class ClockSampler:
         self.samples = []  # (sm_mhz, max_mhz, reason bits)
         self._stop = threading.Event()
         self._t = None
+        self._ready = threading.Event()  # set once the first sample is in
         self.source = "nvml"
 
     def _run_nvml(self, nv):
@@ -88,6 +89,7 @@ class ClockSampler:
             except Exception:
                 bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
             self.samples.append((float(sm), float(mx), int(bits)))
+            self._ready.set()
             self._stop.wait(0.002)
 
     def _run_smi(self):
@@ -99,6 +101,7 @@ class ClockSampler:
                 self.samples.append((float(out[0]), float(out[1]), int(out[2].strip(), 16)))
             except Exception:
                 pass
+            self._ready.set()
             self._stop.wait(0.05)
 
     def _run(self):
@@ -116,7 +119,10 @@ class ClockSampler:
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
-        time.sleep(0.01)  # first sample before the timed region starts
+        # NVML init can take longer than a short timed region: wait for the
+        # first sample, then drop it, so every kept sample falls inside
+        self._ready.wait(timeout=10.0)
+        self.samples.clear()
         return self
 
     def __exit__(self, *a):
