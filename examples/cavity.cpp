@@ -14,6 +14,8 @@ int main(int argc, char** argv) {
     cfg.high_order_rate = 1.5;
     cfg.policy = lbm::RatePolicy::RelaxTowardOne;
     cfg.boundary.faces[5] = {lbm::FaceCondition::VelocityInlet, {0.05, 0.0, 0.0}};
+    // smoke tracers under the lid (tracer.hpp), emitted and advected on the device
+    cfg.emitters.push_back({{8.0, 8.0, 48.0}, {56.0, 56.0, 60.0}, 10});
     const long steps = argc > 1 ? std::atol(argv[1]) : 100;
     try {
         lbm::Scene scene = lbm::build_scene(cfg);
@@ -22,7 +24,11 @@ int main(int argc, char** argv) {
         lbm::FieldStore rho = runner.gather_rho();
         double mass = 0.0;
         for (std::size_t k = 0; k < rho.n_nodes(); ++k) mass += rho.get(k, 0);
-        std::printf("steps=%ld ok=%d mass=%.10f\n", runner.step_count(), int(st.ok), mass);
+        const lbm::TracerCloud cloud = runner.tracers();
+        double smoke = 0.0;
+        for (double v : runner.tracer_density()) smoke += v;
+        std::printf("steps=%ld ok=%d mass=%.10f tracers=%zu smoke=%.6f\n", runner.step_count(), int(st.ok), mass,
+                    cloud.size(), smoke);
     } catch (const lbm::ConfigError& e) {
         std::fprintf(stderr, "config: %s\n", e.what());
         return 2;

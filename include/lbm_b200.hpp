@@ -96,6 +96,17 @@ struct SolidConfig {  // scene.hpp:35-40
     std::optional<RigidMotion> motion;
 };
 
+struct TracerEmitter {  // tracer.hpp:14-17
+    Vec3 lo, hi;
+    int rate = 0;
+};
+
+struct TracerCloud {  // tracer.hpp:19-25
+    std::vector<Vec3> positions;
+    std::vector<long> birth_step;
+    std::size_t size() const { return positions.size(); }
+};
+
 struct SceneConfig {  // scene.hpp:49-78 (hot-path fields)
     GridDims dims;
     double viscosity = 0.05;
@@ -107,6 +118,7 @@ struct SceneConfig {  // scene.hpp:49-78 (hot-path fields)
     BoundarySet boundary;
     Vec3 body_force;
     std::vector<SolidConfig> solids;
+    std::vector<TracerEmitter> emitters;
     InitKind init = InitKind::Uniform;
     double init_density = 1.0;
     Vec3 init_velocity;
@@ -240,6 +252,15 @@ inline Scene build_scene(const SceneConfig& cfg) {
     Scene s;
     s.cfg = cfg;
     detail::check(lbmg_scene_build(&c, &s.h_));
+    if (!cfg.emitters.empty()) {
+        std::vector<lbmg_emitter> em(cfg.emitters.size());
+        for (std::size_t k = 0; k < em.size(); ++k) {
+            detail::put3(em[k].lo, cfg.emitters[k].lo);
+            detail::put3(em[k].hi, cfg.emitters[k].hi);
+            em[k].rate = cfg.emitters[k].rate;
+        }
+        detail::check(lbmg_scene_set_emitters(s.h_, int(em.size()), em.data()));
+    }
     return s;
 }
 
@@ -329,6 +350,26 @@ public:
         return t;
     }
 
+    // Runner::tracers (runner.hpp:54): the live cloud after the last step.
+    TracerCloud tracers() const {
+        const std::size_t n = lbmg_runner_tracer_count(h_);
+        std::vector<double> pos(3 * n);
+        std::vector<std::int64_t> birth(n);
+        detail::check(lbmg_runner_tracers(h_, pos.data(), birth.data()));
+        TracerCloud c;
+        for (std::size_t k = 0; k < n; ++k) {
+            c.positions.push_back({pos[3 * k], pos[3 * k + 1], pos[3 * k + 2]});
+            c.birth_step.push_back(long(birth[k]));
+        }
+        return c;
+    }
+    // rasterize_density(tracers(), dims()) from the device-resident cloud.
+    std::vector<double> tracer_density() const {
+        std::vector<double> vol(dims().n_nodes());
+        detail::check(lbmg_runner_tracer_density(h_, vol.data()));
+        return vol;
+    }
+
     lbmg_runner* handle() { return h_; }
 
 private:
@@ -342,6 +383,14 @@ private:
     }
     lbmg_runner* h_ = nullptr;
 };
+
+// rasterize_density (tracer.hpp:43, tracer.cpp:67-92) on device 0.
+inline std::vector<double> rasterize_density(const TracerCloud& cloud, const GridDims& dims) {
+    std::vector<double> pos(3 * cloud.size()), vol(dims.n_nodes());
+    for (std::size_t k = 0; k < cloud.size(); ++k) detail::put3(&pos[3 * k], cloud.positions[k]);
+    detail::check(lbmg_rasterize_density(cloud.size(), pos.data(), dims.nx, dims.ny, dims.nz, 0, vol.data()));
+    return vol;
+}
 
 // dump_field (io.hpp:19-20, canonical = true): LBF1 file readable by load_field.
 inline void dump_field(const FieldStore& field, const GridDims& dims, const std::string& path) {

@@ -263,6 +263,32 @@ int lbmg_runner_sync(lbmg_runner* r, lbmg_status* status);
  * captured step CUDA graph (0 before the first graph-replayed advance). */
 long lbmg_runner_kernels_per_step(const lbmg_runner* r);
 
+/* ---- smoke tracers (tracer.hpp / tracer.cpp, runner.cpp:213-223) -------- */
+/* TracerEmitter, tracer.hpp:14-17: axis-aligned region (grid units) and
+ * particles per step. */
+typedef struct {
+    double lo[3], hi[3];
+    int rate;
+} lbmg_emitter;
+/* SceneConfig::emitters (scene.hpp:60; the "tracers" JSON key,
+ * scene.cpp:244-258): replaces the scene's emitter list.  A runner built
+ * from the scene emits and advects tracers every step on the device. */
+int lbmg_scene_set_emitters(lbmg_scene* s, int n, const lbmg_emitter* emitters);
+/* emit_tracers, tracer.cpp:28-40, host: the positions one step appends
+ * (sum of the rates, AoS n*3) from the same mt19937_64 stream. */
+int lbmg_emit_tracers(int n, const lbmg_emitter* emitters, long step, uint64_t seed, double* positions);
+/* Runner::tracers(), runner.hpp:54: the live cloud after the last step, in
+ * the reference's order (emission order, retired particles removed).
+ * positions n*3 (AoS), birth_step n; either may be NULL. */
+size_t lbmg_runner_tracer_count(const lbmg_runner* r);
+int lbmg_runner_tracers(const lbmg_runner* r, double* positions, int64_t* birth_step);
+/* rasterize_density(runner.tracers(), dims), tracer.cpp:67-92, on the device
+ * from the resident cloud: vol has nx*ny*nz doubles (node_index order). */
+int lbmg_runner_tracer_density(const lbmg_runner* r, double* vol);
+/* rasterize_density of a host cloud (positions n*3) on device `device`. */
+int lbmg_rasterize_density(size_t n, const double* positions, int nx, int ny, int nz, int device,
+                           double* vol);
+
 /* ---- kernel-level entry points (unit parity, GPU) ----------------------- */
 /* collide (collision.cpp:207-212) of n nodes on the device, fp32 arithmetic:
  * f (n*27), rho (n), u (n*3) host FP64 in, omega (n*27) host FP64 out. */

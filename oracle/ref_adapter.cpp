@@ -23,6 +23,7 @@
 #include "lbm/runner.hpp"
 #include "lbm/scene.hpp"
 #include "lbm/solver.hpp"
+#include "lbm/tracer.hpp"
 #include "lbmg.h"
 #include "oracles.hpp"
 
@@ -167,6 +168,67 @@ int ref_runner_create_with_samples(const lbmg_scene_config* c, int regions, unsi
 }
 
 void ref_runner_destroy(void* h) { delete static_cast<RefRunner*>(h); }
+
+// Scene with tracer emitters (SceneConfig::emitters) + Runner.
+int ref_runner_create_tracers(const lbmg_scene_config* c, int regions, unsigned threads, int n_emitters,
+                              const lbmg_emitter* em, void** out) {
+    return guard([&] {
+        SceneConfig cfg = to_cfg(c);
+        for (int k = 0; k < n_emitters; ++k) {
+            TracerEmitter e;
+            e.lo = v3(em[k].lo);
+            e.hi = v3(em[k].hi);
+            e.rate = em[k].rate;
+            cfg.emitters.push_back(e);
+        }
+        auto rr = new RefRunner;
+        rr->scene = build_scene(cfg);
+        rr->runner = std::make_unique<Runner>(rr->scene, regions, threads);
+        *out = rr;
+    });
+}
+
+size_t ref_runner_tracer_count(void* h) { return static_cast<RefRunner*>(h)->runner->tracers().size(); }
+
+void ref_runner_tracers(void* h, double* pos, int64_t* birth) {
+    const TracerCloud& c = static_cast<RefRunner*>(h)->runner->tracers();
+    for (std::size_t k = 0; k < c.size(); ++k) {
+        pos[3 * k] = c.positions[k].x;
+        pos[3 * k + 1] = c.positions[k].y;
+        pos[3 * k + 2] = c.positions[k].z;
+        birth[k] = c.birth_step[k];
+    }
+}
+
+// emit_tracers of one step into an empty cloud: E positions (AoS).
+size_t ref_emit_tracers(int n_emitters, const lbmg_emitter* em, long step, uint64_t seed, double* pos) {
+    std::vector<TracerEmitter> es;
+    for (int k = 0; k < n_emitters; ++k) {
+        TracerEmitter e;
+        e.lo = v3(em[k].lo);
+        e.hi = v3(em[k].hi);
+        e.rate = em[k].rate;
+        es.push_back(e);
+    }
+    TracerCloud c;
+    emit_tracers(c, es, step, seed);
+    for (std::size_t k = 0; k < c.size(); ++k) {
+        pos[3 * k] = c.positions[k].x;
+        pos[3 * k + 1] = c.positions[k].y;
+        pos[3 * k + 2] = c.positions[k].z;
+    }
+    return c.size();
+}
+
+void ref_rasterize_density(size_t n, const double* pos, int nx, int ny, int nz, double* vol) {
+    TracerCloud c;
+    for (size_t k = 0; k < n; ++k) {
+        c.positions.push_back(v3(pos + 3 * k));
+        c.birth_step.push_back(0);
+    }
+    const std::vector<double> v = rasterize_density(c, GridDims{nx, ny, nz});
+    std::copy(v.begin(), v.end(), vol);
+}
 
 int ref_runner_advance(void* h, long steps, lbmg_status* st) {
     return guard([&] {

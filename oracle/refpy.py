@@ -44,6 +44,11 @@ def ref_lib():
         "ref_runner_create_with_samples": (I, [CFG, I, C.c_uint, C.POINTER(SZ), C.POINTER(D), C.POINTER(D),
                                                C.POINTER(U32P), C.POINTER(P)]),
         "ref_runner_destroy": (None, [P]),
+        "ref_runner_create_tracers": (I, [CFG, I, C.c_uint, I, C.POINTER(_abi.EmitterC), C.POINTER(P)]),
+        "ref_runner_tracer_count": (SZ, [P]),
+        "ref_runner_tracers": (None, [P, D, C.POINTER(C.c_int64)]),
+        "ref_emit_tracers": (SZ, [I, C.POINTER(_abi.EmitterC), C.c_long, C.c_uint64, D]),
+        "ref_rasterize_density": (None, [SZ, D, I, I, I, D]),
         "ref_runner_advance": (I, [P, C.c_long, C.POINTER(_abi.StatusC)]),
         "ref_runner_advance_timed": (I, [P, C.c_long, C.POINTER(_abi.StatusC), C.POINTER(_abi.TimingRowC), SZ,
                                          C.POINTER(SZ)]),
@@ -102,6 +107,31 @@ def _check(code):
         raise RuntimeError("reference: " + ref_lib().ref_last_error().decode())
 
 
+def _emitters(emitters):
+    arr = (_abi.EmitterC * max(len(emitters), 1))()
+    for k, e in enumerate(emitters):
+        arr[k].lo[:] = [float(v) for v in e.lo]
+        arr[k].hi[:] = [float(v) for v in e.hi]
+        arr[k].rate = int(e.rate)
+    return arr
+
+
+def ref_emit_tracers(emitters, step, seed):
+    n = sum(int(e.rate) for e in emitters)
+    out = np.zeros((n, 3))
+    got = ref_lib().ref_emit_tracers(len(emitters), _emitters(emitters), step, seed, _dp(out))
+    assert got == n
+    return out
+
+
+def ref_rasterize_density(positions, dims):
+    pos = np.ascontiguousarray(positions, dtype=np.float64)
+    nx, ny, nz = dims
+    vol = np.zeros(nx * ny * nz)
+    ref_lib().ref_rasterize_density(len(pos), _dp(pos), nx, ny, nz, _dp(vol))
+    return vol
+
+
 class RefRunner:
     """lbm_ref::Runner (the unmodified reference) driven through the adapter."""
 
@@ -113,7 +143,10 @@ class RefRunner:
         h = C.c_void_p()
         m = cfg.regions if regions is None else regions
         t = (os.cpu_count() or 1) if threads is None else threads
-        if samples is None:
+        if samples is None and cfg.emitters:
+            em = _emitters(cfg.emitters)
+            _check(L.ref_runner_create_tracers(cs.ptr, m, t, len(cfg.emitters), em, C.byref(h)))
+        elif samples is None:
             _check(L.ref_runner_create(cs.ptr, m, t, C.byref(h)))
         else:
             ns = len(samples)
@@ -154,6 +187,13 @@ class RefRunner:
 
     def step_count(self):
         return int(ref_lib().ref_runner_step_count(self._h))
+
+    def tracers(self):
+        n = ref_lib().ref_runner_tracer_count(self._h)
+        pos = np.zeros((n, 3))
+        birth = np.zeros(n, dtype=np.int64)
+        ref_lib().ref_runner_tracers(self._h, _dp(pos), birth.ctypes.data_as(C.POINTER(C.c_int64)))
+        return pos, birth
 
     def set_layout(self, ell, alpha):
         _check(ref_lib().ref_runner_set_layout(self._h, ell, alpha))

@@ -7,11 +7,11 @@
     r.advance(100)                    # fused sm_100a step kernels
     rho = r.gather_rho()              # canonical AoS FP64 readback
 """
-from .scene import (ConfigError, FaceSpec, MeshConfig, RigidMotion, SceneConfig, SolidConfig,
+from .scene import (ConfigError, FaceSpec, MeshConfig, RigidMotion, SceneConfig, SolidConfig, TracerEmitter,
                     load_scene_config, parse_scene_config)
 from .runner import (CudaError, Runner, Scene, StateError, StepStatus, TimingRow, build_scene,
-                     collide_batch, device_count, dump_field, lib, model_rates, morton3, reorder_permutation,
-                     split_domain)
+                     collide_batch, device_count, dump_field, emit_tracers, lib, model_rates, morton3, rasterize_density,
+                     reorder_permutation, split_domain, TracerCloud)
 
 from . import autotune
 from .autotune import TuneOutcome, TuneSpec
@@ -21,5 +21,6 @@ __all__ = [
     "ConfigError", "FaceSpec", "MeshConfig", "RigidMotion", "SceneConfig", "SolidConfig",
     "load_scene_config", "parse_scene_config", "CudaError", "Runner", "Scene", "StateError",
     "StepStatus", "TimingRow", "build_scene", "collide_batch", "device_count", "dump_field", "lib", "model_rates",
-    "morton3", "reorder_permutation", "split_domain",
+    "morton3", "reorder_permutation", "split_domain", "TracerEmitter", "TracerCloud", "emit_tracers",
+    "rasterize_density",
 ]

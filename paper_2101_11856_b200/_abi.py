@@ -40,6 +40,10 @@ class SceneConfigC(C.Structure):
     ]
 
 
+class EmitterC(C.Structure):  # lbmg_emitter (TracerEmitter, tracer.hpp:14-17)
+    _fields_ = [("lo", C.c_double * 3), ("hi", C.c_double * 3), ("rate", C.c_int)]
+
+
 class StatusC(C.Structure):
     _fields_ = [("ok", C.c_int), ("mach_warning", C.c_int), ("step", C.c_long), ("reason", C.c_char * 120)]
 

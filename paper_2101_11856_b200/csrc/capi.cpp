@@ -419,6 +419,65 @@ int lbmg_runner_cell_flags(const lbmg_runner* r, uint8_t* out) {
     return guarded([&] { R(r).cell_flags(out); });
 }
 
+// ---- tracers -------------------------------------------------------------
+
+int lbmg_scene_set_emitters(lbmg_scene* s, int n, const lbmg_emitter* emitters) {
+    return guarded([&] {
+        if (!s) throw StateError("null scene");
+        if (n < 0 || (n > 0 && !emitters)) throw lbmg::ConfigError("tracers: bad emitter list");
+        for (int k = 0; k < n; ++k)  // scene.cpp:251-257: rate in [0, 1e6]
+            if (emitters[k].rate < 0 || emitters[k].rate > 1000000)
+                throw lbmg::ConfigError("$.tracers[" + std::to_string(k) + "].rate: out of range [0, 1000000]");
+        s->emitters.assign(emitters, emitters + n);
+    });
+}
+
+int lbmg_emit_tracers(int n, const lbmg_emitter* emitters, long step, uint64_t seed, double* positions) {
+    return guarded([&] {
+        if (n < 0 || (n > 0 && !emitters)) throw lbmg::ConfigError("tracers: bad emitter list");
+        emit_positions(std::vector<lbmg_emitter>(emitters, emitters + n), step, seed, positions);
+    });
+}
+
+size_t lbmg_runner_tracer_count(const lbmg_runner* r) {
+    try {
+        return R(r).tracer_count();
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 0;
+    }
+}
+
+int lbmg_runner_tracers(const lbmg_runner* r, double* positions, int64_t* birth_step) {
+    return guarded([&] { R(r).tracers(positions, birth_step); });
+}
+
+int lbmg_runner_tracer_density(const lbmg_runner* r, double* vol) {
+    return guarded([&] { R(r).tracer_density(vol); });
+}
+
+int lbmg_rasterize_density(size_t n, const double* positions, int nx, int ny, int nz, int device, double* vol) {
+    return guarded([&] {
+        if (nx < 2 || ny < 2 || nz < 2) throw lbmg::ConfigError("rasterize_density: every extent must be >= 2");
+        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        const size_t nn = size_t(nx) * ny * nz;
+        double *dp = nullptr, *dv = nullptr;
+        cuda_check(cudaMalloc(&dv, sizeof(double) * nn), "cudaMalloc(vol)");
+        if (n && cudaMalloc(&dp, sizeof(double) * 3 * n) != cudaSuccess) {
+            cudaFree(dv);
+            throw OomError("rasterize_density: position upload allocation failed");
+        }
+        cuda_check(cudaMemset(dv, 0, sizeof(double) * nn), "cudaMemset");
+        if (n) {
+            cuda_check(cudaMemcpy(dp, positions, sizeof(double) * 3 * n, cudaMemcpyHostToDevice), "upload");
+            launch_rasterize(dp, dp + 1, dp + 2, 3, nullptr, n, nx, ny, nz, dv, nullptr);
+        }
+        cuda_check(cudaMemcpy(vol, dv, sizeof(double) * nn, cudaMemcpyDeviceToHost), "download");
+        cudaFree(dp);
+        cudaFree(dv);
+    });
+}
+
 int lbmg_runner_halo_f(lbmg_runner* r, int parity, void** sl, void** sh, void** rl, void** rh, size_t* b) {
     return guarded([&] { R(r).halo_f(parity, sl, sh, rl, rh, b); });
 }

@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <type_traits>
 #include <string>
 
 namespace lbmg {
@@ -178,6 +179,28 @@ Runner::Runner(const lbmg_scene& scene, int regions, int device, int world, int 
     upload_solids();
     init_fields();
     if (rank_mode_ && has_solids_) fill_motion_table(0, cap_ + 1, true);
+    for (const auto& e : scene_.emitters) {
+        if (e.rate < 0) throw ConfigError("tracers: rate must be >= 0");
+        temit_ += (unsigned long long)e.rate;
+    }
+    has_tracers_ = !scene_.emitters.empty();
+    if (has_tracers_ && rank_mode_)
+        throw ConfigError("tracers: emitters need an in-process runner (rank mode samples one slab only)");
+    if (has_tracers_) {
+        treg_dev_ = static_cast<TracerRegion*>(dalloc(sizeof(TracerRegion) * regions_.size()));
+        tdev_.state = static_cast<unsigned long long*>(dalloc(2 * sizeof(unsigned long long)));
+        temit_dev_ = static_cast<double*>(dalloc(sizeof(double) * 3 * std::max<unsigned long long>(temit_, 1) * cap_, false));
+        CK(cudaMallocHost(&pinned_temit_, sizeof(double) * 3 * std::max<unsigned long long>(temit_, 1) * cap_));
+        CK(cudaMallocHost(&pinned_tstate_, 2 * sizeof(unsigned long long)));
+        tdev_.emit = temit_dev_;
+        tdev_.E = temit_;
+        tdev_.reg = treg_dev_;
+        tdev_.m = int(regions_.size());
+        tdev_.nx = nx_;
+        tdev_.ny = ny_;
+        tdev_.nz = nz_;
+        tracer_reserve(4096);
+    }
     CK(cudaStreamSynchronize(stream_));
 }
 
@@ -190,6 +213,8 @@ Runner::~Runner() {
     if (snap_done_) cudaEventDestroy(snap_done_);
     if (pinned_up_) cudaFreeHost(pinned_up_);
     if (pinned_down_) cudaFreeHost(pinned_down_);
+    if (pinned_temit_) cudaFreeHost(pinned_temit_);
+    if (pinned_tstate_) cudaFreeHost(pinned_tstate_);
     for (void* p : allocs_) cudaFree(p);
     allocs_.clear();
     if (stream_) cudaStreamDestroy(stream_);
@@ -578,6 +603,7 @@ bool Runner::fused_ib() const {
 // fluid = the fused stream/moments/collision kernel [3] step end [4].
 void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
     cudaStream_t st = stream();
+    write_macro = write_macro || has_tracers_;  // the tracers sample u* of every step
     if (ev) CK(cudaEventRecord((*ev)[0], st));
     // ghost fill || fused IB when no IB support node can touch a ghost slot
     // (a fork/join inside the captured graph); timed runs keep them serial
@@ -620,9 +646,11 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
     bool ended = false;
     for (auto& r : regions_) {
         FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
-        ended = launch_fluid(P, 0, write_macro, st, false, regions_.size() == 1);
+        ended = launch_fluid(P, 0, write_macro, st, false, regions_.size() == 1 && !has_tracers_);
     }
     if (ev) CK(cudaEventRecord((*ev)[3], st));
+    // emit + advect after collision, before the step counter moves (runner.cpp:213-223)
+    if (has_tracers_) launch_tracer_step(tdev_, ctr_, sm_count_, st);
     if (!ended) launch_step_end(ctr_, st);
     if (ev) CK(cudaEventRecord((*ev)[4], st));
 }
@@ -640,6 +668,7 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
         if (snap_pending_ && has_solids_ && !fused_ib()) CK(cudaStreamWaitEvent(st, snap_done_, 0));
         // inputs of the chunk (pinned, async, ordered before the step graphs)
         if (has_solids_) fill_motion_table(t0, chunk + 1, false);
+        if (has_tracers_) tracer_prepare_chunk(t0, chunk);
         *reinterpret_cast<long long*>(pinned_up_) = t0;
         CK(cudaMemcpyAsync(&ctr_->chunk_t0, pinned_up_, sizeof(long long), cudaMemcpyHostToDevice, st));
         std::vector<std::array<cudaEvent_t, 5>> evs;
@@ -703,6 +732,7 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
                 if (seg[0] > 0.f) timings->push_back({"boundary", step, seg[0] * 1e-3});
                 if (has_solids_) timings->push_back({"ib", step, seg[1] * 1e-3});
                 timings->push_back({"fluid", step, seg[2] * 1e-3});
+                if (has_tracers_) timings->push_back({"tracers", step, seg[3] * 1e-3});
                 timings->push_back({"total", step, (seg[0] + seg[1] + seg[2] + seg[3]) * 1e-3});
                 for (auto x : evs[j]) cudaEventDestroy(x);
             }
@@ -735,6 +765,12 @@ void Runner::finish_chunk(long t0, long) {
                     for (int a = 0; a < 6; ++a) sum[a] += tot[((size_t(j) * m + r) * ns + s) * 6 + a];
             totals_.push_back(sum);
         }
+    }
+    if (has_tracers_ && completed > 0) {
+        tn_ += temit_ * (unsigned long long)completed;
+        unsigned long long ts[2];
+        CK(cudaMemcpy(ts, tdev_.state, sizeof ts, cudaMemcpyDeviceToHost));
+        tdead_ = ts[1];
     }
     t_ = long(h.t);
     if (h.mach) status_.mach_warning = true;
@@ -1029,9 +1065,117 @@ void Runner::copy_state_from(const Runner& o) {
         }
     }
     cp(ctr_, o.ctr_, sizeof(DevCounters));
+    if (has_tracers_) {
+        tracer_reserve(o.tn_);
+        cp(tdev_.x, o.tdev_.x, sizeof(double) * o.tn_);
+        cp(tdev_.y, o.tdev_.y, sizeof(double) * o.tn_);
+        cp(tdev_.z, o.tdev_.z, sizeof(double) * o.tn_);
+        cp(tdev_.birth, o.tdev_.birth, sizeof(long long) * o.tn_);
+        cp(tdev_.state, o.tdev_.state, 2 * sizeof(unsigned long long));
+        tn_ = o.tn_;
+        tdead_ = o.tdead_;
+    }
     t_ = o.t_;
     status_ = o.status_;
     totals_ = o.totals_;
+}
+
+// ---- tracers ---------------------------------------------------------------
+
+void Runner::tracer_reserve(unsigned long long need) {
+    if (need <= tcap_) return;
+    const unsigned long long cap = std::max<unsigned long long>({need, 2 * tcap_, 4096ull});
+    auto grow = [&](auto*& p, size_t elem) {
+        using T = std::remove_reference_t<decltype(*p)>;
+        T* q = static_cast<T*>(dalloc(elem * cap, false));
+        if (p) {
+            if (tn_) CK(cudaMemcpyAsync(q, p, elem * tn_, cudaMemcpyDeviceToDevice, stream()));
+            CK(cudaStreamSynchronize(stream()));
+            dfree(p);
+        }
+        p = q;
+    };
+    grow(tdev_.x, sizeof(double));
+    grow(tdev_.y, sizeof(double));
+    grow(tdev_.z, sizeof(double));
+    grow(tdev_.birth, sizeof(long long));
+    tcap_ = cap;
+    invalidate_graphs();  // the step graphs hold the cloud pointers
+}
+
+// Inputs of a chunk: compaction once half the entries are tombstones, room
+// for the chunk's emissions, the emission batch itself (host mt19937_64, the
+// reference's stream), the region table and the entry count at chunk start.
+void Runner::tracer_prepare_chunk(long t0, long chunk) {
+    cudaStream_t st = stream();
+    if (tdead_ > 0 && 2 * tdead_ >= tn_) {
+        double* sx = static_cast<double*>(dalloc(sizeof(double) * tn_, false));
+        double* sy = static_cast<double*>(dalloc(sizeof(double) * tn_, false));
+        double* sz = static_cast<double*>(dalloc(sizeof(double) * tn_, false));
+        long long* sb = static_cast<long long*>(dalloc(sizeof(long long) * tn_, false));
+        tn_ = tracer_compact(tdev_, tn_, sx, sy, sz, sb, st);
+        dfree(sx);
+        dfree(sy);
+        dfree(sz);
+        dfree(sb);
+        tdead_ = 0;
+    }
+    tracer_reserve(tn_ + temit_ * (unsigned long long)chunk);
+    std::vector<TracerRegion> reg;
+    for (const auto& r : regions_) reg.push_back({r.ptr.u, r.z0, r.z1, r.geo.ns});
+    bool same = reg.size() == treg_host_.size();
+    for (size_t k = 0; same && k < reg.size(); ++k)
+        same = reg[k].u == treg_host_[k].u && reg[k].z0 == treg_host_[k].z0 && reg[k].ns == treg_host_[k].ns;
+    if (!same) {
+        CK(cudaMemcpy(treg_dev_, reg.data(), sizeof(TracerRegion) * reg.size(), cudaMemcpyHostToDevice));
+        treg_host_ = reg;
+    }
+    if (temit_) {
+        for (long j = 0; j < chunk; ++j)
+            emit_positions(scene_.emitters, t0 + j, scene_.cfg.seed, pinned_temit_ + 3 * temit_ * size_t(j));
+        CK(cudaMemcpyAsync(temit_dev_, pinned_temit_, sizeof(double) * 3 * temit_ * size_t(chunk),
+                           cudaMemcpyHostToDevice, st));
+    }
+    pinned_tstate_[0] = tn_;
+    pinned_tstate_[1] = tdead_;
+    CK(cudaMemcpyAsync(tdev_.state, pinned_tstate_, 2 * sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+}
+
+void Runner::tracers(double* pos, int64_t* birth) const {
+    CK(cudaStreamSynchronize(stream()));
+    if (!has_tracers_ || tn_ == 0) return;
+    std::vector<double> x(tn_), y(tn_), z(tn_);
+    std::vector<long long> b(tn_);
+    CK(cudaMemcpy(x.data(), tdev_.x, sizeof(double) * tn_, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(y.data(), tdev_.y, sizeof(double) * tn_, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(z.data(), tdev_.z, sizeof(double) * tn_, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(b.data(), tdev_.birth, sizeof(long long) * tn_, cudaMemcpyDeviceToHost));
+    size_t w = 0;
+    for (size_t p = 0; p < tn_; ++p) {
+        if (b[p] < 0) continue;  // tombstone: retired (advect_tracers removes it, order kept)
+        if (pos) {
+            pos[3 * w] = x[p];
+            pos[3 * w + 1] = y[p];
+            pos[3 * w + 2] = z[p];
+        }
+        if (birth) birth[w] = b[p];
+        ++w;
+    }
+}
+
+void Runner::tracer_density(double* vol) const {
+    const size_t n = size_t(nx_) * ny_ * nz_;
+    double* d = nullptr;
+    if (cudaMalloc(&d, sizeof(double) * n) != cudaSuccess) {
+        cudaGetLastError();
+        throw OomError("tracer density volume allocation failed");
+    }
+    cudaStream_t st = stream();
+    CK(cudaMemsetAsync(d, 0, sizeof(double) * n, st));
+    if (has_tracers_) launch_rasterize(tdev_.x, tdev_.y, tdev_.z, 1, tdev_.birth, tn_, nx_, ny_, nz_, d, st);
+    CK(cudaMemcpyAsync(vol, d, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    cudaFree(d);
 }
 
 // ---- rank mode -----------------------------------------------------------

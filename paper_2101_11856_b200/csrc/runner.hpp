@@ -12,6 +12,7 @@
 
 #include "engine.hpp"
 #include "scene.hpp"
+#include "tracers.hpp"
 
 namespace lbmg {
 
@@ -97,6 +98,10 @@ public:
     void samples(int region, int solid, double* pos, double* ub, double* force, double* sampled,
                  uint32_t* src, uint8_t* flagged) const;
     void cell_flags(uint8_t* out) const;
+    // smoke tracers (Runner::tracers, runner.hpp:54; tracers.cu)
+    size_t tracer_count() const { return size_t(tn_ - tdead_); }
+    void tracers(double* pos, int64_t* birth) const;
+    void tracer_density(double* vol) const;
     void set_stream(cudaStream_t s) { ext_stream_ = s; invalidate_graphs(); }
     cudaStream_t stream() const { return ext_stream_ ? ext_stream_ : stream_; }
 
@@ -157,6 +162,8 @@ private:
     void invalidate_graphs();
     void finish_chunk(long t0, long requested);
     void copy_state_from(const Runner& o);
+    void tracer_reserve(unsigned long long need);
+    void tracer_prepare_chunk(long t0, long chunk);
 
     lbmg_scene scene_;
     int nx_ = 0, ny_ = 0, nz_ = 0;
@@ -202,7 +209,18 @@ private:
     long t_ = 0;
     Status status_;
     std::vector<std::array<double, 6>> totals_;
-    long ext_chunk_t0_ = 0;  // rank mode: start of the externally driven chunk
+    long ext_chunk_t0_ = 0;
+
+    // tracers: cloud SoA in HBM with tombstones (tracers.cu)
+    bool has_tracers_ = false;
+    unsigned long long temit_ = 0;  // particles emitted per step
+    unsigned long long tcap_ = 0, tn_ = 0, tdead_ = 0;
+    TracerDev tdev_{};
+    TracerRegion* treg_dev_ = nullptr;
+    std::vector<TracerRegion> treg_host_;
+    double* temit_dev_ = nullptr;             // [cap][E][3]
+    double* pinned_temit_ = nullptr;          // same, host staging
+    unsigned long long* pinned_tstate_ = nullptr;  // rank mode: start of the externally driven chunk
 
 public:
     long kernels_per_step_ = 0;  // kernel nodes of the captured step graph

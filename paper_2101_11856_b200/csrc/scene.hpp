@@ -92,4 +92,5 @@ struct lbmg_scene {
     lbmg_scene_config cfg;  // solids pointer re-targeted to solid_cfgs
     std::vector<lbmg_solid_config> solid_cfgs;
     std::vector<lbmg::SolidInstance> solids;
+    std::vector<lbmg_emitter> emitters;  // SceneConfig::emitters (scene.hpp:60)
 };

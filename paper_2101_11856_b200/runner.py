@@ -95,6 +95,12 @@ def lib():
         "lbmg_runner_sync": (I, [P, C.POINTER(_abi.StatusC)]),
         "lbmg_collide_batch": (I, [C.POINTER(_abi.SceneConfigC), SZ, D, D, D, D]),
         "lbmg_runner_kernels_per_step": (C.c_long, [P]),
+        "lbmg_scene_set_emitters": (I, [P, I, C.POINTER(_abi.EmitterC)]),
+        "lbmg_emit_tracers": (I, [I, C.POINTER(_abi.EmitterC), C.c_long, C.c_uint64, D]),
+        "lbmg_runner_tracer_count": (SZ, [P]),
+        "lbmg_runner_tracers": (I, [P, D, C.POINTER(C.c_int64)]),
+        "lbmg_runner_tracer_density": (I, [P, D]),
+        "lbmg_rasterize_density": (I, [SZ, D, I, I, I, I, D]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -186,6 +192,43 @@ class TimingRow:
     seconds: float
 
 
+def _emitters_c(emitters):
+    arr = (_abi.EmitterC * max(len(emitters), 1))()
+    for k, e in enumerate(emitters):
+        arr[k].lo[:] = [float(v) for v in e.lo]
+        arr[k].hi[:] = [float(v) for v in e.hi]
+        arr[k].rate = int(e.rate)
+    return arr
+
+
+@dataclass
+class TracerCloud:
+    """tracer.hpp:19-25: live particles in emission order (retired ones removed)."""
+    positions: np.ndarray  # (n, 3) FP64
+    birth_step: np.ndarray  # (n,) int64
+
+    def size(self) -> int:
+        return len(self.birth_step)
+
+
+def emit_tracers(emitters, step: int, seed: int) -> np.ndarray:
+    """emit_tracers (tracer.cpp:28-40): the positions step `step` appends, (E, 3)."""
+    n = sum(int(e.rate) for e in emitters)
+    out = np.zeros((n, 3))
+    _check(lib().lbmg_emit_tracers(len(emitters), _emitters_c(emitters), step, seed, _dp(out)))
+    return out
+
+
+def rasterize_density(cloud, dims, device: int = 0) -> np.ndarray:
+    """rasterize_density (tracer.cpp:67-92) on the device: (nz, ny, nx) flattened
+    in node_index order, FP64."""
+    pos = np.ascontiguousarray(cloud.positions if hasattr(cloud, "positions") else cloud, dtype=np.float64)
+    nx, ny, nz = dims
+    vol = np.zeros(nx * ny * nz)
+    _check(lib().lbmg_rasterize_density(len(pos), _dp(pos), nx, ny, nz, device, _dp(vol)))
+    return vol
+
+
 class Scene:
     """build_scene (scene.cpp:341-366): sampled, ordered, motion-annotated solids."""
 
@@ -195,6 +238,9 @@ class Scene:
         h = C.c_void_p()
         _check(lib().lbmg_scene_build(cs.ptr, C.byref(h)))
         self._h = h
+        if cfg.emitters:
+            em = _emitters_c(cfg.emitters)
+            _check(lib().lbmg_scene_set_emitters(h, len(cfg.emitters), em))
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -380,6 +426,21 @@ class Runner:
         arrs["source_id"] = src
         arrs["flagged"] = fl
         return arrs
+
+    # -- tracers (runner.hpp:54, runner.cpp:213-223) -------------------------
+    def tracers(self) -> TracerCloud:
+        n = int(lib().lbmg_runner_tracer_count(self._h))
+        pos = np.zeros((n, 3))
+        birth = np.zeros(n, dtype=np.int64)
+        _check(lib().lbmg_runner_tracers(self._h, _dp(pos), birth.ctypes.data_as(C.POINTER(C.c_int64))))
+        return TracerCloud(pos, birth)
+
+    def tracer_density(self) -> np.ndarray:
+        """rasterize_density(tracers(), dims) from the device-resident cloud."""
+        nx, ny, nz = self.dims()
+        vol = np.zeros(nx * ny * nz)
+        _check(lib().lbmg_runner_tracer_density(self._h, _dp(vol)))
+        return vol
 
     def cell_flags(self) -> np.ndarray:
         out = np.zeros((self._n_local(), 27), dtype=np.uint8)

@@ -67,6 +67,14 @@ class SolidConfig:
 
 
 @dataclass
+class TracerEmitter:
+    """tracer.hpp:14-17: axis-aligned emission region (grid units), particles per step."""
+    lo: Sequence[float] = (0.0, 0.0, 0.0)
+    hi: Sequence[float] = (0.0, 0.0, 0.0)
+    rate: int = 0
+
+
+@dataclass
 class SceneConfig:
     nx: int = 0
     ny: int = 0
@@ -80,6 +88,7 @@ class SceneConfig:
     faces: List[FaceSpec] = field(default_factory=lambda: [FaceSpec() for _ in range(6)])
     body_force: Sequence[float] = (0.0, 0.0, 0.0)
     solids: List[SolidConfig] = field(default_factory=list)
+    emitters: List[TracerEmitter] = field(default_factory=list)
     init: str = "uniform"
     init_density: float = 1.0
     init_velocity: Sequence[float] = (0.0, 0.0, 0.0)
@@ -321,6 +330,14 @@ def parse_scene_config(text: str) -> SceneConfig:
                 mo.center = _vec3(mj["center"], sp + ".motion.center")
             sc.motion = mo
         cfg.solids.append(sc)
+    for idx, tj in enumerate(j.get("tracers", [])):  # scene.cpp:244-258
+        tp = f"$.tracers[{idx}]"
+        _check_keys(tj, tp, {"region", "rate"})
+        rj = tj["region"]
+        _check_keys(rj, tp + ".region", {"lo", "hi"})
+        cfg.emitters.append(TracerEmitter(lo=_vec3(rj["lo"], tp + ".region.lo"),
+                                          hi=_vec3(rj["hi"], tp + ".region.hi"),
+                                          rate=_int(tj["rate"], tp + ".rate", 0, 1000000)))
     if "initial" in j:
         ij = j["initial"]
         t = ij.get("type", "uniform")

@@ -33,7 +33,9 @@ def test_cpp_example_runs(tmp_path):
     from tests import scenes
     r = lbm.Runner(lbm.build_scene(scenes.cavity(n=64)))
     r.advance(20)
-    mass = float(out.split("mass=")[1])
+    mass = float(out.split("mass=")[1].split()[0])
+    n_tr = int(out.split("tracers=")[1].split()[0])
+    assert n_tr == 200 and abs(float(out.split("smoke=")[1]) - n_tr) < 1e-4
     assert abs(mass - r.gather_rho().sum()) < 1e-6
 
 
