@@ -449,6 +449,23 @@ __device__ __forceinline__ const float* pull_source(const FluidParams& P, int p,
     return &P.faces.inlet[0][0];  // unreachable: the owner strictly decreases along the chain
 }
 
+// A persistent face slot is only ever read by an outflow chain (pull_source /
+// reconstruct), which reaches a node by stepping one layer inward from an
+// outflow face: only slots of nodes on the second layer of some outflow face
+// can be read, so the fill stores only those (none without outflow faces).
+__device__ __forceinline__ bool slot_readable(const FluidParams& P, int x, int y, int gz) {
+    const RegionGeo& g = P.g;
+    bool r = false;
+#pragma unroll
+    for (int f = 0; f < 6; ++f) {
+        if (P.faces.cond[f] != kOutflow) continue;
+        const int a = f >> 1, c = a == 0 ? x : (a == 1 ? y : gz);
+        const int n = a == 0 ? g.nx : (a == 1 ? g.ny : g.NZ);
+        r |= c == ((f & 1) ? n - 2 : 1);
+    }
+    return r;
+}
+
 // One thread per (slab-face node, crossing direction) entry; faces 0..5 in
 // order, direction slot j (the two other velocity components, cross9 order)
 // slowest, so consecutive threads walk a face row.  Common rules inline —
@@ -497,7 +514,7 @@ __device__ __forceinline__ void ghost_fill_entry(const FluidParams& P, int p, un
         if (cond == kNoSlip) val = fin[g.gaddr(sn, 27 - i)];
         else if (cond == kInlet) val = P.faces.inlet[own][i];
         else val = *pull_source(P, p, x, y, lz, i);
-        P.p.slot[p ^ 1][own][g.slot_index(own, x, y, lz, i)] = val;
+        if (slot_readable(P, x, y, g.gz0 + lz)) P.p.slot[p ^ 1][own][g.slot_index(own, x, y, lz, i)] = val;
     }
     fin[g.gaddr((unsigned long long)((long long)sn - g.soff(i)), i)] = val;
 }
