@@ -329,11 +329,17 @@ def run_ours(args):
         rho_probe = None
         dt = time.perf_counter() - t0
         ns = len(cfg.solids)
+        moving = sum(1 for s in cfg.solids if s.motion is not None)
+        # runner.cpp advance(): the chunk start (8 B) + the motion rows of moving
+        # solids up (static ones are uploaded once); counters (64 B, a 256 B slot
+        # when solids are present) + the step's reaction totals down, one copy
         e2e = {"value": nodes_global * k_e2e / dt / 1e6, "unit": "MLUPS",
-               "h2d_bytes_per_step": 8 + 2 * ns * 18 * 8, "d2h_bytes_per_step": 64 + ns * 6 * 8,
+               "h2d_bytes_per_step": 8 + (2 * ns * 18 * 8 if moving else 0),
+               "d2h_bytes_per_step": (256 + ns * 6 * 8) if ns else 64,
                "how": "one Runner.advance(1) call per step through the C ABI, host wall clock: each call "
-                      "uploads that step's inputs (chunk start + rigid-motion rows) from pinned host memory "
-                      "and downloads its results (step counters/status + reaction totals), one stream sync",
+                      "uploads that step's inputs (chunk start, motion rows of moving solids) from pinned host "
+                      "memory and downloads its results (step counters/status + reaction totals) in one copy, "
+                      "one stream sync",
                "steps": k_e2e}
         del rho_probe, st
 

@@ -113,6 +113,7 @@ Runner::Runner(const lbmg_scene& scene, int regions, int device, int world, int 
     has_solids_ = !scene_.solids.empty();
     for (const auto& s : scene_.solids) {
         moving_.push_back(s.moving ? 1 : 0);
+        any_moving_ = any_moving_ || s.moving;
         total_samples_ += s.samples.size();
     }
     ell_ = c.block_edge;
@@ -164,16 +165,21 @@ Runner::Runner(const lbmg_scene& scene, int regions, int device, int world, int 
     }
     build_regions(device);
     link_halos();
-    ctr_ = static_cast<DevCounters*>(dalloc(sizeof(DevCounters)));
+    // counters and the chunk's reaction totals share one allocation (totals at
+    // kCtrBytes) so a chunk's results come back in one D2H copy
+    static_assert(sizeof(DevCounters) <= kCtrBytes, "DevCounters outgrew its slot");
+    const size_t tot_bytes = has_solids_ ? sizeof(double) * cap_ * regions_.size() * scene_.solids.size() * 6 : 0;
+    char* ctr_block = static_cast<char*>(dalloc(kCtrBytes + tot_bytes));
+    ctr_ = reinterpret_cast<DevCounters*>(ctr_block);
     if (has_solids_) {
         const size_t ns = scene_.solids.size();
         motion_tab_ = static_cast<double*>(dalloc(sizeof(double) * (cap_ + 2) * ns * kMotionRow));
-        totals_dev_ = static_cast<double*>(dalloc(sizeof(double) * cap_ * regions_.size() * ns * 6));
+        totals_dev_ = reinterpret_cast<double*>(ctr_block + kCtrBytes);
     }
     {
         const size_t ns = scene_.solids.size();
         CK(cudaMallocHost(&pinned_up_, sizeof(double) * (1 + (cap_ + 2) * std::max<size_t>(ns, 1) * kMotionRow)));
-        pinned_down_bytes_ = sizeof(DevCounters) + sizeof(double) * cap_ * regions_.size() * std::max<size_t>(ns, 1) * 6;
+        pinned_down_bytes_ = kCtrBytes + sizeof(double) * cap_ * regions_.size() * std::max<size_t>(ns, 1) * 6;
         CK(cudaMallocHost(&pinned_down_, pinned_down_bytes_));
     }
     upload_solids();
@@ -484,9 +490,10 @@ void Runner::fill_motion_table(long t0, long rows, bool sync) {
     double* tab = pinned_up_ + 1;
     for (size_t s = 0; s < ns; ++s)
         for (long j = 0; j < rows; ++j) motion_row(int(s), t0 + j, &tab[(s * (cap_ + 2) + j) * kMotionRow]);
-    for (size_t s = 0; s < ns; ++s)
-        CK(cudaMemcpyAsync(motion_tab_ + s * (cap_ + 2) * kMotionRow, &tab[s * (cap_ + 2) * kMotionRow],
-                           sizeof(double) * rows * kMotionRow, cudaMemcpyHostToDevice, stream()));
+    // one strided copy for every solid's rows
+    const size_t pitch = sizeof(double) * size_t(cap_ + 2) * kMotionRow;
+    CK(cudaMemcpy2DAsync(motion_tab_, pitch, tab, pitch, sizeof(double) * size_t(rows) * kMotionRow, ns,
+                         cudaMemcpyHostToDevice, stream()));
     if (sync) CK(cudaStreamSynchronize(stream()));
 }
 
@@ -667,7 +674,11 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
         // them at band nodes every step, the fluid kernel on the last step
         if (snap_pending_ && has_solids_ && !fused_ib()) CK(cudaStreamWaitEvent(st, snap_done_, 0));
         // inputs of the chunk (pinned, async, ordered before the step graphs)
-        if (has_solids_) fill_motion_table(t0, chunk + 1, false);
+        // static solids: every row is the same, the table is uploaded once
+        if (has_solids_ && (any_moving_ || !motion_static_done_)) {
+            fill_motion_table(t0, any_moving_ ? chunk + 1 : cap_ + 1, false);
+            motion_static_done_ = true;
+        }
         if (has_tracers_) tracer_prepare_chunk(t0, chunk);
         *reinterpret_cast<long long*>(pinned_up_) = t0;
         CK(cudaMemcpyAsync(&ctr_->chunk_t0, pinned_up_, sizeof(long long), cudaMemcpyHostToDevice, st));
@@ -716,11 +727,9 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
             }
         }
         // results of the chunk (counters + reaction totals), one sync
-        CK(cudaMemcpyAsync(pinned_down_, ctr_, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
-        if (has_solids_)
-            CK(cudaMemcpyAsync(pinned_down_ + sizeof(DevCounters), totals_dev_,
-                               sizeof(double) * size_t(chunk) * regions_.size() * scene_.solids.size() * 6,
-                               cudaMemcpyDeviceToHost, st));
+        const size_t tot_now = has_solids_ ? sizeof(double) * size_t(chunk) * regions_.size() * scene_.solids.size() * 6 : 0;
+        CK(cudaMemcpyAsync(pinned_down_, ctr_, (has_solids_ ? kCtrBytes : sizeof(DevCounters)) + tot_now,
+                           cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         CK(cudaGetLastError());
         downloaded_ = true;
@@ -756,7 +765,7 @@ void Runner::finish_chunk(long t0, long) {
     if (has_solids_ && completed > 0) {
         const size_t ns = scene_.solids.size(), m = regions_.size();
         std::vector<double> tot(size_t(completed) * m * ns * 6);
-        if (pre) std::memcpy(tot.data(), pinned_down_ + sizeof(DevCounters), sizeof(double) * tot.size());
+        if (pre) std::memcpy(tot.data(), pinned_down_ + kCtrBytes, sizeof(double) * tot.size());
         else CK(cudaMemcpy(tot.data(), totals_dev_, sizeof(double) * tot.size(), cudaMemcpyDeviceToHost));
         for (long j = 0; j < completed; ++j) {
             std::array<double, 6> sum{};

@@ -180,6 +180,9 @@ private:
     ModelConst model_{};
     bool has_solids_ = false;
     std::vector<char> moving_;
+    bool any_moving_ = false;
+    bool motion_static_done_ = false;  // static solids: motion table uploaded once
+    static constexpr size_t kCtrBytes = 256;  // DevCounters slot ahead of the totals
     size_t total_samples_ = 0;
 
     DevCounters* ctr_ = nullptr;

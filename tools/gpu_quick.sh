@@ -8,7 +8,7 @@ timeout 600 python bench.py --steps 200 --warmup 5 --no-cpu-baseline > $OUT/benc
 timeout 600 python bench.py --config c3 --steps 20 --warmup 3 --no-cpu-baseline > $OUT/bench_c3_$TAG.json 2> $OUT/bench_c3_$TAG.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 150 --csv \
    --log-file $OUT/launches_c2_$TAG.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-# CTA-size probe of the staged fluid kernel on C2 (LBMG_GHOST_THREADS)
-for T in 256 128; do
+# CTA-size probe of the staged fluid kernel on C2 (LBMG_GHOST_THREADS), on request
+for T in ${PROBE_T:-}; do
   LBMG_GHOST_THREADS=$T timeout 300 python bench.py --steps 200 --warmup 5 --no-cpu-baseline > $OUT/bench_c2_T${T}_$TAG.json 2>&1
 done
