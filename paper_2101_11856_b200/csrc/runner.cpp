@@ -3,6 +3,8 @@
 // counter, CUDA-graph replay, in-process or NCCL-driven halo exchange).
 #include "runner.hpp"
 
+#include <cuda.h>  // driver types only: cuStreamWriteValue64 is fetched at run time (no libcuda link)
+
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -26,6 +28,25 @@ void cuda_check(cudaError_t e, const char* what) {
 namespace {
 
 unsigned round_up(unsigned n, unsigned a) { return (n + a - 1) / a * a; }
+
+// A 64-bit value written into device memory in stream order by the stream's
+// front end (cuStreamWriteValue64): no copy-engine transfer for the 8-byte
+// chunk start of every advance() call.  Falls back to a pinned H2D copy when
+// the driver entry point or 64-bit stream memory operations are unavailable.
+using WriteValue64Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+WriteValue64Fn write_value64() {
+    static const WriteValue64Fn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return WriteValue64Fn(nullptr);
+        }
+        return reinterpret_cast<WriteValue64Fn>(p);
+    }();
+    return fn;
+}
 
 size_t next_pow2(size_t v) {
     size_t p = 1;
@@ -681,7 +702,15 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
         }
         if (has_tracers_) tracer_prepare_chunk(t0, chunk);
         *reinterpret_cast<long long*>(pinned_up_) = t0;
-        CK(cudaMemcpyAsync(&ctr_->chunk_t0, pinned_up_, sizeof(long long), cudaMemcpyHostToDevice, st));
+        bool written = false;
+        if (!no_write_value_) {
+            if (auto wv = write_value64())
+                written = wv(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(&ctr_->chunk_t0),
+                             cuuint64_t(t0), 0) == CUDA_SUCCESS;
+            if (!written) no_write_value_ = true;
+        }
+        if (!written)
+            CK(cudaMemcpyAsync(&ctr_->chunk_t0, pinned_up_, sizeof(long long), cudaMemcpyHostToDevice, st));
         std::vector<std::array<cudaEvent_t, 5>> evs;
         // graphs: [0] one step, [1] the last step (writes rho*/u*), [2] kMultiSteps
         // steps (fewer graph launches and inter-graph gaps)

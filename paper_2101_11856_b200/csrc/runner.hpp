@@ -181,6 +181,7 @@ private:
     bool has_solids_ = false;
     std::vector<char> moving_;
     bool any_moving_ = false;
+    bool no_write_value_ = false;  // stream write-value unavailable: chunk start by H2D copy
     bool motion_static_done_ = false;  // static solids: motion table uploaded once
     static constexpr size_t kCtrBytes = 256;  // DevCounters slot ahead of the totals
     size_t total_samples_ = 0;
