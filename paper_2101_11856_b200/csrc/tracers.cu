@@ -87,7 +87,7 @@ __device__ __forceinline__ void sample_u(const TracerDev& T, const Support& s, d
                 const size_t k =
                     (size_t(z - R.z0) * unsigned(T.ny) + size_t(s.b[1] + oy)) * unsigned(T.nx) + size_t(s.b[0] + ox);
                 for (int c = 0; c < 3; ++c)
-                    v[c] = __dadd_rn(v[c], __dmul_rn(w, double(__ldcg(R.u + k + size_t(c) * R.ns))));
+                    v[c] = __dadd_rn(v[c], __dmul_rn(w, double(__ldg(R.u + k + size_t(c) * R.ns))));
             }
     }
 }
