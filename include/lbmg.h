@@ -190,6 +190,11 @@ int lbmg_runner_set_layout(lbmg_runner* r, int block_edge, size_t alpha);
  * Results are identical up to fp32 atomic order in the IB scatter. */
 int lbmg_runner_set_variant(lbmg_runner* r, int fluid, int ib);
 int lbmg_runner_variant(const lbmg_runner* r, int* fluid, int* ib);
+/* CTA shape of the TMA-staged fluid kernel (tuner dimension next to the
+ * variants): 512, 256 or 128 threads per CTA (1024/512/256-slot tiles), 0 =
+ * default.  Results are bitwise identical across shapes. */
+int lbmg_runner_set_cta(lbmg_runner* r, int threads);
+int lbmg_runner_cta(const lbmg_runner* r);
 /* measure_cost (autotune.cpp:29-36): set_layout(block_edge, alpha), advance
  * warmup steps, then the mean device seconds per step of advance(n_steps)
  * (CUDA events on the runner's stream); +inf when the run diverges.  The

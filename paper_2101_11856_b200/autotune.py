@@ -17,7 +17,9 @@ B200 extensions:
     "launch split chosen from the cost model"; the reference fixes the
     two-pass split at kSplitBoundary = 14, collision.hpp:58): fluid kernel
     (TMA-staged ghost layout / register-direct compact layout) x IB pipeline
-    (fused / split), ties toward variant (0, 0);
+    (fused / split), ties toward variant (0, 0); a variant may carry a third
+    entry, the staged kernel's CTA shape (512 / 256 / 128 threads per CTA =
+    1024 / 512 / 256-slot tiles, 0 = default) — the CTA-shape dimension;
   * alphas that map to the same device layout (Runner.layout_key) are
     measured once and share the cost, so a sweep is seconds, not minutes.
 """
@@ -37,7 +39,7 @@ class TuneSpec:
     alphas: List[int] = field(default_factory=list)
     n_steps: int = 10
     warmup: int = 5
-    variants: List[Tuple[int, int]] = field(default_factory=lambda: [(0, 0)])
+    variants: List[Tuple[int, ...]] = field(default_factory=lambda: [(0, 0)])
 
     def candidate_count(self) -> int:
         return (self.ell_max - self.ell_min + 1) * len(self.alphas) * len(self.variants)
@@ -75,7 +77,7 @@ class TuneRow:
     ell: int
     alpha: int
     seconds: float
-    variant: Tuple[int, int] = (0, 0)
+    variant: Tuple[int, ...] = (0, 0)
 
 
 @dataclass
@@ -83,7 +85,7 @@ class TuneOutcome:
     ell: int = 0
     alpha: int = 0
     cost: float = math.inf
-    variant: Tuple[int, int] = (0, 0)
+    variant: Tuple[int, ...] = (0, 0)
     rows: List[TuneRow] = field(default_factory=list)
 
 
@@ -115,7 +117,8 @@ def search(base, spec: TuneSpec, dedup: bool = True) -> TuneOutcome:
     seen = {}
 
     def cost(ell, alpha, v=(0, 0)):
-        if tuple(probe.variant()) != tuple(v):
+        cur = tuple(probe.variant()) + ((probe.cta(),) if len(v) > 2 else ())
+        if cur != tuple(v):
             probe.set_variant(*v)
         key = (v, ell, probe.layout_key(alpha)) if dedup else None
         if key is not None and key in seen:

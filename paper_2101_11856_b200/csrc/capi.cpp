@@ -415,6 +415,19 @@ int lbmg_runner_samples(const lbmg_runner* r, int region, int solid, double* pos
     return guarded([&] { R(r).samples(region, solid, pos, ub, force, sampled, src, flagged); });
 }
 
+int lbmg_runner_set_cta(lbmg_runner* r, int threads) {
+    return guarded([&] { R(r).set_cta(threads); });
+}
+
+int lbmg_runner_cta(const lbmg_runner* r) {
+    try {
+        return R(r).cta();
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 int lbmg_runner_cell_flags(const lbmg_runner* r, uint8_t* out) {
     return guarded([&] { R(r).cell_flags(out); });
 }

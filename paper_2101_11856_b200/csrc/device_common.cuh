@@ -72,6 +72,7 @@ struct RegionGeo {
     int ghost;
     unsigned PX, PY, PP;  // row pitch, rows per plane, PX * PY
     unsigned base;        // leading pad (a multiple of 256 slots)
+    int cta;              // staged fluid kernel CTA size (0: LBMG_GHOST_THREADS or 512); a tuner dimension
     int zwrap;            // the slab is its own z neighbour (one periodic region)
     int has_outflow;      // some face is an outflow face (face slots are read)
     FastDiv div_px, div_py;

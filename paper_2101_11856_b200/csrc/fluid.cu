@@ -908,10 +908,11 @@ template <int KIND, int POLICY, bool STD>
 void launch_ghost_planes(const FluidParams& P, int z_a, int z_b, int slot, int write_macro, cudaStream_t st,
                          int end_step = 0) {
     if (z_b <= z_a) return;
-    static const int threads = [] {
+    static const int env_threads = [] {
         const char* e = std::getenv("LBMG_GHOST_THREADS");
         return e ? std::atoi(e) : 512;
     }();
+    const int threads = P.g.cta > 0 ? P.g.cta : env_threads;  // Runner::set_cta (tuner) wins
     const unsigned block = P.g.amask + 1u;  // Eq. 9 block (slots); SoA: 2^31
     if (threads >= 512 && block >= 1024u)
         launch_ghost_planes_t<KIND, POLICY, STD, 512>(P, z_a, z_b, slot, write_macro, st, end_step);

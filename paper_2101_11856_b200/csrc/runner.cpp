@@ -260,6 +260,7 @@ void Runner::invalidate_graphs() {
 
 void Runner::compute_geo(Region& r) const {
     RegionGeo& g = r.geo;
+    g.cta = cta_;
     g.nx = nx_;
     g.ny = ny_;
     g.nzl = r.z1 - r.z0;
@@ -1025,6 +1026,14 @@ void Runner::set_variant(int fluid, int ib) {
     invalidate_graphs();
 }
 
+void Runner::set_cta(int threads) {
+    if (threads != 0 && threads != 128 && threads != 256 && threads != 512)
+        throw ConfigError("set_cta: the staged fluid kernel runs 128, 256 or 512 threads per CTA (0 = default)");
+    cta_ = threads;
+    for (auto& r : regions_) r.geo.cta = threads;
+    invalidate_graphs();
+}
+
 unsigned long long Runner::layout_key(size_t alpha) const {
     Runner* self = const_cast<Runner*>(this);
     const size_t keep = layout_.alpha_req;
@@ -1060,6 +1069,7 @@ std::unique_ptr<Runner> Runner::clone() const {
     auto c = std::make_unique<Runner>(scene_, rank_mode_ ? 1 : m_global_, device_, rank_mode_ ? m_global_ : 0,
                                       rank_);
     c->variant_ib_ = variant_ib_;
+    if (cta_) c->set_cta(cta_);
     if (variant_fluid_ != c->variant_fluid_) c->set_variant(variant_fluid_, variant_ib_);
     if (layout_.alpha_req != c->layout_.alpha_req || ell_ != c->ell_) c->set_layout(ell_, layout_.alpha_req);
     c->copy_state_from(*this);

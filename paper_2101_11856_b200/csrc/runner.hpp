@@ -73,6 +73,11 @@ public:
     // IB kernel, 1 = mark / band / spread / totals pipeline.
     void set_variant(int fluid, int ib);
     int fluid_variant() const { return variant_fluid_; }
+    // CTA size of the staged fluid kernel (512 / 256 / 128 threads = 1024 /
+    // 512 / 256-slot tiles; 0 = LBMG_GHOST_THREADS or 512): results are
+    // identical, only the tile period changes — the tuner's CTA-shape dimension
+    void set_cta(int threads);
+    int cta() const { return cta_; }
     int ib_variant() const { return variant_ib_; }
     // Eq. 10 cost of one candidate (autotune.cpp:29-36): set_layout, warm-up,
     // mean device seconds per step over n_steps (CUDA events around advance);
@@ -176,6 +181,7 @@ private:
     Layout layout_;
     int ell_ = 1;
     int variant_fluid_ = 0, variant_ib_ = 0;
+    int cta_ = 0;
     FaceTable faces_{};
     ModelConst model_{};
     bool has_solids_ = false;

@@ -95,6 +95,8 @@ def lib():
         "lbmg_runner_sync": (I, [P, C.POINTER(_abi.StatusC)]),
         "lbmg_collide_batch": (I, [C.POINTER(_abi.SceneConfigC), SZ, D, D, D, D]),
         "lbmg_runner_kernels_per_step": (C.c_long, [P]),
+        "lbmg_runner_set_cta": (I, [P, I]),
+        "lbmg_runner_cta": (I, [P]),
         "lbmg_scene_set_emitters": (I, [P, I, C.POINTER(_abi.EmitterC)]),
         "lbmg_emit_tracers": (I, [I, C.POINTER(_abi.EmitterC), C.c_long, C.c_uint64, D]),
         "lbmg_runner_tracer_count": (SZ, [P]),
@@ -334,11 +336,20 @@ class Runner:
     def alpha(self) -> int:
         return int(lib().lbmg_runner_alpha(self._h))
 
-    def set_variant(self, fluid: int, ib: int):
+    def set_variant(self, fluid: int, ib: int, cta: Optional[int] = None):
         """Kernel variants (tuner launch-split dimension): fluid 0 = TMA-staged
         ghost-layout kernel, 1 = register-direct compact kernels; ib 0 = fused
-        single-region IB kernel, 1 = split IB pipeline."""
+        single-region IB kernel, 1 = split IB pipeline; cta = threads per CTA of
+        the staged kernel (512/256/128, 0 = default; None keeps it)."""
         _check(lib().lbmg_runner_set_variant(self._h, fluid, ib))
+        if cta is not None:
+            self.set_cta(cta)
+
+    def set_cta(self, threads: int):
+        _check(lib().lbmg_runner_set_cta(self._h, threads))
+
+    def cta(self) -> int:
+        return int(lib().lbmg_runner_cta(self._h))
 
     def variant(self):
         f, i = C.c_int(), C.c_int()

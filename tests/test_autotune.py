@@ -82,3 +82,36 @@ def test_device_search_never_alters_physics():
     autotune.apply(tuned, out)
     tuned.advance(12)
     assert np.abs(tuned.gather_f() - ref.gather_f()).max() <= 2e-5  # fp32 IB atomics order only
+
+
+def test_cta_shape_dimension_in_search():
+    """Variants may carry the staged kernel's CTA shape as a third entry."""
+    spec = autotune.TuneSpec(ell_min=1, ell_max=1, alphas=[2, 4],
+                             variants=[(0, 0, 512), (0, 0, 256), (0, 0, 128)])
+    assert spec.candidate_count() == 6
+    out = autotune.search_with_cost(spec, lambda l, a, v: {512: 3.0, 256: 2.0, 128: 2.0}[v[2]])
+    assert out.variant == (0, 0, 256) and out.alpha == 2  # ties keep the earlier candidate
+
+
+@pytest.mark.gpu
+def test_cta_shapes_are_bitwise_identical_and_searchable():
+    cfg = scenes.channel(n=32, nz=40)
+    scene = lbm.build_scene(cfg)
+    outs = []
+    for cta in (512, 256, 128):
+        r = lbm.Runner(scene)
+        r.set_cta(cta)
+        assert r.cta() == cta
+        r.advance(7)
+        outs.append(r.gather_f())
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    with pytest.raises(lbm.ConfigError):
+        lbm.Runner(scene).set_cta(96)
+    base = lbm.Runner(scene)
+    spec = autotune.TuneSpec(ell_min=1, ell_max=1, alphas=[1 << 20], n_steps=2, warmup=1,
+                             variants=[(0, 0, 512), (0, 0, 256), (0, 0, 128)])
+    out = autotune.search(base, spec)
+    assert len(out.rows) == 3 and all(math.isfinite(r.seconds) for r in out.rows)
+    tuned = lbm.Runner(scene)
+    autotune.apply(tuned, out)
+    assert tuned.cta() == out.variant[2]

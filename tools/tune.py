@@ -24,7 +24,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--ell-max", type=int, default=None)
     ap.add_argument("--alphas", default=None)
-    ap.add_argument("--variants", default="0:0,0:1,1:0,1:1")
+    ap.add_argument("--variants", default="0:0,0:1,1:0,1:1",
+                    help="fluid:ib[:cta] list; cta = staged-kernel threads per CTA (512/256/128)")
     a = ap.parse_args()
     cfg, desc = bench.CONFIGS[a.config](1)
     scene = lbm.build_scene(cfg)
