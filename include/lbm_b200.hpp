@@ -333,6 +333,9 @@ public:
         detail::check(lbmg_runner_variant(h_, &v[0], &v[1]));
         return v;
     }
+    // CTA shape of the staged fluid kernel (512 / 256 / 128 threads, 0 = default).
+    void set_cta(int threads) { detail::check(lbmg_runner_set_cta(h_, threads)); }
+    int cta() const { return lbmg_runner_cta(h_); }
     std::uint64_t layout_key(std::size_t alpha) const {
         std::uint64_t k = 0;
         detail::check(lbmg_runner_layout_key(h_, alpha, &k));
