@@ -1,16 +1,21 @@
 #!/usr/bin/env python
 """Benchmark of the B200 ACM-MRT + IB lattice-Boltzmann step.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c3|c1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2|c1|c3|c4|c5]
 
-A "step" is one full time step (IB band pre-pass + IB spread/totals + fused
-stream/face/moments/CM-MRT collision) of the workload.  N=1: configs[1] of
-BASELINE.json (flow past a sphere 256x128x128 with IB samples).  N>1 (torchrun,
-one process per GPU): the same per-GPU workload stacked along z (weak
-scaling), z-slab halos over NCCL.  Rank 0 prints one JSON line.
+A "step" is one full time step (ghost fill = the six face passes, the IB
+pass, the fused stream/moments/CM-MRT collision/forcing kernel) of the
+workload.  Default: configs[1] of BASELINE.json (flow past a sphere
+256x128x128 with 8,329 IB samples) on one GPU.  c1/c3/c4/c5 are configs[0],
+[2], [3] and [4] at their named sizes.  N>1 (torchrun, one process per GPU):
+c1/c2/c3 stack the per-GPU workload along z (weak scaling), c4/c5 split the
+named domain (strong scaling); z-slab halos over NCCL.  Rank 0 prints one
+JSON line.
 
 --impl reference times the reference's own CPU implementation (the
-unmodified reference compiled into oracle/_ref) on this box's host cores.
+unmodified reference compiled into oracle/_ref) on this box's host cores,
+with the same `config` object.
 """
 from __future__ import annotations
 
@@ -39,28 +44,79 @@ def c2_config(n_gpus: int):
     cfg.alpha = 1 << 22     # SoA on the device (set_layout is a pure permutation)
     if n_gpus > 1:          # weak scaling: one sphere per 128-plane slab
         cfg.nz = 128 * n_gpus
-        sph = cfg.solids[0]
         cfg.solids = [lbm.SolidConfig(lbm.MeshConfig(type="sphere", center=(80, 64, 64 + 128 * k), radius=16.0,
                                                      subdivisions=4), poisson_radius=0.5) for k in range(n_gpus)]
-        del sph
-    return cfg, "flow past a sphere 256x128x128 per GPU, D3Q27 ACM-MRT + IB (configs[1])"
+    return cfg, "flow past a sphere 256x128x128 per GPU, D3Q27 ACM-MRT + IB (configs[1])", "weak"
 
 
 def c3_config(n_gpus: int):
     from tests import scenes
     cfg = scenes.channel(n=512, nz=512 * n_gpus)
     cfg.alpha = 1 << 30
-    return cfg, "channel 512^3 per GPU, D3Q27 ACM-MRT, z-periodic ring (configs[2])"
+    return cfg, "channel 512^3 per GPU, D3Q27 ACM-MRT, z-periodic ring (configs[2])", "weak"
 
 
 def c1_config(n_gpus: int):
     from tests import scenes
     cfg = scenes.cavity(n=64)
     cfg.alpha = 1 << 20
-    return cfg, "lid-driven cavity 64^3 D3Q27 ACM-MRT (configs[0], L2-resident)"
+    return cfg, "lid-driven cavity 64^3 D3Q27 ACM-MRT (configs[0], L2-resident)", "weak"
 
 
-CONFIGS = {"c2": c2_config, "c3": c3_config, "c1": c1_config}
+def c4_config(n_gpus: int):
+    from tests import scenes
+    cfg = scenes.city_c4()
+    cfg.alpha = 1 << 30
+    return cfg, ("smoke through complex architecture 1200x250x840, 220 box solids, ~3.5M IB samples, "
+                 "D3Q27 ACM-MRT + IB (configs[3], whole domain split over the GPUs)"), "strong"
+
+
+def c5_config(n_gpus: int):
+    from tests import scenes
+    cfg = scenes.fan_c5()
+    cfg.alpha = 1 << 30
+    return cfg, "rotating fan 512x256x256, moving IB samples, D3Q27 ACM-MRT + IB (configs[4])", "strong"
+
+
+CONFIGS = {"c2": c2_config, "c3": c3_config, "c1": c1_config, "c4": c4_config, "c5": c5_config}
+
+
+def cpu_sample_config(cfg):
+    """The CPU leg's bounded sample of a workload: the whole grid when its FP64
+    reference state (488 B/node) fits comfortably in host memory, else a
+    z-slab of it (the solids that intersect the slab are kept)."""
+    import copy
+    n = cfg.nx * cfg.ny * cfg.nz
+    max_nodes = 40_000_000  # ~20 GB of FP64 reference state
+    if n <= max_nodes:
+        return cfg, f"the full {cfg.nx}x{cfg.ny}x{cfg.nz} grid"
+    nz = max(8, max_nodes // (cfg.nx * cfg.ny))
+    sub = copy.deepcopy(cfg)
+    sub.nz = nz
+    keep = []
+    for s in sub.solids:
+        m = s.mesh
+        zlo = m.lo[2] if m.type == "box" else (m.center[2] - m.radius if m.type == "sphere" else m.origin[2])
+        if zlo + 2 < nz:
+            if m.type == "box" and m.hi[2] > nz - 2:
+                m.hi = (m.hi[0], m.hi[1], float(nz - 2))
+            keep.append(s)
+    sub.solids = keep
+    return sub, f"a {cfg.nx}x{cfg.ny}x{nz} z-slab of the {cfg.nx}x{cfg.ny}x{cfg.nz} grid ({len(keep)} solids)"
+
+
+def config_dict(cfg, desc, world, n_samples):
+    """The `config` object, identical in both arms."""
+    nodes = cfg.nx * cfg.ny * cfg.nz
+    return {"workload": desc, "nodes": nodes, "nodes_per_gpu": nodes // world, "solid_samples": n_samples,
+            "parallelism": f"z-slab x{world}", "layout": "SoA fp32 DDF-shifted (alpha >= n)",
+            "l2": "inputs larger than L2 (f: %.2f GB/GPU vs 126 MB L2)" % (2 * 27 * 4 * nodes / world / 1e9)}
+
+
+def scene_samples(cfg):
+    import paper_2101_11856_b200 as lbm
+    scene = lbm.build_scene(cfg)
+    return scene, sum(len(scene.samples(s)["source_id"]) for s in range(len(cfg.solids)))
 
 
 class ClockSampler:
@@ -155,54 +211,72 @@ def ncu_traffic(config: str):
     return d.get(config, {}).get("fluid_dram_bytes_per_launch")
 
 
-def cpu_baseline_sample(cfg, seconds: float = 12.0):
-    """The reference (oracle/_ref) on this box's host cores: a bounded sample
-    of the same workload (whole grid, a few steps)."""
+def _time_reference(cfg, threads, warmup, runs, budget_s):
+    """the reference Runner on `threads` host threads, `warmup`
+    steps, then `runs` timed advance(k) calls (k sized to the budget); returns
+    (median MLUPS, k, per-run seconds)."""
     from oracle.refpy import RefRunner
-    threads = os.cpu_count() or 1
     r = RefRunner(cfg, threads=threads)
     t0 = time.perf_counter()
-    r.advance(1)
-    dt1 = max(time.perf_counter() - t0, 1e-3)
-    k = max(1, min(50, int(seconds / dt1)))
-    t0 = time.perf_counter()
-    r.advance(k)
-    dt = time.perf_counter() - t0
+    r.advance(max(1, warmup))
+    per = max((time.perf_counter() - t0) / max(1, warmup), 1e-4)
+    k = max(1, min(50, int(budget_s / runs / per)))
     n = cfg.nx * cfg.ny * cfg.nz
-    return {"value": n * k / dt / 1e6, "unit": "MLUPS", "cores": threads, "kind": "reference",
-            "sample": f"{k} steps of the full {cfg.nx}x{cfg.ny}x{cfg.nz} grid (FP64 reference, "
-                      f"{threads} threads, after 1 warm-up step)"}
+    secs = []
+    for _ in range(runs):
+        t0 = time.perf_counter()
+        r.advance(k)
+        secs.append(time.perf_counter() - t0)
+    return n * k / statistics.median(secs) / 1e6, k, secs
+
+
+def cpu_baseline_sample(cfg, seconds: float = 15.0):
+    """The reference (oracle/_ref) on this box's host cores: median of 5
+    advance(k) runs after 2 warm-up steps, on a bounded sample of the workload."""
+    threads = os.cpu_count() or 1
+    sub, what = cpu_sample_config(cfg)
+    v, k, secs = _time_reference(sub, threads, 2, 5, seconds)
+    return {"value": v, "unit": "MLUPS", "cores": threads, "kind": "reference",
+            "sample": f"median of 5 x advance({k}) after 2 warm-up steps on {what} "
+                      f"(unmodified FP64 reference, {threads} threads; run seconds "
+                      + ", ".join(f"{x:.2f}" for x in secs) + ")"}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg, desc = CONFIGS[args.config](1)
-    from oracle.refpy import RefRunner
+    cfg, desc, scaling = CONFIGS[args.config](args.gpus)
+    _, n_samples = scene_samples(cfg)
     threads = os.cpu_count() or 1
-    r = RefRunner(cfg, threads=threads)
-    n = cfg.nx * cfg.ny * cfg.nz
+    sub, what = cpu_sample_config(cfg)
+    from oracle.refpy import RefRunner
+    r = RefRunner(sub, threads=threads)
+    n = sub.nx * sub.ny * sub.nz
+    w = max(2, args.warmup)
     t0 = time.perf_counter()
     r.advance(1)
     per = max(time.perf_counter() - t0, 1e-3)
     budget = 150.0
-    w = max(0, min(args.warmup, int(0.2 * budget / per)))
+    w = max(1, min(w - 1, int(0.2 * budget / per)))
     k = max(1, min(args.steps, int(0.8 * budget / per)))
-    if w:
-        r.advance(w)
-    t0 = time.perf_counter()
-    r.advance(k)
-    dt = time.perf_counter() - t0
+    r.advance(w)
+    secs = []
+    for _ in range(k):  # one timed advance(1) per step: the median is robust to host noise
+        t0 = time.perf_counter()
+        r.advance(1)
+        secs.append(time.perf_counter() - t0)
+    dt = sum(secs)
     v = n * k / dt / 1e6
     line = {
         "impl": "reference", "metric": "MLUPS (lattice-node updates/s, whole job)", "value": v, "unit": "MLUPS",
         "n_gpus": args.gpus, "steps": k, "warmup": w + 1, "ms_per_step": dt / k * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": desc, "nodes": n, "solid_samples": 8329 if args.config == "c2" else 0,
-                   "sample": "per-GPU workload (one slab) on the host cores" if args.gpus > 1 else "full workload"},
+        "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(cfg, desc, args.gpus, n_samples),
         "cpu_baseline": {"value": v, "unit": "MLUPS", "cores": threads, "kind": "reference",
-                         "sample": f"{k} timed steps of {cfg.nx}x{cfg.ny}x{cfg.nz} after {w + 1} warm-up"},
+                         "sample": f"{k} timed steps (advance(1) each) on {what} after {w + 1} warm-up steps; "
+                                   f"median step {statistics.median(secs) * 1e3:.1f} ms",
+                         "median_mlups": n / statistics.median(secs) / 1e6},
         "e2e": {"value": v, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -228,9 +302,8 @@ def run_ours(args):
     if lbm.device_count() < 1:
         raise SystemExit("no CUDA device visible to the engine")
 
-    cfg, desc = CONFIGS[args.config](world)
-    scene = lbm.build_scene(cfg)
-    n_samples = sum(len(scene.samples(s)["source_id"]) for s in range(len(cfg.solids)))
+    cfg, desc, scaling = CONFIGS[args.config](world)
+    scene, n_samples = scene_samples(cfg)
     # a dedicated (capturable) stream: the engine launches on it, the CUDA
     # events and NCCL synchronise with it
     stream = torch.cuda.Stream(device)
@@ -352,12 +425,9 @@ def run_ours(args):
         line = {
             "metric": "MLUPS (lattice-node updates/s, whole job)", "value": value, "unit": "MLUPS",
             "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": desc, "nodes": nodes_global, "nodes_per_gpu": nodes_local,
-                       "solid_samples": n_samples, "parallelism": f"z-slab x{world}",
-                       "layout": "SoA fp32 DDF-shifted (alpha >= n)",
-                       "l2": "inputs larger than L2 (f: %.2f GB/GPU vs 126 MB L2)" % (2 * 27 * 4 * nodes_local / 1e9)},
+            "config": config_dict(cfg, desc, world, n_samples),
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
             "clocks": clocks.summary(), "gpu_launches": gpu_launches,
             "per_gpu_mlups": value / world,

@@ -264,6 +264,10 @@ int lbmg_runner_phase(lbmg_runner* r, int phase, int write_macro);
 /* After an externally driven run: synchronise and fold device status/totals
  * into the host-side Runner state (like the tail of lbmg_runner_advance). */
 int lbmg_runner_sync(lbmg_runner* r, lbmg_status* status);
+/* Most steps an externally driven run may enqueue between two
+ * lbmg_runner_sync calls (the device motion / reaction-totals tables hold
+ * that many rows); lbmg_runner_phase(PRE) fails with LBMG_ERR_STATE beyond it. */
+long lbmg_runner_sync_interval(const lbmg_runner* r);
 /* Diagnostics: number of engine kernels one step launches, counted from the
  * captured step CUDA graph (0 before the first graph-replayed advance). */
 long lbmg_runner_kernels_per_step(const lbmg_runner* r);

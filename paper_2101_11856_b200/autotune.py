@@ -111,16 +111,47 @@ def measure_cost(runner, ell: int, alpha: int, spec: TuneSpec) -> float:
     return runner.measure_cost(ell, alpha, spec.warmup, spec.n_steps)
 
 
+def _norm_variant(v) -> Tuple[int, int, int]:
+    """(fluid, ib[, cta]) -> (fluid, ib, cta); cta 0 = the default shape."""
+    v = tuple(int(x) for x in v)
+    return (v + (0, 0, 0)[len(v):])[:3]
+
+
+def _effective_cta(layout_key: int, cta: int) -> int:
+    """CTA size the staged fluid launcher actually runs for a layout (a tile of
+    2*cta slots must fit one Eq. 9 block; fluid.cu launch_ghost_planes)."""
+    if not (layout_key >> 40) & 1:  # compact layout: no staged kernel
+        return 0
+    la = (layout_key >> 32) & 0xFF
+    block = 1 << 62 if la == 31 else 1 << la
+    want = cta or 512
+    for t in (512, 256, 128):
+        if t <= want and block >= 2 * t:
+            return t
+    return 128
+
+
 def search(base, spec: TuneSpec, dedup: bool = True) -> TuneOutcome:
-    """autotune.cpp:62-70: sweep on a clone of `base` (never alters its physics)."""
+    """autotune.cpp:62-70: sweep on a clone of `base` (never alters its physics).
+
+    Every variant is normalised to (fluid, ib, cta) and applied in full before
+    a measurement, so a 2-entry variant never inherits the CTA shape of the
+    previous one.  A CTA shape the launcher cannot honour for a layout (its
+    tile would straddle an Eq. 9 block) is an invalid candidate (+inf), and
+    the dedup key holds the shape that actually runs."""
     probe = base.clone()
     seen = {}
 
     def cost(ell, alpha, v=(0, 0)):
-        cur = tuple(probe.variant()) + ((probe.cta(),) if len(v) > 2 else ())
-        if cur != tuple(v):
-            probe.set_variant(*v)
-        key = (v, ell, probe.layout_key(alpha)) if dedup else None
+        nv = _norm_variant(v)
+        if (tuple(probe.variant()) + (probe.cta(),)) != nv:
+            probe.set_variant(nv[0], nv[1])
+            probe.set_cta(nv[2])
+        lkey = probe.layout_key(alpha)
+        eff = _effective_cta(lkey, nv[2])
+        if nv[2] and eff and eff != nv[2]:
+            return math.inf
+        key = (nv[0], nv[1], eff, ell, lkey) if dedup else None
         if key is not None and key in seen:
             return seen[key]
         c = measure_cost(probe, ell, alpha, spec)
@@ -132,6 +163,8 @@ def search(base, spec: TuneSpec, dedup: bool = True) -> TuneOutcome:
 
 
 def apply(runner, outcome: TuneOutcome):
-    """Apply a search result to the production runner."""
-    runner.set_variant(*outcome.variant)
+    """Apply a search result to the production runner (variant, CTA shape, layout)."""
+    nv = _norm_variant(outcome.variant)
+    runner.set_variant(nv[0], nv[1])
+    runner.set_cta(nv[2])
     runner.set_layout(outcome.ell, outcome.alpha)

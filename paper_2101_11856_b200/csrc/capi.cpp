@@ -507,6 +507,10 @@ int lbmg_runner_sync(lbmg_runner* r, lbmg_status* status) {
     return guarded([&] { put_status(R(r).sync_external(), status); });
 }
 
+long lbmg_runner_sync_interval(const lbmg_runner* r) {
+    return r && r->impl ? r->impl->chunk_cap() : 0;
+}
+
 long lbmg_runner_kernels_per_step(const lbmg_runner* r) {
     return r && r->impl ? r->impl->kernels_per_step_ : 0;
 }

@@ -877,19 +877,22 @@ void launch_ghost_planes_t(const FluidParams& P, int z_a, int z_b, int slot, int
     const RegionGeo& g = P.g;
     constexpr unsigned smem = staged_smem<T>();
     const unsigned ntiles = unsigned(z_b - z_a) * g.PP / GhostTile<T>::kTile + 2;
-    static int grid_per_sm = -1, sms = 0;
+    // function attributes and occupancy are per device context: cached per device
+    constexpr int kMaxDev = 64;
+    static int grid_per_sm[kMaxDev] = {}, sms[kMaxDev] = {};
     auto kern = fluid_ghost_kernel<KIND, POLICY, STD, T>;
-    if (grid_per_sm < 0) {
+    int dev = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    if (dev >= kMaxDev) throw std::runtime_error("fluid kernel: device index beyond the per-device cache");
+    if (grid_per_sm[dev] == 0) {
         CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        int dev = 0;
-        CUDA_OK(cudaGetDevice(&dev));
-        CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        CUDA_OK(cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev));
         int nb = 0;
         CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T, smem));
-        grid_per_sm = nb > 0 ? nb : 1;
+        grid_per_sm[dev] = nb > 0 ? nb : 1;
     }
-    const unsigned grid = std::min<unsigned>(ntiles, unsigned(grid_per_sm * sms));
+    const unsigned grid = std::min<unsigned>(ntiles, unsigned(grid_per_sm[dev] * sms[dev]));
     static const int dbg = [] {
         const char* e = std::getenv("LBMG_GHOST_DBG");
         return e ? std::atoi(e) : 0;

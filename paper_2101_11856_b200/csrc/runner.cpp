@@ -684,6 +684,37 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
     if (ev) CK(cudaEventRecord((*ev)[4], st));
 }
 
+// Step graphs: [0] one step, [1] the last step of an advance (writes
+// rho*/u*), [2] kMultiSteps steps (fewer graph launches and inter-graph gaps).
+// All three are captured and instantiated together on first use.
+void Runner::ensure_graphs() {
+    cudaStream_t st = stream();
+    for (int which = 0; which < 3; ++which) {
+        cudaGraphExec_t& g = graph_[which];
+        if (g) continue;
+        cudaGraph_t graph;
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        const int n = which == 2 ? kMultiSteps : 1;
+        for (int q = 0; q < n; ++q) enqueue_step(which == 1, nullptr);
+        CK(cudaStreamEndCapture(st, &graph));
+        size_t nn = 0;
+        CK(cudaGraphGetNodes(graph, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        CK(cudaGraphGetNodes(graph, nodes.data(), &nn));
+        long kernels = 0;
+        for (auto nd : nodes) {
+            cudaGraphNodeType ty;
+            CK(cudaGraphNodeGetType(nd, &ty));
+            if (ty == cudaGraphNodeTypeKernel) ++kernels;
+        }
+        if (which == 0) kernels_per_step_ = kernels;
+        CK(cudaGraphInstantiate(&g, graph, 0));
+        CK(cudaGraphDestroy(graph));
+        // upload now: the first launch of a fresh executable graph pays it otherwise
+        CK(cudaGraphUpload(g, st));
+    }
+}
+
 Status Runner::advance(long steps, std::vector<Timing>* timings) {
     if (!status_.ok || steps <= 0) return status_;
     cudaStream_t st = stream();
@@ -694,7 +725,9 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
         const long t0 = t_;
         // an in-flight snapshot reads rho/u: the split IB pipeline rewrites
         // them at band nodes every step, the fluid kernel on the last step
-        if (snap_pending_ && has_solids_ && !fused_ib()) CK(cudaStreamWaitEvent(st, snap_done_, 0));
+        // (on every step when tracers sample u*)
+        if (snap_pending_ && (has_tracers_ || (has_solids_ && !fused_ib())))
+            CK(cudaStreamWaitEvent(st, snap_done_, 0));
         // inputs of the chunk (pinned, async, ordered before the step graphs)
         // static solids: every row is the same, the table is uploaded once
         if (has_solids_ && (any_moving_ || !motion_static_done_)) {
@@ -713,32 +746,9 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
         if (!written)
             CK(cudaMemcpyAsync(&ctr_->chunk_t0, pinned_up_, sizeof(long long), cudaMemcpyHostToDevice, st));
         std::vector<std::array<cudaEvent_t, 5>> evs;
-        // graphs: [0] one step, [1] the last step (writes rho*/u*), [2] kMultiSteps
-        // steps (fewer graph launches and inter-graph gaps)
-        auto graph_for = [&](int which) -> cudaGraphExec_t {
-            cudaGraphExec_t& g = graph_[which];
-            if (!g) {
-                cudaGraph_t graph;
-                CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-                const int n = which == 2 ? kMultiSteps : 1;
-                for (int q = 0; q < n; ++q) enqueue_step(which == 1, nullptr);
-                CK(cudaStreamEndCapture(st, &graph));
-                size_t nn = 0;
-                CK(cudaGraphGetNodes(graph, nullptr, &nn));
-                std::vector<cudaGraphNode_t> nodes(nn);
-                CK(cudaGraphGetNodes(graph, nodes.data(), &nn));
-                long kernels = 0;
-                for (auto nd : nodes) {
-                    cudaGraphNodeType ty;
-                    CK(cudaGraphNodeGetType(nd, &ty));
-                    if (ty == cudaGraphNodeTypeKernel) ++kernels;
-                }
-                if (which != 2) kernels_per_step_ = kernels;
-                CK(cudaGraphInstantiate(&g, graph, 0));
-                CK(cudaGraphDestroy(graph));
-            }
-            return g;
-        };
+        // every step graph is captured and instantiated before the first one
+        // runs, so no later advance() pays a capture inside its own time
+        if (!timings) ensure_graphs();
         for (long j = 0; j < chunk;) {
             const bool last = done + j == steps - 1;
             if (last && snap_pending_) CK(cudaStreamWaitEvent(st, snap_done_, 0));
@@ -749,10 +759,10 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
                 evs.push_back({e[0], e[1], e[2], e[3], e[4]});
                 ++j;
             } else if (!last && j + kMultiSteps < chunk && done + j + kMultiSteps < steps) {
-                CK(cudaGraphLaunch(graph_for(2), st));
+                CK(cudaGraphLaunch(graph_[2], st));
                 j += kMultiSteps;
             } else {
-                CK(cudaGraphLaunch(graph_for(last ? 1 : 0), st));
+                CK(cudaGraphLaunch(graph_[last ? 1 : 0], st));
                 ++j;
             }
         }
@@ -1124,6 +1134,9 @@ void Runner::copy_state_from(const Runner& o) {
         tdead_ = o.tdead_;
     }
     t_ = o.t_;
+    ext_chunk_t0_ = o.ext_chunk_t0_;
+    t_ext_ = o.t_ext_;
+    if (rank_mode_ && has_solids_) fill_motion_table(ext_chunk_t0_, cap_ + 1, true);
     status_ = o.status_;
     totals_ = o.totals_;
 }
@@ -1251,6 +1264,13 @@ void Runner::halo_macro(void** send_lo, void** send_hi, void** recv_lo, void** r
 void Runner::phase(int ph, int write_macro) {
     if (!rank_mode_) throw StateError("phase(): only valid for a rank-mode runner");
     CK(cudaSetDevice(device_));
+    // an in-flight snapshot reads rho/u, which the IB band pass and the fluid
+    // phases (write_macro) rewrite
+    if (snap_pending_) CK(cudaStreamWaitEvent(stream(), snap_done_, 0));
+    // the device motion / totals tables hold cap_ steps from the chunk start
+    if (ph == LBMG_PHASE_PRE && t_ext_ - ext_chunk_t0_ >= cap_)
+        throw StateError("phase(): " + std::to_string(cap_) +
+                         " steps since the last sync(); call lbmg_runner_sync at least that often");
     switch (ph) {
         case LBMG_PHASE_PRE:
             // the motion/totals tables cover cap_ steps: call sync() at least
@@ -1264,6 +1284,7 @@ void Runner::phase(int ph, int write_macro) {
         case LBMG_PHASE_FLUID_BULK: enqueue_fluid(write_macro != 0, 2); break;
         case LBMG_PHASE_END:
             launch_step_end(ctr_, stream());
+            ++t_ext_;
             break;
         default: throw StateError("unknown phase");
     }
@@ -1274,6 +1295,7 @@ Status Runner::sync_external() {
     CK(cudaStreamSynchronize(stream()));
     finish_chunk(ext_chunk_t0_, 0);
     ext_chunk_t0_ = t_;
+    t_ext_ = t_;
     if (has_solids_) {
         fill_motion_table(t_, cap_ + 1, true);
         long long t0d = t_;

@@ -115,6 +115,7 @@ public:
     void halo_macro(void** send_lo, void** send_hi, void** recv_lo, void** recv_hi, size_t* bytes);
     void phase(int ph, int write_macro);
     Status sync_external();
+    long chunk_cap() const { return cap_; }
 
 private:
     struct SolidDev {
@@ -165,6 +166,7 @@ private:
     void fill_ghosts_full();
     void enqueue_fluid(bool write_macro, int part);
     void invalidate_graphs();
+    void ensure_graphs();
     void finish_chunk(long t0, long requested);
     void copy_state_from(const Runner& o);
     void tracer_reserve(unsigned long long need);
@@ -220,6 +222,7 @@ private:
     Status status_;
     std::vector<std::array<double, 6>> totals_;
     long ext_chunk_t0_ = 0;
+    long t_ext_ = 0;  // rank mode: steps enqueued through phase(END)
 
     // tracers: cloud SoA in HBM with tombstones (tracers.cu)
     bool has_tracers_ = false;

@@ -100,12 +100,20 @@ class RankStepper:
         # step 0 reads recv[0]: move the initial boundary planes once
         exchange(dist, self.nb, rank, *self.f[self.t & 1], async_op=False)
         self.pending = []
+        # the engine's device motion / totals tables cover this many steps
+        # between two syncs (lbmg_runner_sync_interval)
+        self.sync_every = runner.sync_interval()
+        self.since_sync = 0
+        self.status = None
 
     def step(self, write_macro: bool = False):
         r = self.r
         for w in self.pending:
             w.wait()
         self.pending = []
+        if self.since_sync >= self.sync_every:
+            self.status = r.sync()
+            self.since_sync = 0
         r.phase(_abi.PHASE_PRE)
         if self.has_solids:
             exchange(self.dist, self.nb, self.rank, *self.macro, async_op=False)
@@ -116,9 +124,12 @@ class RankStepper:
         r.phase(_abi.PHASE_FLUID_BULK, write_macro)
         r.phase(_abi.PHASE_END)
         self.t += 1
+        self.since_sync += 1
 
     def finish(self):
         for w in self.pending:
             w.wait()
         self.pending = []
-        return self.r.sync()
+        self.since_sync = 0
+        self.status = self.r.sync()
+        return self.status

@@ -95,6 +95,7 @@ def lib():
         "lbmg_runner_sync": (I, [P, C.POINTER(_abi.StatusC)]),
         "lbmg_collide_batch": (I, [C.POINTER(_abi.SceneConfigC), SZ, D, D, D, D]),
         "lbmg_runner_kernels_per_step": (C.c_long, [P]),
+        "lbmg_runner_sync_interval": (C.c_long, [P]),
         "lbmg_runner_set_cta": (I, [P, I]),
         "lbmg_runner_cta": (I, [P]),
         "lbmg_scene_set_emitters": (I, [P, I, C.POINTER(_abi.EmitterC)]),
@@ -306,7 +307,7 @@ class Runner:
         if timings is None:
             _check(lib().lbmg_runner_advance(self._h, steps, C.byref(st), None, 0, None))
         else:
-            cap = max(1, steps) * 4
+            cap = max(1, steps) * 5  # boundary, ib, fluid, tracers, total
             rows = (_abi.TimingRowC * cap)()
             n = C.c_size_t()
             _check(lib().lbmg_runner_advance(self._h, steps, C.byref(st), rows, cap, C.byref(n)))
@@ -473,6 +474,10 @@ class Runner:
 
     def phase(self, ph: int, write_macro: bool = False):
         _check(lib().lbmg_runner_phase(self._h, ph, int(write_macro)))
+
+    def sync_interval(self) -> int:
+        """Most steps between two sync() calls in an externally driven run."""
+        return int(lib().lbmg_runner_sync_interval(self._h))
 
     def kernels_per_step(self) -> int:
         return int(lib().lbmg_runner_kernels_per_step(self._h))

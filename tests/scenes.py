@@ -102,3 +102,66 @@ def city(nx=64, ny=32, nz=48, n_boxes=4, seed=7, r=0.7) -> SceneConfig:
                                       poisson_radius=r))
     cfg.block_edge = 2
     return cfg
+
+
+def city_c4(n_boxes=220, seed=7, r=0.7, nx=1200, ny=250, nz=840) -> SceneConfig:
+    """configs[3] at full size: 1200x250x840 "smoke through complex
+    architecture" — a seeded city of box solids (Poisson r = 0.7), x- inlet,
+    x+ outflow, no-slip ground and walls; ~3.5 M solid samples."""
+    import numpy as np
+    cfg = acm(SceneConfig(nx=nx, ny=ny, nz=nz, viscosity=0.02))
+    cfg.faces = faces("inlet", "outflow", "no-slip", "no-slip", "no-slip", "no-slip")
+    cfg.init_velocity = (0.05, 0.0, 0.0)
+    rng = np.random.default_rng(seed)
+    cfg.solids = []
+    # non-overlapping lots (overlapping boxes double the local sample density,
+    # which the unnormalised penalty force does not survive, SURVEY §0 fact 5a)
+    lots = [(150 + 50 * i, 20 + 50 * k) for i in range((nx - 300) // 50) for k in range((nz - 40) // 50)]
+    for j in rng.permutation(len(lots))[:n_boxes]:
+        lx, lz = lots[j]
+        w, d = rng.uniform(10, 40, size=2)
+        h = rng.uniform(20, 200)
+        x0 = lx + rng.uniform(0, 45 - w)
+        z0 = lz + rng.uniform(0, 45 - d)
+        cfg.solids.append(SolidConfig(MeshConfig(type="box", lo=(x0, 1.2, z0), hi=(x0 + w, 1.2 + h, z0 + d)),
+                                      poisson_radius=r))
+    cfg.block_edge = 2
+    return cfg
+
+
+def city_twin(seed=7, r=0.7) -> SceneConfig:
+    """configs[3] 1/8-scale parity twin (SURVEY §8(d) C4 row, App. B `twins`
+    (3)): 150x64x105, 12 seeded boxes with footprints 4..12, heights 8..40 on
+    base y = 1.2, x in [30, 120], z in [8, 85]; Poisson r = 0.7."""
+    import numpy as np
+    cfg = acm(SceneConfig(nx=150, ny=64, nz=105, viscosity=0.02))
+    cfg.faces = faces("inlet", "outflow", "no-slip", "no-slip", "no-slip", "no-slip")
+    cfg.init_velocity = (0.05, 0.0, 0.0)
+    rng = np.random.default_rng(seed)
+    cfg.solids = []
+    # 12 non-overlapping lots of 22 x 19 cells inside x [30, 120], z [8, 85]
+    lots = [(30 + 22 * i, 8 + 19 * k) for i in range(4) for k in range(4)]
+    for j in rng.permutation(len(lots))[:12]:
+        lx, lz = lots[j]
+        w, d = rng.uniform(4, 12, size=2)
+        h = rng.uniform(8, 40)
+        x0 = lx + rng.uniform(0, 20 - w)
+        z0 = lz + rng.uniform(0, 17 - d)
+        cfg.solids.append(SolidConfig(MeshConfig(type="box", lo=(x0, 1.2, z0), hi=(x0 + w, 1.2 + h, z0 + d)),
+                                      poisson_radius=r))
+    cfg.block_edge = 2
+    return cfg
+
+
+def fan_c5(r=0.5) -> SceneConfig:
+    """configs[4] at full size: rotating fan (8-fin comb about x) in a closed
+    512x256x256 box, one revolution per 2000 steps (tip speed ~0.25)."""
+    import math
+    cfg = acm(SceneConfig(nx=512, ny=256, nz=256, viscosity=0.02))
+    cfg.faces = faces(*["no-slip"] * 6)
+    cfg.solids = [SolidConfig(MeshConfig(type="fin-comb", origin=(208, 88, 88), fins=8, fin_length=80,
+                                         fin_height=64, fin_spacing=10.0), poisson_radius=r,
+                              motion=RigidMotion(angular_velocity=(2 * math.pi / 2000, 0, 0),
+                                                 center=(248, 123, 120)))]
+    cfg.block_edge = 2
+    return cfg
