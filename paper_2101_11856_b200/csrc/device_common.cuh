@@ -73,6 +73,7 @@ struct RegionGeo {
     unsigned PX, PY, PP;  // row pitch, rows per plane, PX * PY
     unsigned base;        // leading pad (a multiple of 256 slots)
     int cta;              // staged fluid kernel CTA size (0: LBMG_GHOST_THREADS or 512); a tuner dimension
+    int nbuf;             // population buffers: 2 (A/B) or 3 (step pipeline, pipeline.cu)
     int zwrap;            // the slab is its own z neighbour (one periodic region)
     int has_outflow;      // some face is an outflow face (face slots are read)
     FastDiv div_px, div_py;
@@ -138,12 +139,13 @@ struct ModelConst {
     float body[3];   // body force
 };
 
-// Pointers of one region; the [2] arrays are selected by step parity p=t&1:
-// f[p] = f(t) in, f[p^1] = f(t+1) out; slot[p] = f* slots of step t-1 (read
+// Pointers of one region.  Populations: f[fcur(t)] = f(t) in, f[fnext(t)] =
+// f(t+1) out.  The [2] arrays are selected by step parity p=t&1:
+// slot[p] = f* slots of step t-1 (read
 // for stale outflow), slot[p^1] written; recv[p] = f(t) neighbour halo in;
 // send[p^1] = f(t+1) halo out.
 struct RegionPtrs {
-    float* f[2];
+    float* f[3];  // f(t) lives in f[t % nbuf] (fcur); f[2] only with nbuf == 3
     float* slot[2][6];
     const float* recv_lo[2];
     const float* recv_hi[2];
@@ -163,6 +165,13 @@ struct RegionPtrs {
     float* msend_hi;
     unsigned* band_count;  // IB band nodes this step
 };
+
+// Physical population buffer of f(t): nbuf = 2 is the A/B pair; the step
+// pipeline (pipeline.cu) runs step t+1 while step t's tail is still in
+// flight, so it rotates three buffers and f(t) stays intact until step t
+// has completed (the diverging step's f(t) is what the reference keeps).
+LBMG_HD int fcur(const RegionGeo& g, long long t) { return int(t % g.nbuf); }
+LBMG_HD int fnext(const RegionGeo& g, long long t) { return int((t + 1) % g.nbuf); }
 
 struct DevCounters {
     long long t;               // step counter

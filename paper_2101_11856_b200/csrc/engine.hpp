@@ -13,8 +13,9 @@ struct IbSolidDev {
     double* pos;      // n*3
     double* ref;      // n*3
     double* ub;       // n*3
-    double* force;    // n*3
-    double* sampled;  // n*3
+    double* force;    // kIbHalves * n*3: one part per buffered step (ib_half)
+    double* sampled;  // kIbHalves * n*3
+    int nbuf;         // parts in use: the region's population buffer count
     unsigned* source;
     unsigned char* flagged;
     // deterministic accumulation (ib_accumulation = deterministic): one
@@ -28,6 +29,18 @@ struct IbSolidDev {
     void* sort_temp = nullptr;
     size_t sort_temp_bytes = 0;
 };
+
+// Offset of step t's part of the penalty-force / sampled-velocity arrays
+// (nbuf parts, like the population buffers).  Step t writes part t % nbuf;
+// the values the reference holds after a run are those of the last step whose
+// IB phase ran, t_ - 1, so readback uses part (t_ - 1) % nbuf: a diverging
+// step's IB output (and, in the step pipeline, that of the step already
+// running ahead of it) lands in another part and is never seen (the
+// reference returns before IB, runner.cpp:154-161).
+constexpr int kIbHalves = 3;
+LBMG_HD size_t ib_half(const IbSolidDev& S, long long t) {
+    return size_t(((t % S.nbuf) + S.nbuf) % S.nbuf) * 3 * size_t(S.n);
+}
 
 // Motion table row per step: center(t)[3], R(t)[9], v[3], omega[3].
 constexpr int kMotionRow = 18;
@@ -56,7 +69,7 @@ bool ghost_layout_enabled();
 // launches step_end_kernel.
 bool launch_fluid(const FluidParams& P, int part, int write_macro, cudaStream_t st, bool fill = true,
                   bool end_step = false);
-void launch_macro(const FluidParams& P, int parity, cudaStream_t st);
+void launch_macro(const FluidParams& P, long long t, cudaStream_t st);  // rho*/u* of step t from f(t)
 void launch_ib_mark(const FluidParams& P, const IbSolidDev& S, unsigned* stamp, unsigned* band,
                     cudaStream_t st);
 void launch_ib_band(const FluidParams& P, const unsigned* band, int sm_count, cudaStream_t st);
@@ -98,7 +111,7 @@ void launch_ib_motion_once(const IbSolidDev& S, const double* row, int nx, int n
                            cudaStream_t st);
 void launch_step_end(DevCounters* ctr, cudaStream_t st);
 void launch_init(const FluidParams& P, const InitParams& ip, cudaStream_t st);
-void launch_read_f(const FluidParams& P, int parity, unsigned k0, unsigned k1, double* out,
+void launch_read_f(const FluidParams& P, int buffer, unsigned k0, unsigned k1, double* out,
                    cudaStream_t st);
 void launch_read_macro(const FluidParams& P, unsigned k0, unsigned k1, double* rho, double* u,
                        cudaStream_t st);

@@ -25,41 +25,12 @@
 #include "collision.cuh"
 #include "device_common.cuh"
 #include "engine.hpp"
+#include "fluid_dev.cuh"
 #include "tma.cuh"
 
 namespace lbmg {
 
 namespace {
-
-constexpr unsigned kFull = 0xffffffffu;
-
-// Buffers of step parity p (slot pointers stay in kernel-parameter space:
-// indexing them by a runtime face id must not spill a copy to local memory).
-struct StepView {
-    const float* fin;
-    const float* halo_lo;
-    const float* halo_hi;
-    int p;
-};
-
-__device__ __forceinline__ StepView make_view(const FluidParams& P, int p) {
-    return StepView{P.p.f[p], P.p.recv_lo[p], P.p.recv_hi[p], p};
-}
-
-// Streamed value f_i(x - c_i) for a pull that is not missing (stream,
-// solver.cpp:46-87): periodic wrap in x/y, ghost planes from the halo.
-__device__ __forceinline__ float pull_rt(const RegionGeo& g, const StepView& v, int x, int y, int lz, int i) {
-    int sx = x - cx(i), sy = y - cy(i);
-    if (sx < 0) sx += g.nx;
-    else if (sx >= g.nx) sx -= g.nx;
-    if (sy < 0) sy += g.ny;
-    else if (sy >= g.ny) sy -= g.ny;
-    const int lzs = lz - cz(i);
-    const unsigned hp = cross9(i, 2) * g.plane + unsigned(sy) * g.nx + unsigned(sx);
-    if (lzs < 0) return v.halo_lo[hp];
-    if (lzs >= g.nzl) return v.halo_hi[hp];
-    return v.fin[g.at(sx, sy, lzs, i)];
-}
 
 // f*_i at (x,y,lz) once face pass `owner` has run this step (apply_face,
 // boundary.cpp:42-118).  Outflow copies f*_i of the interior neighbour as it
@@ -136,16 +107,6 @@ __device__ __forceinline__ void gather_node(const FluidParams& P, const StepView
     }
 }
 
-// Sticky Mach warning (|u|^2 >= 0.16, collision.hpp:55): once set, further
-// nodes only read it (L2), so a flow with many fast nodes does not serialise
-// every thread on one atomic address.
-__device__ __forceinline__ void raise_mach(DevCounters* ctr) {
-    if (__ldcg(&ctr->mach) == 0u) atomicOr(&ctr->mach, 1u);
-}
-
-__device__ __forceinline__ void flag_divergence(DevCounters* ctr) {
-    if (atomicExch(&ctr->diverged, 1u) == 0u) ctr->diverged_step = ctr->t;
-}
 
 // Shell enumeration: planes lz=0 and lz=nzl-1 first (the "edge" part that
 // feeds the halos), then per interior plane the rows y=0, y=ny-1 and the
@@ -200,9 +161,10 @@ __global__ void __launch_bounds__(128) fluid_shell_kernel(const FluidParams P, u
     if (all_nodes) decode(g, s, x, y, lz);
     else shell_decode(g, s, x, y, lz);
     const unsigned k = g.node(x, y, lz);
-    const int p = int(ctr->t & 1);
-    const unsigned char epoch = ib_epoch(ctr->t);  // IB force flags of this step
-    const StepView v = make_view(P, p);
+    const long long t = ctr->t;
+    const int p = int(t & 1);
+    const unsigned char epoch = ib_epoch(t);  // IB force flags of this step
+    const StepView v = make_view(P, t);
 
     float fs[27];
     gather_node<true>(P, v, P.p.slot[p ^ 1], k, x, y, lz, fs);
@@ -231,7 +193,7 @@ __global__ void __launch_bounds__(128) fluid_shell_kernel(const FluidParams P, u
     StashFor<FORM, float> stash;
     collide_v<KIND, POLICY, STD, float>(fs, mc, gx, gy, gz, gx != 0.f || gy != 0.f || gz != 0.f, P.m, stash);
 
-    float* fout = P.p.f[p ^ 1];
+    float* fout = P.p.f[fnext(g, t)];
     static_for<0, 27>([&](auto I) {
         constexpr int i = decltype(I)::value;
         fout[g.idx(k, i)] = fs[i];
@@ -291,9 +253,9 @@ __global__ void __launch_bounds__(kBulkThreads, FORM == 2 ? 4 : 3) fluid_bulk_ke
     // lanes without a valid node load from a safe interior pair instead
     const unsigned kl = (v0 || v1) ? k : g.plane + unsigned(g.nx) + 2u;
 
-    const int p = int(ctr->t & 1);
-    const unsigned char epoch = ib_epoch(ctr->t);  // IB force flags of this step
-    const float* __restrict__ fin = P.p.f[p];
+    const long long t = ctr->t;
+    const unsigned char epoch = ib_epoch(t);  // IB force flags of this step
+    const float* __restrict__ fin = P.p.f[fcur(g, t)];
     float2 fs[27];
     static_for<0, 27>([&](auto I) {
         constexpr int i = decltype(I)::value;
@@ -358,7 +320,7 @@ __global__ void __launch_bounds__(kBulkThreads, FORM == 2 ? 4 : 3) fluid_bulk_ke
     typename std::conditional<FORM == 1, SmemStash, StashFor<FORM, float2>>::type stash;
     collide_v<KIND, POLICY, STD, float2>(fs, mc, gx, gy, gz, any_force, P.m, stash);
 
-    float* __restrict__ fout = P.p.f[p ^ 1];
+    float* __restrict__ fout = P.p.f[fnext(g, t)];
     if (both) {
         static_for<0, 27>([&](auto I) {
             constexpr int i = decltype(I)::value;
@@ -395,130 +357,6 @@ __global__ void __launch_bounds__(kBulkThreads, FORM == 2 ? 4 : 3) fluid_bulk_ke
 //                      while the CTA computes the current one (two nodes per
 //                      thread, packed FFMA2 collision, 64-bit stores).  Lanes on
 //                      ghost/pad slots compute but do not store.
-// Tile geometry per CTA size T (threads): 2T storage slots per tile.
-template <int T>
-struct GhostTile {
-    static constexpr int kThreads = T;
-    static constexpr int kTile = 2 * T;               // storage slots per tile
-    static constexpr int kWin = kTile + 4;            // staged floats per direction
-    static constexpr unsigned kStageBytes = 27u * kWin * 4u;
-};
-constexpr int kStages = 2;
-template <int T>
-constexpr unsigned staged_smem() { return kStages * GhostTile<T>::kStageBytes + 8u * kStages; }
-
-// Window offset of slot 0 of a tile for direction i: tiles start at multiples
-// of 4 and PX, PP are multiples of 4, so (tile start - off_i) = -c_x (mod 4).
-__host__ __device__ constexpr int win_shift(int i) { return (4 - cx(i)) & 3; }
-
-// Address of f*_i at (x,y,lz) for a pull that does not stream from inside
-// the slab: the wrapped / halo source, or — for a missing pull — the value
-// face pass `owner` reconstructs (same chain as reconstruct(): bounce-back
-// source, inlet constant in kernel-parameter space, stale slot of a later
-// face, or the streamed source of the outflow neighbour).  Never a ghost slot.
-__device__ __forceinline__ const float* pull_source(const FluidParams& P, int p, int x, int y, int lz, int i) {
-    const RegionGeo& g = P.g;
-    const StepView v = make_view(P, p);
-    auto pull_addr = [&](int xx, int yy, int zz) -> const float* {
-        int sx = xx - cx(i), sy = yy - cy(i);
-        if (sx < 0) sx += g.nx;
-        else if (sx >= g.nx) sx -= g.nx;
-        if (sy < 0) sy += g.ny;
-        else if (sy >= g.ny) sy -= g.ny;
-        const int lzs = zz - cz(i);
-        const unsigned hp = cross9(i, 2) * g.plane + unsigned(sy) * g.nx + unsigned(sx);
-        if (lzs < 0) return v.halo_lo + hp;
-        if (lzs >= g.nzl) return v.halo_hi + hp;
-        return v.fin + g.at(sx, sy, lzs, i);
-    };
-    int f = owner_face(g, x, y, g.gz0 + lz, i);
-    if (f == kNoOwner) return pull_addr(x, y, lz);
-    for (int guard = 0; guard < 7; ++guard) {
-        const int cond = P.faces.cond[f];
-        if (cond == kNoSlip) return v.fin + g.at(x, y, lz, opposite(i));
-        if (cond == kInlet) return &P.faces.inlet[f][i];
-        const int a = face_axis(f), s = face_side(f);
-        if (a == 0) x -= s;
-        else if (a == 1) y -= s;
-        else lz -= s;
-        const int fn = owner_face(g, x, y, g.gz0 + lz, i);
-        if (fn == kNoOwner) return pull_addr(x, y, lz);
-        if (fn > f) return P.p.slot[p][fn] + g.slot_index(fn, x, y, lz, i);
-        f = fn;
-    }
-    return &P.faces.inlet[0][0];  // unreachable: the owner strictly decreases along the chain
-}
-
-// A persistent face slot is only ever read by an outflow chain (pull_source /
-// reconstruct), which reaches a node by stepping one layer inward from an
-// outflow face: only slots of nodes on the second layer of some outflow face
-// can be read, so the fill stores only those (none without outflow faces).
-__device__ __forceinline__ bool slot_readable(const FluidParams& P, int x, int y, int gz) {
-    const RegionGeo& g = P.g;
-    bool r = false;
-#pragma unroll
-    for (int f = 0; f < 6; ++f) {
-        if (P.faces.cond[f] != kOutflow) continue;
-        const int a = f >> 1, c = a == 0 ? x : (a == 1 ? y : gz);
-        const int n = a == 0 ? g.nx : (a == 1 ? g.ny : g.NZ);
-        r |= c == ((f & 1) ? n - 2 : 1);
-    }
-    return r;
-}
-
-// One thread per (slab-face node, crossing direction) entry; faces 0..5 in
-// order, direction slot j (the two other velocity components, cross9 order)
-// slowest, so consecutive threads walk a face row.  Common rules inline —
-// bounce-back (f*_i = f_{i'}(N), boundary.cpp:98-100), inlet
-// (feq(1, u_in)_i), periodic wrap / z halo (plain pull) — the outflow chain
-// through pull_source().
-template <int F>
-__device__ __forceinline__ void ghost_fill_entry(const FluidParams& P, int p, unsigned q, unsigned j) {
-    const RegionGeo& g = P.g;
-    constexpr int A = face_axis(F), S = face_side(F);
-    int x, y, lz;
-    if constexpr (A == 0) {
-        const unsigned qq = g.div_ny.div(q);
-        y = int(q - qq * unsigned(g.ny));
-        lz = int(qq);
-        x = S < 0 ? 0 : g.nx - 1;
-    } else {
-        const unsigned qq = g.div_nx.div(q);
-        x = int(q - qq * unsigned(g.nx));
-        if constexpr (A == 1) {
-            lz = int(qq);
-            y = S < 0 ? 0 : g.ny - 1;
-        } else {
-            y = int(qq);
-            lz = S < 0 ? 0 : g.nzl - 1;
-        }
-    }
-    const int ja = int(j % 3u) - 1, jb = int(j / 3u) - 1;
-    const int c0 = A == 0 ? -S : ja, c1 = A == 0 ? ja : (A == 1 ? -S : jb), c2 = A == 2 ? -S : jb;
-    const int i = tensor_dir((c0 + 1) + 3 * (c1 + 1) + 9 * (c2 + 1));
-    const int own = owner_face(g, x, y, g.gz0 + lz, i);
-    const unsigned sn = g.sidx(x, y, lz);
-    float* fin = P.p.f[p];
-    float val;
-    if (own == kNoOwner) {  // periodic wrap in x/y, z halo
-        int sx = x - c0, sy = y - c1;
-        sx += sx < 0 ? g.nx : (sx >= g.nx ? -g.nx : 0);
-        sy += sy < 0 ? g.ny : (sy >= g.ny ? -g.ny : 0);
-        const int lzs = lz - c2;
-        const unsigned hp = cross9(i, 2) * g.plane + unsigned(sy) * g.nx + unsigned(sx);
-        if (lzs < 0) val = P.p.recv_lo[p][hp];
-        else if (lzs >= g.nzl) val = P.p.recv_hi[p][hp];
-        else val = fin[g.gaddr(g.sidx(sx, sy, lzs), i)];
-    } else {
-        const int cond = P.faces.cond[own];
-        if (cond == kNoSlip) val = fin[g.gaddr(sn, 27 - i)];
-        else if (cond == kInlet) val = P.faces.inlet[own][i];
-        else val = *pull_source(P, p, x, y, lz, i);
-        if (slot_readable(P, x, y, g.gz0 + lz)) P.p.slot[p ^ 1][own][g.slot_index(own, x, y, lz, i)] = val;
-    }
-    fin[g.gaddr((unsigned long long)((long long)sn - g.soff(i)), i)] = val;
-}
-
 // grid: x over a face's nodes, y = face * 9 + direction slot (block-uniform)
 __global__ void __launch_bounds__(256) ghost_fill_kernel(const __grid_constant__ FluidParams P) {
     DevCounters* ctr = P.ctr;
@@ -529,14 +367,14 @@ __global__ void __launch_bounds__(256) ghost_fill_kernel(const __grid_constant__
     const unsigned F = f < 2 ? unsigned(g.ny) * g.nzl : (f < 4 ? unsigned(g.nx) * g.nzl : g.plane);
     const unsigned q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= F) return;
-    const int p = int(ctr->t & 1);
+    const long long t = ctr->t;
     switch (f) {
-        case 0: ghost_fill_entry<0>(P, p, q, j); break;
-        case 1: ghost_fill_entry<1>(P, p, q, j); break;
-        case 2: ghost_fill_entry<2>(P, p, q, j); break;
-        case 3: ghost_fill_entry<3>(P, p, q, j); break;
-        case 4: ghost_fill_entry<4>(P, p, q, j); break;
-        default: ghost_fill_entry<5>(P, p, q, j); break;
+        case 0: ghost_fill_entry<0>(P, t, q, j); break;
+        case 1: ghost_fill_entry<1>(P, t, q, j); break;
+        case 2: ghost_fill_entry<2>(P, t, q, j); break;
+        case 3: ghost_fill_entry<3>(P, t, q, j); break;
+        case 4: ghost_fill_entry<4>(P, t, q, j); break;
+        default: ghost_fill_entry<5>(P, t, q, j); break;
     }
 }
 
@@ -558,10 +396,11 @@ __global__ void __launch_bounds__(T, 512 / T)
         return;
     }
     const RegionGeo& g = P.g;
-    const int p = int(ctr->t & 1);
-    const unsigned char epoch = ib_epoch(ctr->t);  // IB force flags of this step
-    const float* __restrict__ fin = P.p.f[p];
-    float* __restrict__ fout = P.p.f[p ^ 1];
+    const long long t = ctr->t;
+    const int p = int(t & 1);
+    const unsigned char epoch = ib_epoch(t);  // IB force flags of this step
+    const float* __restrict__ fin = P.p.f[fcur(g, t)];
+    float* __restrict__ fout = P.p.f[fnext(g, t)];
     const unsigned tid = threadIdx.x;
     // slots of planes [z_a, z_b); tiles are kTile-aligned (CSoA blocks are
     // multiples of kTile), lanes outside [sb, se) do not store
@@ -746,11 +585,11 @@ __global__ void __launch_bounds__(T, 512 / T)
 
 // Recompute rho*/u* of the current step from f(t) (after divergence, so the
 // readback matches the reference's partially written moments, solver.cpp:113).
-__global__ void macro_kernel(const FluidParams P, int parity) {
+__global__ void macro_kernel(const FluidParams P, long long t) {
     const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
     const RegionGeo& g = P.g;
     if (k >= g.n) return;
-    const StepView v = make_view(P, parity);
+    const StepView v = make_view(P, t);
     int x, y, lz;
     decode(g, k, x, y, lz);
     float fs[27];
@@ -770,8 +609,7 @@ __global__ void ib_band_kernel(const FluidParams P, const unsigned* band) {
     if (ctr->diverged) return;
     const unsigned count = *P.p.band_count;
     const RegionGeo& g = P.g;
-    const int p = int(ctr->t & 1);
-    const StepView v = make_view(P, p);
+    const StepView v = make_view(P, ctr->t);
     for (unsigned j = blockIdx.x * blockDim.x + threadIdx.x; j < count; j += gridDim.x * blockDim.x) {
         const unsigned k = band[j];
         int x, y, lz;
@@ -1008,8 +846,8 @@ bool launch_fluid(const FluidParams& P, int part, int write_macro, cudaStream_t 
     return t_end;
 }
 
-void launch_macro(const FluidParams& P, int parity, cudaStream_t st) {
-    macro_kernel<<<blocks_for(P.g.n, 256), 256, 0, st>>>(P, parity);
+void launch_macro(const FluidParams& P, long long t, cudaStream_t st) {
+    macro_kernel<<<blocks_for(P.g.n, 256), 256, 0, st>>>(P, t);
 }
 
 void launch_ib_band(const FluidParams& P, const unsigned* band, int sm_count, cudaStream_t st) {

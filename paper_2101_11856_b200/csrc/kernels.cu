@@ -24,46 +24,13 @@
 
 #include "device_common.cuh"
 #include "engine.hpp"
+#include "ib_dev.cuh"
 
 namespace lbmg {
 
 // ---------------------------------------------------------------------------
 // Immersed boundary (ib.cpp:294-501).
 
-namespace {
-
-struct Support {
-    int base[3];
-    double w[3][2];
-    bool inside;
-};
-
-// kernel_support (ib.cpp:294-308), FP64, bit-exact flags.
-__device__ __forceinline__ Support kernel_support(const double p[3], int nx, int ny, int nz) {
-    Support ks;
-    ks.inside = true;
-    const int n[3] = {nx, ny, nz};
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        if (p[a] < 0.0 || p[a] > double(n[a] - 1)) ks.inside = false;
-        int b = int(floor(p[a]));
-        b = max(0, min(b, n[a] - 2));
-        ks.base[a] = b;
-        const double t = __dsub_rn(p[a], double(b));
-        ks.w[a][0] = __dsub_rn(1.0, t);
-        ks.w[a][1] = t;
-    }
-    return ks;
-}
-
-// sample_active (ib.cpp:313-317)
-__device__ __forceinline__ bool sample_active(double pz, int NZ, int z0, int z1) {
-    int bz = int(floor(pz));
-    bz = max(0, min(bz, NZ - 2));
-    return bz + 1 >= z0 && bz < z1;
-}
-
-}  // namespace
 
 __global__ void ib_mark_kernel(const FluidParams P, IbSolidDev S, unsigned* stamp, unsigned* band) {
     DevCounters* ctr = P.ctr;
@@ -161,9 +128,12 @@ __global__ void __launch_bounds__(kSpreadThreads) ib_spread_kernel(const FluidPa
                     }
             for (int a = 0; a < 3; ++a) fg[a] = rs * (S.ub[3 * s + a] - us[a]);
         }
+        // this step's half of the A/B sample outputs (the diverging step's IB
+        // results are never read back: runner.cpp:154-161 skips IB there)
+        const size_t po = ib_half(S, ctr->t);
         for (int a = 0; a < 3; ++a) {
-            S.sampled[3 * s + a] = us[a];
-            S.force[3 * s + a] = fg[a];
+            S.sampled[po + 3 * s + a] = us[a];
+            S.force[po + 3 * s + a] = fg[a];
         }
         if constexpr (DET) {  // one (owned node | ~0u, w g_s) record per corner, sample-major
             for (int c = 0; c < 8; ++c) {
@@ -226,12 +196,13 @@ __global__ void __launch_bounds__(kTotThreads) ib_totals_partial_kernel(const Fl
     __shared__ double sh[6][kTotThreads];
     const double* motion_row = table + (P.ctr->t - P.ctr->chunk_t0) * kMotionRow;
     const double c[3] = {motion_row[0], motion_row[1], motion_row[2]};
+    const double* force = S.force + ib_half(S, P.ctr->t);
     double acc[6] = {0, 0, 0, 0, 0, 0};
     const double z0 = P.g.gz0, z1 = P.g.gz0 + P.g.nzl;
     for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s < S.n; s += gridDim.x * blockDim.x) {
         const double pz = S.pos[3 * s + 2];
         if (pz < z0 || pz >= z1) continue;
-        const double F[3] = {S.force[3 * s], S.force[3 * s + 1], S.force[3 * s + 2]};
+        const double F[3] = {force[3 * s], force[3 * s + 1], force[3 * s + 2]};
         const double r[3] = {S.pos[3 * s] - c[0], S.pos[3 * s + 1] - c[1], pz - c[2]};
         acc[0] -= F[0];
         acc[1] -= F[1];
@@ -260,31 +231,6 @@ __global__ void ib_totals_final_kernel(const DevCounters* ctr, const double* par
     out_base[(ctr->t - ctr->chunk_t0) * stride + a] = acc;
 }
 
-__device__ void motion_apply(const double* row, IbSolidDev S, unsigned s, int nx, int ny, int nz) {
-    const double* c = row;
-    const double* R = row + 3;
-    const double* v = row + 12;
-    const double* w = row + 15;
-    const double r0 = S.ref[3 * s], r1 = S.ref[3 * s + 1], r2 = S.ref[3 * s + 2];
-    // p = R r, then center + p: same operation order, no contraction
-    double p[3];
-    for (int a = 0; a < 3; ++a)
-        p[a] = __dadd_rn(__dadd_rn(__dmul_rn(R[3 * a], r0), __dmul_rn(R[3 * a + 1], r1)),
-                         __dmul_rn(R[3 * a + 2], r2));
-    double x[3];
-    for (int a = 0; a < 3; ++a) x[a] = __dadd_rn(c[a], p[a]);
-    const double d[3] = {__dsub_rn(x[0], c[0]), __dsub_rn(x[1], c[1]), __dsub_rn(x[2], c[2])};
-    // omega x d (core.hpp:27-29)
-    const double cr[3] = {__dsub_rn(__dmul_rn(w[1], d[2]), __dmul_rn(w[2], d[1])),
-                          __dsub_rn(__dmul_rn(w[2], d[0]), __dmul_rn(w[0], d[2])),
-                          __dsub_rn(__dmul_rn(w[0], d[1]), __dmul_rn(w[1], d[0]))};
-    for (int a = 0; a < 3; ++a) {
-        S.pos[3 * s + a] = x[a];
-        S.ub[3 * s + a] = __dadd_rn(v[a], cr[a]);
-    }
-    const Support ks = kernel_support(x, nx, ny, nz);
-    S.flagged[s] = ks.inside ? 0 : 1;
-}
 
 // update_rigid_motion (ib.cpp:456-489) to step t+1 with host-computed R, c.
 // motion table row (per step): c[3], R[9], v[3], w[3].
@@ -363,7 +309,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     const int ox = corner & 1, oy = (corner >> 1) & 1, oz = corner >> 2;
     const int x = act ? ks.base[0] + ox : 0, y = act ? ks.base[1] + oy : 0;
     const int lz = act ? ks.base[2] + oz - g.gz0 : 0;
-    const float* fin = P.p.f[ctr->t & 1];
+    const float* fin = P.p.f[fcur(g, ctr->t)];
     const long long sl = g.sidx(x, y, lz);
     float v[kLoads];
 #pragma unroll
@@ -422,9 +368,10 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
         S.rec_idx[s * 8u + unsigned(corner)] = s * 8u + unsigned(corner);
     }
     if (have && hl == 0) {
+        const size_t po = ib_half(S, ctr->t);
         for (int a = 0; a < 3; ++a) {
-            S.sampled[3 * s + a] = us[a];
-            S.force[3 * s + a] = fg[a];
+            S.sampled[po + 3 * s + a] = us[a];
+            S.force[po + 3 * s + a] = fg[a];
         }
         if (pos[2] >= double(g.gz0) && pos[2] < double(g.gz0 + g.nzl)) {
             const double rr[3] = {pos[0] - row[0], pos[1] - row[1], pos[2] - row[2]};
@@ -508,11 +455,9 @@ __global__ void init_kernel(const FluidParams P, InitParams ip) {
     double rho, u[3];
     init_state(ip, x, y, gz, rho, u);
     float* f0 = P.p.f[0];
-    float* f1 = P.p.f[1];
     for (int i = 0; i < 27; ++i) {
         const float v = float(feq_shifted(i, rho, u));
-        f0[g.idx(k, i)] = v;
-        f1[g.idx(k, i)] = v;
+        for (int b = 0; b < g.nbuf; ++b) P.p.f[b][g.idx(k, i)] = v;
     }
     P.p.rho[k] = float(rho);
     P.p.u[k] = float(u[0]);
@@ -542,10 +487,10 @@ __global__ void init_kernel(const FluidParams P, InitParams ip) {
 }
 
 // Readback: canonical AoS FP64 for local planes [lz0, lz1).
-__global__ void read_f_kernel(const FluidParams P, int parity, unsigned k0, unsigned k1, double* out) {
+__global__ void read_f_kernel(const FluidParams P, int buffer, unsigned k0, unsigned k1, double* out) {
     const unsigned k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= k1) return;
-    const float* f = P.p.f[parity];
+    const float* f = P.p.f[buffer];
     const RegionGeo& g = P.g;
     for (int i = 0; i < 27; ++i)
         out[size_t(k - k0) * 27 + i] = double(f[g.idx(k, i)]) + weight_d(i);
@@ -692,8 +637,8 @@ void launch_init(const FluidParams& P, const InitParams& ip, cudaStream_t st) {
     init_kernel<<<blocks_for(P.g.n, 256), 256, 0, st>>>(P, ip);
 }
 
-void launch_read_f(const FluidParams& P, int parity, unsigned k0, unsigned k1, double* out, cudaStream_t st) {
-    if (k1 > k0) read_f_kernel<<<blocks_for(k1 - k0, 256), 256, 0, st>>>(P, parity, k0, k1, out);
+void launch_read_f(const FluidParams& P, int buffer, unsigned k0, unsigned k1, double* out, cudaStream_t st) {
+    if (k1 > k0) read_f_kernel<<<blocks_for(k1 - k0, 256), 256, 0, st>>>(P, buffer, k0, k1, out);
 }
 
 void launch_read_macro(const FluidParams& P, unsigned k0, unsigned k1, double* rho, double* u, cudaStream_t st) {

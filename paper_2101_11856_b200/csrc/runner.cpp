@@ -288,6 +288,7 @@ void Runner::compute_geo(Region& r) const {
     g.div_nx = FastDiv(unsigned(nx_));
     g.div_ny = FastDiv(unsigned(ny_));
     g.ghost = 0;
+    g.nbuf = 2;
     if (nx_ % 4 == 0 && ghost_layout_enabled() && variant_fluid_ == 0) {
         // ghost-layer layout (device_common.cuh): pitch nx+4, ny+1 rows,
         // planes -1..nzl, CSoA blocks of alpha >= 256 slots (one staged tile
@@ -328,7 +329,7 @@ void Runner::compute_geo(Region& r) const {
 }
 
 void Runner::alloc_f(Region& r) {
-    for (int p = 0; p < 2; ++p) {
+    for (int p = 0; p < r.geo.nbuf; ++p) {
         r.f[p] = static_cast<float*>(dalloc(sizeof(float) * f_alloc_floats(r.geo), false));
         r.ptr.f[p] = r.f[p];
     }
@@ -424,8 +425,9 @@ void Runner::upload_solids() {
             d.pos = static_cast<double*>(dalloc(sizeof(double) * 3 * n));
             d.ref = static_cast<double*>(dalloc(sizeof(double) * 3 * n));
             d.ub = static_cast<double*>(dalloc(sizeof(double) * 3 * n));
-            d.force = static_cast<double*>(dalloc(sizeof(double) * 3 * n));
-            d.sampled = static_cast<double*>(dalloc(sizeof(double) * 3 * n));
+            d.force = static_cast<double*>(dalloc(sizeof(double) * 3 * kIbHalves * n));  // parts (ib_half)
+            d.sampled = static_cast<double*>(dalloc(sizeof(double) * 3 * kIbHalves * n));
+            d.nbuf = r.geo.nbuf;
             d.source = static_cast<unsigned*>(dalloc(sizeof(unsigned) * n));
             d.flagged = static_cast<unsigned char*>(dalloc(n));
             if (scene_.cfg.ib_mode == LBMG_IB_DETERMINISTIC && n) {
@@ -830,7 +832,7 @@ void Runner::finish_chunk(long t0, long) {
         // rho*/u* of the diverging step from f(t) (solver.cpp:113-122)
         for (auto& r : regions_) {
             FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
-            launch_macro(P, int(t_ & 1), stream());
+            launch_macro(P, t_, stream());
         }
         // the reference returns before update_rigid_motion(t+1)
         if (has_solids_) {
@@ -866,7 +868,7 @@ void Runner::gather(int what, double* out) const {
             const size_t off = size_t(r.z0) * r.geo.plane - base_plane;
             for (unsigned k0 = 0; k0 < r.geo.n; k0 += chunk) {
                 const unsigned k1 = std::min(r.geo.n, k0 + chunk);
-                if (what == 2) launch_read_f(P, int(t_ & 1), k0, k1, stage, stream());
+                if (what == 2) launch_read_f(P, fcur(r.geo, t_), k0, k1, stage, stream());
                 else launch_read_macro(P, k0, k1, what == 0 ? stage : nullptr, what == 1 ? stage : nullptr, stream());
                 CK(cudaGetLastError());
                 CK(cudaMemcpyAsync(out + (off + k0) * beta, stage, sizeof(double) * beta * (k1 - k0),
@@ -933,8 +935,9 @@ void Runner::samples(int region, int solid, double* pos, double* ub, double* for
     CK(cudaStreamSynchronize(stream()));
     if (pos) CK(cudaMemcpy(pos, d.pos, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
     if (ub) CK(cudaMemcpy(ub, d.ub, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
-    if (force) CK(cudaMemcpy(force, d.force, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
-    if (sampled) CK(cudaMemcpy(sampled, d.sampled, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
+    const size_t half = ib_half(d, t_ - 1);  // the last step whose IB phase ran
+    if (force) CK(cudaMemcpy(force, d.force + half, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
+    if (sampled) CK(cudaMemcpy(sampled, d.sampled + half, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
     if (src) CK(cudaMemcpy(src, d.source, sizeof(unsigned) * n, cudaMemcpyDeviceToHost));
     if (flagged) CK(cudaMemcpy(flagged, d.flagged, n, cudaMemcpyDeviceToHost));
 }
@@ -967,14 +970,38 @@ void Runner::set_layout(int ell, size_t alpha) {
         const RegionGeo go = r.geo;
         compute_geo(r);
         const RegionGeo gn = r.geo;
-        if (gn.la == go.la && gn.A == go.A && gn.n_pad == go.n_pad && gn.ghost == go.ghost) continue;
-        for (int p = 0; p < 2; ++p) {
-            float* nf = static_cast<float*>(dalloc(sizeof(float) * f_alloc_floats(gn), false));
-            launch_relayout(r.f[p], nf, go, gn, stream());
-            CK(cudaStreamSynchronize(stream()));
-            dfree(r.f[p]);
-            r.f[p] = nf;
-            r.ptr.f[p] = nf;
+        if (gn.la == go.la && gn.A == go.A && gn.n_pad == go.n_pad && gn.ghost == go.ghost && gn.nbuf == go.nbuf)
+            continue;
+        // f(t) is the population state: permute it into every buffer of the
+        // new layout (the one holding step t first)
+        float* nf[3] = {nullptr, nullptr, nullptr};
+        const int src = fcur(go, t_);
+        for (int b = 0; b < gn.nbuf; ++b) {
+            nf[b] = static_cast<float*>(dalloc(sizeof(float) * f_alloc_floats(gn), false));
+            launch_relayout(r.f[src], nf[b], go, gn, stream());
+        }
+        CK(cudaStreamSynchronize(stream()));
+        for (int b = 0; b < 3; ++b) {
+            if (b < go.nbuf) dfree(r.f[b]);
+            r.f[b] = nf[b];
+            r.ptr.f[b] = nf[b];
+        }
+        if (gn.nbuf != go.nbuf) {  // per-step IB parts: move the readback part
+            for (auto& d : r.solids) {
+                if (d.n) {
+                    IbSolidDev o = d;
+                    o.nbuf = go.nbuf;
+                    const size_t from = ib_half(o, t_ - 1);
+                    d.nbuf = gn.nbuf;
+                    const size_t to = ib_half(d, t_ - 1);
+                    CK(cudaMemcpy(d.force + to, d.force + from, 24 * d.n, cudaMemcpyDeviceToDevice));
+                    CK(cudaMemcpy(d.sampled + to, d.sampled + from, 24 * d.n, cudaMemcpyDeviceToDevice));
+                }
+                d.nbuf = gn.nbuf;
+            }
+            if (r.batch_solids)
+                CK(cudaMemcpy(r.batch_solids, r.solids.data(), sizeof(IbSolidDev) * r.solids.size(),
+                              cudaMemcpyHostToDevice));
         }
     }
     (void)old;
@@ -984,23 +1011,24 @@ void Runner::set_layout(int ell, size_t alpha) {
         for (auto& d : r.solids) {
             const size_t n = d.n;
             if (n == 0) continue;
-            std::vector<double> pos(3 * n), ref(3 * n), ub(3 * n), fo(3 * n), sa(3 * n);
+            std::vector<double> pos(3 * n), ref(3 * n), ub(3 * n), fo(3 * kIbHalves * n), sa(3 * kIbHalves * n);
             std::vector<unsigned> src(n);
             std::vector<unsigned char> fl(n);
             CK(cudaMemcpy(pos.data(), d.pos, 24 * n, cudaMemcpyDeviceToHost));
             CK(cudaMemcpy(ref.data(), d.ref, 24 * n, cudaMemcpyDeviceToHost));
             CK(cudaMemcpy(ub.data(), d.ub, 24 * n, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(fo.data(), d.force, 24 * n, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(sa.data(), d.sampled, 24 * n, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(fo.data(), d.force, fo.size() * 8, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(sa.data(), d.sampled, sa.size() * 8, cudaMemcpyDeviceToHost));
             CK(cudaMemcpy(src.data(), d.source, 4 * n, cudaMemcpyDeviceToHost));
             CK(cudaMemcpy(fl.data(), d.flagged, n, cudaMemcpyDeviceToHost));
             std::vector<V3> p3(n);
             for (size_t k = 0; k < n; ++k) p3[k] = v3(&pos[3 * k]);
             const auto perm = reorder_permutation(p3, std::vector<uint32_t>(src.begin(), src.end()), ell);
-            auto permute3 = [&](std::vector<double>& v) {
+            auto permute3 = [&](std::vector<double>& v) {  // every 3n half
                 std::vector<double> o(v.size());
-                for (size_t k = 0; k < n; ++k)
-                    for (int a = 0; a < 3; ++a) o[3 * k + a] = v[3 * perm[k] + a];
+                for (size_t h = 0; h < v.size(); h += 3 * n)
+                    for (size_t k = 0; k < n; ++k)
+                        for (int a = 0; a < 3; ++a) o[h + 3 * k + a] = v[h + 3 * perm[k] + a];
                 v.swap(o);
             };
             permute3(pos);
@@ -1017,8 +1045,8 @@ void Runner::set_layout(int ell, size_t alpha) {
             CK(cudaMemcpy(d.pos, pos.data(), 24 * n, cudaMemcpyHostToDevice));
             CK(cudaMemcpy(d.ref, ref.data(), 24 * n, cudaMemcpyHostToDevice));
             CK(cudaMemcpy(d.ub, ub.data(), 24 * n, cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(d.force, fo.data(), 24 * n, cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(d.sampled, sa.data(), 24 * n, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(d.force, fo.data(), fo.size() * 8, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(d.sampled, sa.data(), sa.size() * 8, cudaMemcpyHostToDevice));
             CK(cudaMemcpy(d.source, s2.data(), 4 * n, cudaMemcpyHostToDevice));
             CK(cudaMemcpy(d.flagged, f2.data(), n, cudaMemcpyHostToDevice));
         }
@@ -1095,8 +1123,8 @@ void Runner::copy_state_from(const Runner& o) {
         Region& d = regions_[ri];
         const Region& s = o.regions_[ri];
         const RegionGeo& g = d.geo;
+        for (int b = 0; b < g.nbuf; ++b) cp(d.f[b], s.f[b], sizeof(float) * 27ull * g.n_pad);
         for (int p = 0; p < 2; ++p) {
-            cp(d.f[p], s.f[p], sizeof(float) * 27ull * g.n_pad);
             cp(d.recv_lo[p], s.recv_lo[p], sizeof(float) * 9ull * g.plane);
             cp(d.recv_hi[p], s.recv_hi[p], sizeof(float) * 9ull * g.plane);
             cp(d.own_send_lo[p], s.own_send_lo[p], sizeof(float) * 9ull * g.plane);
@@ -1115,8 +1143,8 @@ void Runner::copy_state_from(const Runner& o) {
                 cp(a.pos, b.pos, 24 * n);
                 cp(a.ref, b.ref, 24 * n);
                 cp(a.ub, b.ub, 24 * n);
-                cp(a.force, b.force, 24 * n);
-                cp(a.sampled, b.sampled, 24 * n);
+                cp(a.force, b.force, 24 * kIbHalves * n);
+                cp(a.sampled, b.sampled, 24 * kIbHalves * n);
                 cp(a.source, b.source, 4 * n);
                 cp(a.flagged, b.flagged, n);
             }

@@ -126,7 +126,7 @@ private:
         bool has_lo = false, has_hi = false;
         RegionGeo geo{};
         RegionPtrs ptr{};
-        float* f[2] = {nullptr, nullptr};
+        float* f[3] = {nullptr, nullptr, nullptr};
         float* recv_lo[2] = {nullptr, nullptr};
         float* recv_hi[2] = {nullptr, nullptr};
         float* own_send_lo[2] = {nullptr, nullptr};  // rank mode only

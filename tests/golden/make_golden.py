@@ -9,6 +9,12 @@ Fixtures (small, FP64, reference threads=1 so atomic-mode IB is ordered):
   fins_ib.npz    rotating fin comb 40x24x24, 20 steps: samples, totals
   c1_anchor.npz  C1 64^3 (SURVEY §8(c) recommended), scalars at t=100 and t=1000
   kats.npz       SPEC.md examples (morton3, split_domain, feq(1,0), ...)
+  c2_anchor.npz  C2 256x128x128 sphere + IB: mass, max|u|,
+                 reaction force at t=100/200/300 and the z=64 rho/u planes at
+                 t=300 (reference on all host threads: atomic-mode spreading,
+                 so the last digits vary at ~1e-15 relative)
+
+    python tests/golden/make_golden.py c2     # only c2_anchor.npz (~5 min)
 """
 import sys
 from pathlib import Path
@@ -31,7 +37,28 @@ def _run(cfg, steps, samples=None):
     return r
 
 
+def c2_anchor():
+    cfg = scenes.sphere()
+    r = refpy.RefRunner(cfg)
+    out = {}
+    for t in (100, 200, 300):
+        st = r.advance(t - r.step_count())
+        assert st["ok"], st
+        rho, u = r.gather_rho(), r.gather_u()
+        out[f"mass_{t}"] = rho.sum()
+        out[f"umax_{t}"] = np.sqrt((u ** 2).sum(axis=1)).max()
+        out[f"force_{t}"] = r.totals_log()[-1][:3]
+    out["rho_plane_300"] = rho.reshape(128, 128, 256)[64]
+    out["u_plane_300"] = u.reshape(128, 128, 256, 3)[64]
+    out["samples"] = len(r.samples(0, 0)["source_id"])
+    np.savez_compressed(HERE / "c2_anchor.npz", **out)
+    print({k: v for k, v in out.items() if np.ndim(v) <= 1})
+
+
 def main():
+    if sys.argv[1:] == ["c2"]:
+        c2_anchor()
+        return
     cfg = scenes.cavity(n=10)
     r = _run(cfg, 30)
     np.savez_compressed(HERE / "cavity10.npz", f=r.gather_f(), rho=r.gather_rho(), u=r.gather_u(), steps=30)
@@ -75,6 +102,7 @@ def main():
         "feq_1_u": refpy.ref_equilibrium(1.02, np.array([0.05, -0.02, 0.01])),
     }
     np.savez_compressed(HERE / "kats.npz", **kats)
+    c2_anchor()
     for p in sorted(HERE.glob("*.npz")):
         print(p.name, p.stat().st_size)
 

@@ -316,10 +316,52 @@ def test_divergence_is_reported_and_freezes():
     sr = r.advance(3000)
     assert not st.ok and not sr["ok"]
     assert st.reason == sr["reason"]
+    # fp32 vs FP64 arithmetic in a blow-up: the detection step may differ by a
+    # step or two; the IB case above pins it exactly
     assert abs(st.step - sr["step"]) <= 3
     assert g.step_count() == st.step
     st2 = g.advance(10)
     assert g.step_count() == st.step and not st2.ok
+
+
+def test_mach_warning_matches_reference():
+    # mach_limit_exceeded (|u|^2 >= 0.16, collision.hpp:55) is a sticky warning
+    # (solver.cpp:120, runner.cpp:159): a periodic box accelerated by a body
+    # force crosses |u| = 0.4 at step ~50 (u = 0.3505 + 1e-3 t)
+    cfg = scenes.taylor_green(nx=8, ny=8, nz=8)
+    cfg.init = "uniform"
+    cfg.init_velocity = (0.3505, 0.0, 0.0)
+    cfg.body_force = (1e-3, 0.0, 0.0)
+    g = lbm.Runner(lbm.build_scene(cfg))
+    r = refpy.RefRunner(cfg, threads=1)
+    for t, expect in ((45, False), (55, True), (60, True)):
+        sg = g.advance(t - g.step_count())
+        sr = r.advance(t - r.step_count())
+        assert sg.ok and sr["ok"]
+        assert bool(sr["mach_warning"]) is expect
+        assert sg.mach_warning is expect, (t, sg)
+        assert g.status().mach_warning is expect
+    assert rel_l2(g.gather_u(), r.gather_u()) <= U_TOL
+
+
+def test_diverging_step_skips_ib_like_reference():
+    # Dense sampling (Poisson r = 0.3) diverges within a few steps (SURVEY §0
+    # fact 5a).  The reference returns before IB on the diverging step
+    # (runner.cpp:154-161): the sample forces / sampled velocities it holds are
+    # those of the previous step, moving samples stay at t, no totals row.
+    cfg = scenes.sphere(48, 32, 32, center=(16, 16, 16), radius=5.0, subdiv=3, r=0.3)
+    g = lbm.Runner(lbm.build_scene(cfg))
+    r = refpy.RefRunner(cfg, threads=1)
+    sg, sr = g.advance(200), r.advance(200)
+    assert not sg.ok and not sr["ok"] and sg.reason == sr["reason"]
+    assert sg.step == sr["step"], (sg.step, sr["step"])
+    assert g.step_count() == r.step_count() == sg.step
+    assert g.totals_log().shape == r.totals_log().shape == (sg.step, 6)
+    a, b = g.samples(0, 0), r.samples(0, 0)
+    assert np.array_equal(a["positions"], b["positions"]) and np.array_equal(a["flagged"], b["flagged"])
+    for k in ("penalty_force", "sampled_velocity"):
+        ref = np.abs(b[k]).max()
+        assert np.abs(a[k] - b[k]).max() <= 1e-3 * ref + 1e-9, k
 
 
 def test_clone_is_independent_and_identical():

@@ -2,6 +2,7 @@
 unmodified reference (oracle/_ref): bit-identical FP64 on every step
 function, integer helper and whole-run field, plus the SPEC examples."""
 import numpy as np
+from pathlib import Path
 import pytest
 
 import paper_2101_11856_b200 as lbm
@@ -153,3 +154,18 @@ def test_divergence_bitwise():
     o, r, so, sr = _run_both(cfg, 2000)
     assert not so["ok"] and so == sr
     assert np.array_equal(o.gather_rho(), r.gather_rho())
+
+
+def test_c2_anchor_fixture_matches_survey_table():
+    # tests/golden/c2_anchor.npz is written by the unmodified reference
+    # (make_golden.py c2); SURVEY.md §8(c) recorded the same anchors from an
+    # independent probe of the reference: mass, max|u|, reaction force.
+    gold = np.load(Path(__file__).parent / "golden" / "c2_anchor.npz")
+    table = {100: (4195873.0964478, 0.06738708, (24.07249, 0.1624865, 0.1420280)),
+             200: (4197716.8690329, 0.06545837, (13.03389, 0.1435446, 0.1404260)),
+             300: (4202373.2614346, 0.06606140, (0.8222260, -0.06475448, -0.04553023))}
+    for t, (mass, umax, force) in table.items():
+        assert abs(float(gold[f"mass_{t}"]) - mass) <= 1e-7 * mass
+        assert abs(float(gold[f"umax_{t}"]) - umax) <= 1e-8
+        assert np.allclose(gold[f"force_{t}"], force, rtol=2e-6, atol=1e-9)
+    assert int(gold["samples"]) == 8329
