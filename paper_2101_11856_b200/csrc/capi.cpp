@@ -511,6 +511,10 @@ long lbmg_runner_sync_interval(const lbmg_runner* r) {
     return r && r->impl ? r->impl->chunk_cap() : 0;
 }
 
+long lbmg_runner_kernel_launches(const lbmg_runner* r) {
+    return r && r->impl ? r->impl->kernel_launches() : 0;
+}
+
 long lbmg_runner_kernels_per_step(const lbmg_runner* r) {
     return r && r->impl ? r->impl->kernels_per_step_ : 0;
 }

@@ -69,6 +69,18 @@ double feq(int i, double rho, const double u[3]) {
 
 }  // namespace
 
+// Every host-side copy of the runner goes through its own (non-blocking)
+// stream and completes before returning: a plain cudaMemcpy runs on the
+// legacy default stream, which non-blocking streams do not wait for, and a
+// device-to-device (or pageable host-to-device) cudaMemcpy may return before
+// the data has landed.
+cudaError_t Runner::copy_sync(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) const {
+    cudaStream_t st = stream();
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, st);
+    if (e != cudaSuccess) return e;
+    return cudaStreamSynchronize(st);
+}
+
 FluidParams Runner::Region::params() const { return FluidParams{geo, {}, {}, ptr, nullptr}; }
 
 void* Runner::dalloc(size_t bytes, bool zero) {
@@ -80,7 +92,10 @@ void* Runner::dalloc(size_t bytes, bool zero) {
         throw OomError("device allocation of " + std::to_string(bytes) + " bytes failed: " +
                        cudaGetErrorString(e));
     }
-    if (zero) CK(cudaMemset(p, 0, bytes));
+    if (zero) {  // on the runner's stream (non-blocking streams skip the legacy one), complete on return
+        CK(cudaMemsetAsync(p, 0, bytes, stream()));
+        CK(cudaStreamSynchronize(stream()));
+    }
     allocs_.push_back(p);
     return p;
 }
@@ -174,6 +189,7 @@ Runner::Runner(const lbmg_scene& scene, int regions, int device, int world, int 
     CK(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming));
 
+    if (pipeline_eligible()) variant_fluid_ = 2;  // the step pipeline where it applies
     const int first = rank_mode_ ? rank_ : 0;
     const int count = rank_mode_ ? 1 : m_global_;
     regions_.resize(count);
@@ -205,6 +221,7 @@ Runner::Runner(const lbmg_scene& scene, int regions, int device, int world, int 
     }
     upload_solids();
     init_fields();
+    if (pipeline_on()) build_pipeline();
     if (rank_mode_ && has_solids_) fill_motion_table(0, cap_ + 1, true);
     for (const auto& e : scene_.emitters) {
         if (e.rate < 0) throw ConfigError("tracers: rate must be >= 0");
@@ -256,6 +273,142 @@ void Runner::invalidate_graphs() {
             cudaGraphExecDestroy(g);
             g = nullptr;
         }
+    for (auto& row : pgraph_)
+        for (auto& g : row)
+            if (g) {
+                cudaGraphExecDestroy(g);
+                g = nullptr;
+            }
+}
+
+bool Runner::pipeline_eligible() const {
+    static const bool off = [] {
+        const char* e = std::getenv("LBMG_PIPELINE");
+        return e && std::string(e) == "0";
+    }();
+    return !off && !rank_mode_ && m_global_ == 1 && nx_ % 4 == 0 && ghost_layout_enabled() &&
+           scene_.emitters.empty() && scene_.cfg.ib_mode == LBMG_IB_ATOMIC;
+}
+
+// Tables of the step pipeline for the current layout (make_pipe_plan): the
+// per-step item order, fill chunks, per-plane item counts, IB items per solid
+// and the planes the IB support can touch over the run.
+void Runner::build_pipeline() {
+    Region& r = regions_[0];
+    const RegionGeo& g = r.geo;
+    const size_t ns = scene_.solids.size();
+    std::vector<unsigned> start(ns + 1, 0);
+    for (size_t k = 0; k < ns; ++k)
+        start[k + 1] = start[k] + unsigned((r.solids[k].n + kPipeIbSamples - 1) / kPipeIbSamples);
+    const unsigned n_ib = start[ns];
+    // static solids: their samples' support planes; rotating ones: the
+    // centre +- the largest reference radius (+1); translating ones: anywhere
+    int z0 = g.nzl, z1 = -1;
+    for (const auto& so : scene_.solids) {
+        if (so.samples.size() == 0) continue;
+        double lo = 1e300, hi = -1e300;
+        if (!so.moving) {
+            for (const auto& q : so.samples.positions) {
+                lo = std::min(lo, q.z);
+                hi = std::max(hi, q.z);
+            }
+        } else if (dot(so.linear_velocity, so.linear_velocity) != 0.0) {
+            lo = -1e300;
+            hi = 1e300;
+        } else {
+            double r2 = 0.0;
+            for (const auto& q : so.samples.reference_positions) r2 = std::max(r2, dot(q, q));
+            const double rad = std::sqrt(r2) + 1.0;
+            lo = so.center.z - rad;
+            hi = so.center.z + rad;
+        }
+        auto base = [&](double z) {
+            const double c = std::min(std::max(std::floor(z), 0.0), double(nz_ - 2));
+            return int(c);
+        };
+        z0 = std::min(z0, std::max(0, base(lo) - g.gz0));
+        z1 = std::max(z1, std::min(g.nzl - 1, base(hi) + 1 - g.gz0));
+    }
+    if (n_ib == 0) {
+        z0 = 0;
+        z1 = -1;
+    }
+    const PipePlan pl = make_pipe_plan(g, n_ib, z0, z1);
+    auto upload = [&](unsigned*& dst, const std::vector<unsigned>& v) {
+        dfree(dst);
+        dst = static_cast<unsigned*>(dalloc(sizeof(unsigned) * std::max<size_t>(v.size(), 1), false));
+        if (!v.empty()) CK(copy_sync(dst, v.data(), sizeof(unsigned) * v.size(), cudaMemcpyHostToDevice));
+    };
+    upload(pipe_.pattern, pl.pattern);
+    upload(pipe_.fill_desc, pl.fill_desc);
+    upload(pipe_.fill_need, pl.fill_need);
+    upload(pipe_.tile_need, pl.tile_need);
+    upload(pipe_.ib_start, start);
+    dfree(pipe_.pc);
+    pipe_.pc = static_cast<PipeCounters*>(dalloc(pipe_counter_bytes(g)));
+    pipe_.n_items = unsigned(pl.pattern.size());
+    pipe_.n_tiles = pl.n_tiles;
+    pipe_.n_ib = n_ib;
+    pipe_.org = pl.org;
+    pipe_.z0 = z0;
+    pipe_.z1 = z1;
+    invalidate_graphs();
+}
+
+void Runner::enqueue_pipeline(int K, int macro_j) {
+    Region& r = regions_[0];
+    PipeParams Q{};
+    Q.P = FluidParams{r.geo, faces_, model_, r.ptr, ctr_};
+    if (has_solids_) {
+        const int ns = int(scene_.solids.size());
+        Q.B.solids = r.batch_solids;
+        Q.B.block_start = r.batch_start;
+        Q.B.moving = r.batch_moving;
+        Q.B.n_solids = unsigned(ns);
+        Q.B.table = motion_tab_;
+        Q.B.table_stride = size_t(cap_ + 2) * kMotionRow;
+        Q.B.partial = r.fused_partial;
+        Q.B.done = r.fused_done;
+        Q.B.out_base = totals_dev_;
+        Q.B.out_stride = ns * 6;
+    }
+    Q.ib_item_start = pipe_.ib_start;
+    Q.pattern = pipe_.pattern;
+    Q.fill_desc = pipe_.fill_desc;
+    Q.fill_need = pipe_.fill_need;
+    Q.tile_need = pipe_.tile_need;
+    Q.pc = pipe_.pc;
+    Q.n_items = pipe_.n_items;
+    Q.K = unsigned(K);
+    Q.n_tiles = pipe_.n_tiles;
+    Q.n_ib = pipe_.n_ib;
+    Q.org = pipe_.org;
+    Q.macro_j = macro_j;
+    Q.z0_ib = pipe_.z0;
+    Q.z1_ib = pipe_.z1;
+    static const int dbg = [] {
+        const char* e = std::getenv("LBMG_PIPE_DBG");
+        return e ? std::atoi(e) : 0;
+    }();
+    Q.dbg = dbg;
+    launch_pipeline(Q, sm_count_, stream());
+}
+
+// Pipeline graphs: K steps per launch (1..kPipeSteps), with or without the
+// rho*/u* write on the launch's last step; captured together on first use.
+cudaGraphExec_t Runner::pipeline_graph(int K, bool macro) {
+    cudaGraphExec_t& g = pgraph_[K][macro ? 1 : 0];
+    if (!g) {
+        cudaStream_t st = stream();
+        cudaGraph_t graph;
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        enqueue_pipeline(K, macro ? K - 1 : -1);
+        CK(cudaStreamEndCapture(st, &graph));
+        CK(cudaGraphInstantiate(&g, graph, 0));
+        CK(cudaGraphDestroy(graph));
+        CK(cudaGraphUpload(g, st));
+    }
+    return g;
 }
 
 void Runner::compute_geo(Region& r) const {
@@ -289,7 +442,8 @@ void Runner::compute_geo(Region& r) const {
     g.div_ny = FastDiv(unsigned(ny_));
     g.ghost = 0;
     g.nbuf = 2;
-    if (nx_ % 4 == 0 && ghost_layout_enabled() && variant_fluid_ == 0) {
+    if (nx_ % 4 == 0 && ghost_layout_enabled() && (variant_fluid_ == 0 || variant_fluid_ == 2)) {
+        g.nbuf = variant_fluid_ == 2 ? 3 : 2;
         // ghost-layer layout (device_common.cuh): pitch nx+4, ny+1 rows,
         // planes -1..nzl, CSoA blocks of alpha >= 256 slots (one staged tile
         // writes one contiguous 27 KB block); alpha >= slots is SoA
@@ -446,9 +600,9 @@ void Runner::upload_solids() {
                     ref[3 * k + a] = s.samples.reference_positions[k][a];
                 }
             if (n) {
-                CK(cudaMemcpy(d.pos, pos.data(), sizeof(double) * 3 * n, cudaMemcpyHostToDevice));
-                CK(cudaMemcpy(d.ref, ref.data(), sizeof(double) * 3 * n, cudaMemcpyHostToDevice));
-                CK(cudaMemcpy(d.source, s.samples.source_id.data(), sizeof(unsigned) * n,
+                CK(copy_sync(d.pos, pos.data(), sizeof(double) * 3 * n, cudaMemcpyHostToDevice));
+                CK(copy_sync(d.ref, ref.data(), sizeof(double) * 3 * n, cudaMemcpyHostToDevice));
+                CK(copy_sync(d.source, s.samples.source_id.data(), sizeof(unsigned) * n,
                               cudaMemcpyHostToDevice));
             }
             r.solids.push_back(d);
@@ -465,9 +619,9 @@ void Runner::upload_solids() {
             r.batch_solids = static_cast<IbSolidDev*>(dalloc(sizeof(IbSolidDev) * ns));
             r.batch_start = static_cast<unsigned*>(dalloc(sizeof(unsigned) * (ns + 1)));
             r.batch_moving = static_cast<int*>(dalloc(sizeof(int) * ns));
-            CK(cudaMemcpy(r.batch_solids, r.solids.data(), sizeof(IbSolidDev) * ns, cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(r.batch_start, start.data(), sizeof(unsigned) * (ns + 1), cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(r.batch_moving, mv.data(), sizeof(int) * ns, cudaMemcpyHostToDevice));
+            CK(copy_sync(r.batch_solids, r.solids.data(), sizeof(IbSolidDev) * ns, cudaMemcpyHostToDevice));
+            CK(copy_sync(r.batch_start, start.data(), sizeof(unsigned) * (ns + 1), cudaMemcpyHostToDevice));
+            CK(copy_sync(r.batch_moving, mv.data(), sizeof(int) * ns, cudaMemcpyHostToDevice));
             r.batch_blocks = start[ns];
         }
     }
@@ -542,7 +696,7 @@ void Runner::init_fields() {
         for (size_t s = 0; s < scene_.solids.size(); ++s) {
             double h[kMotionRow];
             motion_row(int(s), 0, h);
-            CK(cudaMemcpy(row, h, sizeof h, cudaMemcpyHostToDevice));
+            CK(copy_sync(row, h, sizeof h, cudaMemcpyHostToDevice));
             for (auto& r : regions_) launch_ib_motion_once(r.solids[s], row, nx_, ny_, nz_, stream());
             CK(cudaStreamSynchronize(stream()));
         }
@@ -691,6 +845,12 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
 // All three are captured and instantiated together on first use.
 void Runner::ensure_graphs() {
     cudaStream_t st = stream();
+    if (pipeline_on()) {
+        for (int K = 1; K <= kPipeSteps; ++K)
+            for (int m = 0; m < 2; ++m) pipeline_graph(K, m != 0);
+        kernels_per_step_ = 2;  // pipeline_begin + pipeline_kernel per launch of up to kPipeSteps steps
+        return;
+    }
     for (int which = 0; which < 3; ++which) {
         cudaGraphExec_t& g = graph_[which];
         if (g) continue;
@@ -710,6 +870,7 @@ void Runner::ensure_graphs() {
             if (ty == cudaGraphNodeTypeKernel) ++kernels;
         }
         if (which == 0) kernels_per_step_ = kernels;
+        graph_kernels_[which] = kernels;
         CK(cudaGraphInstantiate(&g, graph, 0));
         CK(cudaGraphDestroy(graph));
         // upload now: the first launch of a fresh executable graph pays it otherwise
@@ -748,23 +909,44 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
         if (!written)
             CK(cudaMemcpyAsync(&ctr_->chunk_t0, pinned_up_, sizeof(long long), cudaMemcpyHostToDevice, st));
         std::vector<std::array<cudaEvent_t, 5>> evs;
+        std::vector<std::pair<std::array<cudaEvent_t, 2>, long>> pev;  // pipeline launches (timings)
         // every step graph is captured and instantiated before the first one
         // runs, so no later advance() pays a capture inside its own time
         if (!timings) ensure_graphs();
-        for (long j = 0; j < chunk;) {
+        for (long j = 0; pipeline_on() && j < chunk;) {
+            const long K = std::min<long>(kPipeSteps, chunk - j);
+            const bool last = done + j + K == steps;
+            if (last && snap_pending_) CK(cudaStreamWaitEvent(st, snap_done_, 0));
+            if (timings) {
+                std::array<cudaEvent_t, 2> e;
+                for (auto& x : e) CK(cudaEventCreate(&x));
+                CK(cudaEventRecord(e[0], st));
+                enqueue_pipeline(int(K), last ? int(K) - 1 : -1);
+                CK(cudaEventRecord(e[1], st));
+                pev.push_back({e, K});
+            } else {
+                CK(cudaGraphLaunch(pipeline_graph(int(K), last), st));
+            }
+            launches_ += 2;
+            j += K;
+        }
+        for (long j = 0; !pipeline_on() && j < chunk;) {
             const bool last = done + j == steps - 1;
             if (last && snap_pending_) CK(cudaStreamWaitEvent(st, snap_done_, 0));
             if (timings) {
                 std::vector<cudaEvent_t> e(5);
                 for (auto& x : e) CK(cudaEventCreate(&x));
                 enqueue_step(last, &e);
+                launches_ += kernels_per_step_;
                 evs.push_back({e[0], e[1], e[2], e[3], e[4]});
                 ++j;
             } else if (!last && j + kMultiSteps < chunk && done + j + kMultiSteps < steps) {
                 CK(cudaGraphLaunch(graph_[2], st));
+                launches_ += graph_kernels_[2];
                 j += kMultiSteps;
             } else {
                 CK(cudaGraphLaunch(graph_[last ? 1 : 0], st));
+                launches_ += graph_kernels_[last ? 1 : 0];
                 ++j;
             }
         }
@@ -775,6 +957,18 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
         CK(cudaStreamSynchronize(st));
         CK(cudaGetLastError());
         downloaded_ = true;
+        if (timings) {  // pipeline: the launch's time spread over its K steps
+            long step = t0;
+            for (auto& [e, K] : pev) {
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, e[0], e[1]));
+                for (long q = 0; q < K; ++q, ++step) {
+                    timings->push_back({"fluid", step, ms * 1e-3 / double(K)});
+                    timings->push_back({"total", step, ms * 1e-3 / double(K)});
+                }
+                for (auto x : e) cudaEventDestroy(x);
+            }
+        }
         if (timings) {
             for (size_t j = 0; j < evs.size(); ++j) {
                 float seg[4] = {0, 0, 0, 0};
@@ -802,13 +996,13 @@ void Runner::finish_chunk(long t0, long) {
     downloaded_ = false;
     DevCounters h{};
     if (pre) std::memcpy(&h, pinned_down_, sizeof h);
-    else CK(cudaMemcpy(&h, ctr_, sizeof h, cudaMemcpyDeviceToHost));
+    else CK(copy_sync(&h, ctr_, sizeof h, cudaMemcpyDeviceToHost));
     const long completed = long(h.t) - t0;
     if (has_solids_ && completed > 0) {
         const size_t ns = scene_.solids.size(), m = regions_.size();
         std::vector<double> tot(size_t(completed) * m * ns * 6);
         if (pre) std::memcpy(tot.data(), pinned_down_ + kCtrBytes, sizeof(double) * tot.size());
-        else CK(cudaMemcpy(tot.data(), totals_dev_, sizeof(double) * tot.size(), cudaMemcpyDeviceToHost));
+        else CK(copy_sync(tot.data(), totals_dev_, sizeof(double) * tot.size(), cudaMemcpyDeviceToHost));
         for (long j = 0; j < completed; ++j) {
             std::array<double, 6> sum{};
             for (size_t r = 0; r < m; ++r)
@@ -820,14 +1014,14 @@ void Runner::finish_chunk(long t0, long) {
     if (has_tracers_ && completed > 0) {
         tn_ += temit_ * (unsigned long long)completed;
         unsigned long long ts[2];
-        CK(cudaMemcpy(ts, tdev_.state, sizeof ts, cudaMemcpyDeviceToHost));
+        CK(copy_sync(ts, tdev_.state, sizeof ts, cudaMemcpyDeviceToHost));
         tdead_ = ts[1];
     }
     t_ = long(h.t);
     if (h.mach) status_.mach_warning = true;
     if (h.diverged && status_.ok) {
         status_.ok = false;
-        status_.step = long(h.diverged_step);
+        status_.step = long(h.t);  // the counter stops at the diverging step (both paths)
         status_.reason = "divergence: non-positive or non-finite density";
         // rho*/u* of the diverging step from f(t) (solver.cpp:113-122)
         for (auto& r : regions_) {
@@ -841,7 +1035,7 @@ void Runner::finish_chunk(long t0, long) {
                 if (!moving_[s]) continue;
                 double hrow[kMotionRow];
                 motion_row(int(s), t_, hrow);
-                CK(cudaMemcpy(row, hrow, sizeof hrow, cudaMemcpyHostToDevice));
+                CK(copy_sync(row, hrow, sizeof hrow, cudaMemcpyHostToDevice));
                 for (auto& r : regions_) launch_ib_motion_once(r.solids[s], row, nx_, ny_, nz_, stream());
                 CK(cudaStreamSynchronize(stream()));
             }
@@ -933,13 +1127,13 @@ void Runner::samples(int region, int solid, double* pos, double* ub, double* for
     const size_t n = d.n;
     if (n == 0) return;
     CK(cudaStreamSynchronize(stream()));
-    if (pos) CK(cudaMemcpy(pos, d.pos, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
-    if (ub) CK(cudaMemcpy(ub, d.ub, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
+    if (pos) CK(copy_sync(pos, d.pos, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
+    if (ub) CK(copy_sync(ub, d.ub, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
     const size_t half = ib_half(d, t_ - 1);  // the last step whose IB phase ran
-    if (force) CK(cudaMemcpy(force, d.force + half, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
-    if (sampled) CK(cudaMemcpy(sampled, d.sampled + half, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
-    if (src) CK(cudaMemcpy(src, d.source, sizeof(unsigned) * n, cudaMemcpyDeviceToHost));
-    if (flagged) CK(cudaMemcpy(flagged, d.flagged, n, cudaMemcpyDeviceToHost));
+    if (force) CK(copy_sync(force, d.force + half, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
+    if (sampled) CK(copy_sync(sampled, d.sampled + half, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
+    if (src) CK(copy_sync(src, d.source, sizeof(unsigned) * n, cudaMemcpyDeviceToHost));
+    if (flagged) CK(copy_sync(flagged, d.flagged, n, cudaMemcpyDeviceToHost));
 }
 
 void Runner::cell_flags(uint8_t* out) const {
@@ -951,7 +1145,7 @@ void Runner::cell_flags(uint8_t* out) const {
         launch_cell_flags(P, 0, r.geo.n, d, stream());
         CK(cudaStreamSynchronize(stream()));
         const size_t off = size_t(r.z0) * r.geo.plane - base_plane;
-        cudaError_t e = cudaMemcpy(out + off * 27, d, size_t(r.geo.n) * 27, cudaMemcpyDeviceToHost);
+        cudaError_t e = copy_sync(out + off * 27, d, size_t(r.geo.n) * 27, cudaMemcpyDeviceToHost);
         cudaFree(d);
         CK(e);
     }
@@ -994,13 +1188,13 @@ void Runner::set_layout(int ell, size_t alpha) {
                     const size_t from = ib_half(o, t_ - 1);
                     d.nbuf = gn.nbuf;
                     const size_t to = ib_half(d, t_ - 1);
-                    CK(cudaMemcpy(d.force + to, d.force + from, 24 * d.n, cudaMemcpyDeviceToDevice));
-                    CK(cudaMemcpy(d.sampled + to, d.sampled + from, 24 * d.n, cudaMemcpyDeviceToDevice));
+                    CK(copy_sync(d.force + to, d.force + from, 24 * d.n, cudaMemcpyDeviceToDevice));
+                    CK(copy_sync(d.sampled + to, d.sampled + from, 24 * d.n, cudaMemcpyDeviceToDevice));
                 }
                 d.nbuf = gn.nbuf;
             }
             if (r.batch_solids)
-                CK(cudaMemcpy(r.batch_solids, r.solids.data(), sizeof(IbSolidDev) * r.solids.size(),
+                CK(copy_sync(r.batch_solids, r.solids.data(), sizeof(IbSolidDev) * r.solids.size(),
                               cudaMemcpyHostToDevice));
         }
     }
@@ -1014,13 +1208,13 @@ void Runner::set_layout(int ell, size_t alpha) {
             std::vector<double> pos(3 * n), ref(3 * n), ub(3 * n), fo(3 * kIbHalves * n), sa(3 * kIbHalves * n);
             std::vector<unsigned> src(n);
             std::vector<unsigned char> fl(n);
-            CK(cudaMemcpy(pos.data(), d.pos, 24 * n, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(ref.data(), d.ref, 24 * n, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(ub.data(), d.ub, 24 * n, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(fo.data(), d.force, fo.size() * 8, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(sa.data(), d.sampled, sa.size() * 8, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(src.data(), d.source, 4 * n, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(fl.data(), d.flagged, n, cudaMemcpyDeviceToHost));
+            CK(copy_sync(pos.data(), d.pos, 24 * n, cudaMemcpyDeviceToHost));
+            CK(copy_sync(ref.data(), d.ref, 24 * n, cudaMemcpyDeviceToHost));
+            CK(copy_sync(ub.data(), d.ub, 24 * n, cudaMemcpyDeviceToHost));
+            CK(copy_sync(fo.data(), d.force, fo.size() * 8, cudaMemcpyDeviceToHost));
+            CK(copy_sync(sa.data(), d.sampled, sa.size() * 8, cudaMemcpyDeviceToHost));
+            CK(copy_sync(src.data(), d.source, 4 * n, cudaMemcpyDeviceToHost));
+            CK(copy_sync(fl.data(), d.flagged, n, cudaMemcpyDeviceToHost));
             std::vector<V3> p3(n);
             for (size_t k = 0; k < n; ++k) p3[k] = v3(&pos[3 * k]);
             const auto perm = reorder_permutation(p3, std::vector<uint32_t>(src.begin(), src.end()), ell);
@@ -1042,20 +1236,25 @@ void Runner::set_layout(int ell, size_t alpha) {
                 s2[k] = src[perm[k]];
                 f2[k] = fl[perm[k]];
             }
-            CK(cudaMemcpy(d.pos, pos.data(), 24 * n, cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(d.ref, ref.data(), 24 * n, cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(d.ub, ub.data(), 24 * n, cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(d.force, fo.data(), fo.size() * 8, cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(d.sampled, sa.data(), sa.size() * 8, cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(d.source, s2.data(), 4 * n, cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(d.flagged, f2.data(), n, cudaMemcpyHostToDevice));
+            CK(copy_sync(d.pos, pos.data(), 24 * n, cudaMemcpyHostToDevice));
+            CK(copy_sync(d.ref, ref.data(), 24 * n, cudaMemcpyHostToDevice));
+            CK(copy_sync(d.ub, ub.data(), 24 * n, cudaMemcpyHostToDevice));
+            CK(copy_sync(d.force, fo.data(), fo.size() * 8, cudaMemcpyHostToDevice));
+            CK(copy_sync(d.sampled, sa.data(), sa.size() * 8, cudaMemcpyHostToDevice));
+            CK(copy_sync(d.source, s2.data(), 4 * n, cudaMemcpyHostToDevice));
+            CK(copy_sync(d.flagged, f2.data(), n, cudaMemcpyHostToDevice));
         }
     ell_ = ell;
     invalidate_graphs();
+    if (pipeline_on()) build_pipeline();
 }
 
 void Runner::set_variant(int fluid, int ib) {
-    if (fluid < 0 || fluid > 1 || ib < 0 || ib > 1) throw ConfigError("set_variant: fluid and ib variants are 0 or 1");
+    if (fluid < 0 || fluid > 2 || ib < 0 || ib > 1)
+        throw ConfigError("set_variant: fluid variant is 0, 1 or 2 and ib variant 0 or 1");
+    if (fluid == 2 && !pipeline_eligible())
+        throw ConfigError("set_variant: the step pipeline (fluid variant 2) needs one in-process region, "
+                          "nx % 4 == 0, atomic IB accumulation and no tracer emitters");
     variant_ib_ = ib;
     if (fluid != variant_fluid_) {
         variant_fluid_ = fluid;
@@ -1116,8 +1315,9 @@ std::unique_ptr<Runner> Runner::clone() const {
 
 void Runner::copy_state_from(const Runner& o) {
     CK(cudaStreamSynchronize(o.stream()));
-    auto cp = [](void* d, const void* s, size_t b) {
-        if (d && s && b) CK(cudaMemcpy(d, s, b, cudaMemcpyDeviceToDevice));
+    cudaStream_t st = stream();
+    auto cp = [st](void* d, const void* s, size_t b) {
+        if (d && s && b) CK(cudaMemcpyAsync(d, s, b, cudaMemcpyDeviceToDevice, st));
     };
     for (size_t ri = 0; ri < regions_.size(); ++ri) {
         Region& d = regions_[ri];
@@ -1161,6 +1361,7 @@ void Runner::copy_state_from(const Runner& o) {
         tn_ = o.tn_;
         tdead_ = o.tdead_;
     }
+    CK(cudaStreamSynchronize(st));
     t_ = o.t_;
     ext_chunk_t0_ = o.ext_chunk_t0_;
     t_ext_ = o.t_ext_;
@@ -1216,7 +1417,7 @@ void Runner::tracer_prepare_chunk(long t0, long chunk) {
     for (size_t k = 0; same && k < reg.size(); ++k)
         same = reg[k].u == treg_host_[k].u && reg[k].z0 == treg_host_[k].z0 && reg[k].ns == treg_host_[k].ns;
     if (!same) {
-        CK(cudaMemcpy(treg_dev_, reg.data(), sizeof(TracerRegion) * reg.size(), cudaMemcpyHostToDevice));
+        CK(copy_sync(treg_dev_, reg.data(), sizeof(TracerRegion) * reg.size(), cudaMemcpyHostToDevice));
         treg_host_ = reg;
     }
     if (temit_) {
@@ -1235,10 +1436,10 @@ void Runner::tracers(double* pos, int64_t* birth) const {
     if (!has_tracers_ || tn_ == 0) return;
     std::vector<double> x(tn_), y(tn_), z(tn_);
     std::vector<long long> b(tn_);
-    CK(cudaMemcpy(x.data(), tdev_.x, sizeof(double) * tn_, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(y.data(), tdev_.y, sizeof(double) * tn_, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(z.data(), tdev_.z, sizeof(double) * tn_, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(b.data(), tdev_.birth, sizeof(long long) * tn_, cudaMemcpyDeviceToHost));
+    CK(copy_sync(x.data(), tdev_.x, sizeof(double) * tn_, cudaMemcpyDeviceToHost));
+    CK(copy_sync(y.data(), tdev_.y, sizeof(double) * tn_, cudaMemcpyDeviceToHost));
+    CK(copy_sync(z.data(), tdev_.z, sizeof(double) * tn_, cudaMemcpyDeviceToHost));
+    CK(copy_sync(b.data(), tdev_.birth, sizeof(long long) * tn_, cudaMemcpyDeviceToHost));
     size_t w = 0;
     for (size_t p = 0; p < tn_; ++p) {
         if (b[p] < 0) continue;  // tombstone: retired (advect_tracers removes it, order kept)
@@ -1327,7 +1528,7 @@ Status Runner::sync_external() {
     if (has_solids_) {
         fill_motion_table(t_, cap_ + 1, true);
         long long t0d = t_;
-        CK(cudaMemcpy(&ctr_->chunk_t0, &t0d, sizeof t0d, cudaMemcpyHostToDevice));
+        CK(copy_sync(&ctr_->chunk_t0, &t0d, sizeof t0d, cudaMemcpyHostToDevice));
     }
     return status_;
 }

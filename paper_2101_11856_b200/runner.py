@@ -96,6 +96,7 @@ def lib():
         "lbmg_collide_batch": (I, [C.POINTER(_abi.SceneConfigC), SZ, D, D, D, D]),
         "lbmg_runner_kernels_per_step": (C.c_long, [P]),
         "lbmg_runner_sync_interval": (C.c_long, [P]),
+        "lbmg_runner_kernel_launches": (C.c_long, [P]),
         "lbmg_runner_set_cta": (I, [P, I]),
         "lbmg_runner_cta": (I, [P]),
         "lbmg_scene_set_emitters": (I, [P, I, C.POINTER(_abi.EmitterC)]),
@@ -478,6 +479,10 @@ class Runner:
     def sync_interval(self) -> int:
         """Most steps between two sync() calls in an externally driven run."""
         return int(lib().lbmg_runner_sync_interval(self._h))
+
+    def kernel_launches(self) -> int:
+        """Engine kernels launched by advance() so far (graph kernel nodes included)."""
+        return int(lib().lbmg_runner_kernel_launches(self._h))
 
     def kernels_per_step(self) -> int:
         return int(lib().lbmg_runner_kernels_per_step(self._h))
