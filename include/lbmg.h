@@ -185,11 +185,8 @@ int lbmg_runner_region_count(const lbmg_runner* r);
 int lbmg_runner_set_layout(lbmg_runner* r, int block_edge, size_t alpha);
 /* Kernel variants, the launch-split dimension of the tuner (replaces the
  * fixed kSplitBoundary two-pass collision, collision.hpp:58): fluid 0 = the
- * TMA-staged kernel on the ghost layout (one launch per phase), 1 =
- * register-direct kernels on the compact layout, 2 = the step pipeline (the
- * face passes, IB and staged fluid tiles of up to 8 steps in one persistent
- * launch; the default for a single in-process region with atomic IB and no
- * tracers); ib 0 = fused single-region IB kernel, 1 = split pipeline.
+ * TMA-staged kernel on the ghost layout, 1 = register-direct kernels on the
+ * compact layout; ib 0 = fused single-region IB kernel, 1 = split pipeline.
  * Results are identical up to fp32 atomic order in the IB scatter. */
 int lbmg_runner_set_variant(lbmg_runner* r, int fluid, int ib);
 int lbmg_runner_variant(const lbmg_runner* r, int* fluid, int* ib);

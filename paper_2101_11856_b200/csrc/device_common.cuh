@@ -73,7 +73,7 @@ struct RegionGeo {
     unsigned PX, PY, PP;  // row pitch, rows per plane, PX * PY
     unsigned base;        // leading pad (a multiple of 256 slots)
     int cta;              // staged fluid kernel CTA size (0: LBMG_GHOST_THREADS or 512); a tuner dimension
-    int nbuf;             // population buffers: 2 (A/B) or 3 (step pipeline, pipeline.cu)
+    int nbuf;             // population buffers (2: the A/B pair)
     int zwrap;            // the slab is its own z neighbour (one periodic region)
     int has_outflow;      // some face is an outflow face (face slots are read)
     FastDiv div_px, div_py;
@@ -145,7 +145,7 @@ struct ModelConst {
 // for stale outflow), slot[p^1] written; recv[p] = f(t) neighbour halo in;
 // send[p^1] = f(t+1) halo out.
 struct RegionPtrs {
-    float* f[3];  // f(t) lives in f[t % nbuf] (fcur); f[2] only with nbuf == 3
+    float* f[3];  // f(t) lives in f[fcur(t)]
     float* slot[2][6];
     const float* recv_lo[2];
     const float* recv_hi[2];
@@ -166,12 +166,9 @@ struct RegionPtrs {
     unsigned* band_count;  // IB band nodes this step
 };
 
-// Physical population buffer of f(t): nbuf = 2 is the A/B pair; the step
-// pipeline (pipeline.cu) runs step t+1 while step t's tail is still in
-// flight, so it rotates three buffers and f(t) stays intact until step t
-// has completed (the diverging step's f(t) is what the reference keeps).
-LBMG_HD int fcur(const RegionGeo& g, long long t) { return int(t % g.nbuf); }
-LBMG_HD int fnext(const RegionGeo& g, long long t) { return int((t + 1) % g.nbuf); }
+// Physical population buffer of f(t) (the A/B pair: nbuf = 2).
+LBMG_HD int fcur(const RegionGeo& g, long long t) { return g.nbuf == 2 ? int(t & 1) : int(t % g.nbuf); }
+LBMG_HD int fnext(const RegionGeo& g, long long t) { return fcur(g, t + 1); }
 
 struct DevCounters {
     long long t;               // step counter

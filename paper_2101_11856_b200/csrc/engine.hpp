@@ -3,8 +3,6 @@
 
 #include <cuda_runtime.h>
 
-#include <vector>
-
 #include "device_common.cuh"
 
 namespace lbmg {
@@ -36,10 +34,9 @@ struct IbSolidDev {
 // (nbuf parts, like the population buffers).  Step t writes part t % nbuf;
 // the values the reference holds after a run are those of the last step whose
 // IB phase ran, t_ - 1, so readback uses part (t_ - 1) % nbuf: a diverging
-// step's IB output (and, in the step pipeline, that of the step already
-// running ahead of it) lands in another part and is never seen (the
-// reference returns before IB, runner.cpp:154-161).
-constexpr int kIbHalves = 3;
+// step's IB output lands in the other part and is never seen (the reference
+// returns before IB, runner.cpp:154-161).
+constexpr int kIbHalves = 2;
 LBMG_HD size_t ib_half(const IbSolidDev& S, long long t) {
     return size_t(((t % S.nbuf) + S.nbuf) % S.nbuf) * 3 * size_t(S.n);
 }
@@ -102,52 +99,6 @@ struct IbBatch {
 void launch_ib_fused(const FluidParams& P, IbBatch B, unsigned total_blocks, const IbSolidDev* host_solids,
                      cudaStream_t st, bool deterministic = false);
 
-// ---- step pipeline (pipeline.cu) ------------------------------------------
-// One persistent launch runs K whole steps of a single ghost-layout region as
-// one ordered stream of work items — ghost fill of a plane (the six face
-// passes), the IB pass over 64 samples, a staged stream/collide tile — with
-// per-plane dependency counters instead of kernel boundaries.
-constexpr unsigned kPipeItemTile = 0u, kPipeItemFill = 1u, kPipeItemIb = 2u;
-constexpr unsigned kPipeTypeShift = 30u, kPipeSkip = 1u << 29, kPipeIdxMask = (1u << 29) - 1u;
-constexpr unsigned kPipeFillChunk = 8192u;  // ghost-fill entries per fill item
-constexpr unsigned kPipeIbSamples = 64u;    // samples per IB item
-constexpr int kPipeLookahead = 3;           // the fill of a plane is queued this many planes ahead of its tiles
-
-constexpr int kPipeMaxSteps = 64;            // steps per launch
-struct PipeCounters {
-    unsigned ticket;        // next work item (all K steps)
-    unsigned ib_done;       // completed IB items (cumulative over the launch)
-    long long t_launch;     // step counter at launch start
-    unsigned long long div_min;  // first diverging step seen (~0: none)
-    unsigned step_tiles[kPipeMaxSteps];  // completed tiles per step of the launch
-    unsigned plane[2];      // fill_done[nzl] then tile_done[nzl] (cumulative; allocated to size)
-};
-
-struct PipeParams {
-    FluidParams P;
-    IbBatch B;                      // B.n_solids == 0: no IB items
-    const unsigned* ib_item_start;  // per solid prefix of IB items (n_solids + 1)
-    const unsigned* pattern;        // item codes of one step (n_items)
-    const unsigned* fill_desc;      // per fill item: plane, first entry, end entry
-    const unsigned* fill_need;      // fill items per plane (nzl)
-    const unsigned* tile_need;      // tiles touching each plane (nzl)
-    PipeCounters* pc;
-    unsigned n_items, K, n_tiles, n_ib;
-    unsigned org;                   // storage slot of tile 0
-    int macro_j;                    // step of the launch that writes rho*/u* (-1: none)
-    int z0_ib, z1_ib;               // planes the IB support can touch (z0 > z1: none)
-    int dbg;                        // timing probes (LBMG_PIPE_DBG), 0 in production
-};
-
-// host-side tables of the pipeline (pipeline.cu), built once per layout
-struct PipePlan {
-    std::vector<unsigned> pattern, fill_desc, fill_need, tile_need;
-    unsigned n_tiles = 0, n_fill = 0, org = 0;
-};
-PipePlan make_pipe_plan(const RegionGeo& g, unsigned n_ib, int z0_ib, int z1_ib);
-int pipe_tile_slots();  // storage slots per pipeline tile (2 x consumer threads)
-size_t pipe_counter_bytes(const RegionGeo& g);
-void launch_pipeline(const PipeParams& Q, int sm_count, cudaStream_t st);
 // ghost slots of this step: full = every entry (after init / relayout),
 // otherwise only what the previous fluid step did not push
 void launch_ghost_fill(const FluidParams& P, cudaStream_t st, bool full = false);

@@ -189,7 +189,6 @@ Runner::Runner(const lbmg_scene& scene, int regions, int device, int world, int 
     CK(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming));
 
-    if (pipeline_eligible()) variant_fluid_ = 2;  // the step pipeline where it applies
     const int first = rank_mode_ ? rank_ : 0;
     const int count = rank_mode_ ? 1 : m_global_;
     regions_.resize(count);
@@ -221,7 +220,6 @@ Runner::Runner(const lbmg_scene& scene, int regions, int device, int world, int 
     }
     upload_solids();
     init_fields();
-    if (pipeline_on()) build_pipeline();
     if (rank_mode_ && has_solids_) fill_motion_table(0, cap_ + 1, true);
     for (const auto& e : scene_.emitters) {
         if (e.rate < 0) throw ConfigError("tracers: rate must be >= 0");
@@ -273,142 +271,6 @@ void Runner::invalidate_graphs() {
             cudaGraphExecDestroy(g);
             g = nullptr;
         }
-    for (auto& row : pgraph_)
-        for (auto& g : row)
-            if (g) {
-                cudaGraphExecDestroy(g);
-                g = nullptr;
-            }
-}
-
-bool Runner::pipeline_eligible() const {
-    static const bool off = [] {
-        const char* e = std::getenv("LBMG_PIPELINE");
-        return e && std::string(e) == "0";
-    }();
-    return !off && !rank_mode_ && m_global_ == 1 && nx_ % 4 == 0 && ghost_layout_enabled() &&
-           scene_.emitters.empty() && scene_.cfg.ib_mode == LBMG_IB_ATOMIC;
-}
-
-// Tables of the step pipeline for the current layout (make_pipe_plan): the
-// per-step item order, fill chunks, per-plane item counts, IB items per solid
-// and the planes the IB support can touch over the run.
-void Runner::build_pipeline() {
-    Region& r = regions_[0];
-    const RegionGeo& g = r.geo;
-    const size_t ns = scene_.solids.size();
-    std::vector<unsigned> start(ns + 1, 0);
-    for (size_t k = 0; k < ns; ++k)
-        start[k + 1] = start[k] + unsigned((r.solids[k].n + kPipeIbSamples - 1) / kPipeIbSamples);
-    const unsigned n_ib = start[ns];
-    // static solids: their samples' support planes; rotating ones: the
-    // centre +- the largest reference radius (+1); translating ones: anywhere
-    int z0 = g.nzl, z1 = -1;
-    for (const auto& so : scene_.solids) {
-        if (so.samples.size() == 0) continue;
-        double lo = 1e300, hi = -1e300;
-        if (!so.moving) {
-            for (const auto& q : so.samples.positions) {
-                lo = std::min(lo, q.z);
-                hi = std::max(hi, q.z);
-            }
-        } else if (dot(so.linear_velocity, so.linear_velocity) != 0.0) {
-            lo = -1e300;
-            hi = 1e300;
-        } else {
-            double r2 = 0.0;
-            for (const auto& q : so.samples.reference_positions) r2 = std::max(r2, dot(q, q));
-            const double rad = std::sqrt(r2) + 1.0;
-            lo = so.center.z - rad;
-            hi = so.center.z + rad;
-        }
-        auto base = [&](double z) {
-            const double c = std::min(std::max(std::floor(z), 0.0), double(nz_ - 2));
-            return int(c);
-        };
-        z0 = std::min(z0, std::max(0, base(lo) - g.gz0));
-        z1 = std::max(z1, std::min(g.nzl - 1, base(hi) + 1 - g.gz0));
-    }
-    if (n_ib == 0) {
-        z0 = 0;
-        z1 = -1;
-    }
-    const PipePlan pl = make_pipe_plan(g, n_ib, z0, z1);
-    auto upload = [&](unsigned*& dst, const std::vector<unsigned>& v) {
-        dfree(dst);
-        dst = static_cast<unsigned*>(dalloc(sizeof(unsigned) * std::max<size_t>(v.size(), 1), false));
-        if (!v.empty()) CK(copy_sync(dst, v.data(), sizeof(unsigned) * v.size(), cudaMemcpyHostToDevice));
-    };
-    upload(pipe_.pattern, pl.pattern);
-    upload(pipe_.fill_desc, pl.fill_desc);
-    upload(pipe_.fill_need, pl.fill_need);
-    upload(pipe_.tile_need, pl.tile_need);
-    upload(pipe_.ib_start, start);
-    dfree(pipe_.pc);
-    pipe_.pc = static_cast<PipeCounters*>(dalloc(pipe_counter_bytes(g)));
-    pipe_.n_items = unsigned(pl.pattern.size());
-    pipe_.n_tiles = pl.n_tiles;
-    pipe_.n_ib = n_ib;
-    pipe_.org = pl.org;
-    pipe_.z0 = z0;
-    pipe_.z1 = z1;
-    invalidate_graphs();
-}
-
-void Runner::enqueue_pipeline(int K, int macro_j) {
-    Region& r = regions_[0];
-    PipeParams Q{};
-    Q.P = FluidParams{r.geo, faces_, model_, r.ptr, ctr_};
-    if (has_solids_) {
-        const int ns = int(scene_.solids.size());
-        Q.B.solids = r.batch_solids;
-        Q.B.block_start = r.batch_start;
-        Q.B.moving = r.batch_moving;
-        Q.B.n_solids = unsigned(ns);
-        Q.B.table = motion_tab_;
-        Q.B.table_stride = size_t(cap_ + 2) * kMotionRow;
-        Q.B.partial = r.fused_partial;
-        Q.B.done = r.fused_done;
-        Q.B.out_base = totals_dev_;
-        Q.B.out_stride = ns * 6;
-    }
-    Q.ib_item_start = pipe_.ib_start;
-    Q.pattern = pipe_.pattern;
-    Q.fill_desc = pipe_.fill_desc;
-    Q.fill_need = pipe_.fill_need;
-    Q.tile_need = pipe_.tile_need;
-    Q.pc = pipe_.pc;
-    Q.n_items = pipe_.n_items;
-    Q.K = unsigned(K);
-    Q.n_tiles = pipe_.n_tiles;
-    Q.n_ib = pipe_.n_ib;
-    Q.org = pipe_.org;
-    Q.macro_j = macro_j;
-    Q.z0_ib = pipe_.z0;
-    Q.z1_ib = pipe_.z1;
-    static const int dbg = [] {
-        const char* e = std::getenv("LBMG_PIPE_DBG");
-        return e ? std::atoi(e) : 0;
-    }();
-    Q.dbg = dbg;
-    launch_pipeline(Q, sm_count_, stream());
-}
-
-// Pipeline graphs: K steps per launch (1..kPipeSteps), with or without the
-// rho*/u* write on the launch's last step; captured together on first use.
-cudaGraphExec_t Runner::pipeline_graph(int K, bool macro) {
-    cudaGraphExec_t& g = pgraph_[K][macro ? 1 : 0];
-    if (!g) {
-        cudaStream_t st = stream();
-        cudaGraph_t graph;
-        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-        enqueue_pipeline(K, macro ? K - 1 : -1);
-        CK(cudaStreamEndCapture(st, &graph));
-        CK(cudaGraphInstantiate(&g, graph, 0));
-        CK(cudaGraphDestroy(graph));
-        CK(cudaGraphUpload(g, st));
-    }
-    return g;
 }
 
 void Runner::compute_geo(Region& r) const {
@@ -442,8 +304,7 @@ void Runner::compute_geo(Region& r) const {
     g.div_ny = FastDiv(unsigned(ny_));
     g.ghost = 0;
     g.nbuf = 2;
-    if (nx_ % 4 == 0 && ghost_layout_enabled() && (variant_fluid_ == 0 || variant_fluid_ == 2)) {
-        g.nbuf = variant_fluid_ == 2 ? 3 : 2;
+    if (nx_ % 4 == 0 && ghost_layout_enabled() && variant_fluid_ == 0) {
         // ghost-layer layout (device_common.cuh): pitch nx+4, ny+1 rows,
         // planes -1..nzl, CSoA blocks of alpha >= 256 slots (one staged tile
         // writes one contiguous 27 KB block); alpha >= slots is SoA
@@ -845,12 +706,6 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
 // All three are captured and instantiated together on first use.
 void Runner::ensure_graphs() {
     cudaStream_t st = stream();
-    if (pipeline_on()) {
-        for (int K = 1; K <= kPipeSteps; ++K)
-            for (int m = 0; m < 2; ++m) pipeline_graph(K, m != 0);
-        kernels_per_step_ = 2;  // pipeline_begin + pipeline_kernel per launch of up to kPipeSteps steps
-        return;
-    }
     for (int which = 0; which < 3; ++which) {
         cudaGraphExec_t& g = graph_[which];
         if (g) continue;
@@ -909,28 +764,10 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
         if (!written)
             CK(cudaMemcpyAsync(&ctr_->chunk_t0, pinned_up_, sizeof(long long), cudaMemcpyHostToDevice, st));
         std::vector<std::array<cudaEvent_t, 5>> evs;
-        std::vector<std::pair<std::array<cudaEvent_t, 2>, long>> pev;  // pipeline launches (timings)
         // every step graph is captured and instantiated before the first one
         // runs, so no later advance() pays a capture inside its own time
         if (!timings) ensure_graphs();
-        for (long j = 0; pipeline_on() && j < chunk;) {
-            const long K = std::min<long>(kPipeSteps, chunk - j);
-            const bool last = done + j + K == steps;
-            if (last && snap_pending_) CK(cudaStreamWaitEvent(st, snap_done_, 0));
-            if (timings) {
-                std::array<cudaEvent_t, 2> e;
-                for (auto& x : e) CK(cudaEventCreate(&x));
-                CK(cudaEventRecord(e[0], st));
-                enqueue_pipeline(int(K), last ? int(K) - 1 : -1);
-                CK(cudaEventRecord(e[1], st));
-                pev.push_back({e, K});
-            } else {
-                CK(cudaGraphLaunch(pipeline_graph(int(K), last), st));
-            }
-            launches_ += 2;
-            j += K;
-        }
-        for (long j = 0; !pipeline_on() && j < chunk;) {
+        for (long j = 0; j < chunk;) {
             const bool last = done + j == steps - 1;
             if (last && snap_pending_) CK(cudaStreamWaitEvent(st, snap_done_, 0));
             if (timings) {
@@ -957,18 +794,6 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
         CK(cudaStreamSynchronize(st));
         CK(cudaGetLastError());
         downloaded_ = true;
-        if (timings) {  // pipeline: the launch's time spread over its K steps
-            long step = t0;
-            for (auto& [e, K] : pev) {
-                float ms = 0.f;
-                CK(cudaEventElapsedTime(&ms, e[0], e[1]));
-                for (long q = 0; q < K; ++q, ++step) {
-                    timings->push_back({"fluid", step, ms * 1e-3 / double(K)});
-                    timings->push_back({"total", step, ms * 1e-3 / double(K)});
-                }
-                for (auto x : e) cudaEventDestroy(x);
-            }
-        }
         if (timings) {
             for (size_t j = 0; j < evs.size(); ++j) {
                 float seg[4] = {0, 0, 0, 0};
@@ -1246,15 +1071,10 @@ void Runner::set_layout(int ell, size_t alpha) {
         }
     ell_ = ell;
     invalidate_graphs();
-    if (pipeline_on()) build_pipeline();
 }
 
 void Runner::set_variant(int fluid, int ib) {
-    if (fluid < 0 || fluid > 2 || ib < 0 || ib > 1)
-        throw ConfigError("set_variant: fluid variant is 0, 1 or 2 and ib variant 0 or 1");
-    if (fluid == 2 && !pipeline_eligible())
-        throw ConfigError("set_variant: the step pipeline (fluid variant 2) needs one in-process region, "
-                          "nx % 4 == 0, atomic IB accumulation and no tracer emitters");
+    if (fluid < 0 || fluid > 1 || ib < 0 || ib > 1) throw ConfigError("set_variant: fluid and ib variants are 0 or 1");
     variant_ib_ = ib;
     if (fluid != variant_fluid_) {
         variant_fluid_ = fluid;

@@ -69,13 +69,9 @@ public:
     void set_layout(int ell, size_t alpha);
     // Kernel variants (the launch-split dimension of the tuner): fluid 0 =
     // TMA-staged kernel on the ghost layout (needs nx % 4 == 0), 1 =
-    // register-direct kernels on the compact layout, 2 = the step pipeline
-    // (pipeline.cu: ghost fill, IB and staged tiles of several steps in one
-    // persistent launch; single region, atomic IB, no tracers; the default
-    // where it applies); ib 0 = fused single-region IB kernel, 1 = mark /
-    // band / spread / totals pipeline (variants 0 and 1 only).
+    // register-direct kernels on the compact layout; ib 0 = fused single-region
+    // IB kernel, 1 = mark / band / spread / totals pipeline.
     void set_variant(int fluid, int ib);
-    bool pipeline_eligible() const;
     long kernel_launches() const { return launches_; }
     int fluid_variant() const { return variant_fluid_; }
     // CTA size of the staged fluid kernel (512 / 256 / 128 threads = 1024 /
@@ -173,10 +169,6 @@ private:
     void enqueue_fluid(bool write_macro, int part);
     void invalidate_graphs();
     void ensure_graphs();
-    bool pipeline_on() const { return variant_fluid_ == 2; }
-    void build_pipeline();
-    void enqueue_pipeline(int K, int macro_j);
-    cudaGraphExec_t pipeline_graph(int K, bool macro);
     void finish_chunk(long t0, long requested);
     void copy_state_from(const Runner& o);
     void tracer_reserve(unsigned long long need);
@@ -229,19 +221,6 @@ private:
     cudaGraphExec_t graph_[3] = {nullptr, nullptr, nullptr};
     long graph_kernels_[3] = {0, 0, 0};  // kernel nodes per graph launch
     long launches_ = 0;                  // engine kernels launched by advance()
-    // step pipeline (fluid variant 2): device tables of make_pipe_plan
-    struct PipeDev {
-        unsigned* pattern = nullptr;
-        unsigned* fill_desc = nullptr;
-        unsigned* fill_need = nullptr;
-        unsigned* tile_need = nullptr;
-        unsigned* ib_start = nullptr;
-        PipeCounters* pc = nullptr;
-        unsigned n_items = 0, n_tiles = 0, n_ib = 0, org = 0;
-        int z0 = 0, z1 = -1;
-    } pipe_;
-    static constexpr int kPipeSteps = 8;  // steps per pipeline launch
-    cudaGraphExec_t pgraph_[kPipeSteps + 1][2] = {};
 
     long t_ = 0;
     Status status_;

@@ -52,37 +52,6 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity)
         : "memory");
 }
 
-// mbar_wait_parity that gives up: a phase that never completes (a pipeline
-// scheduling bug) traps the launch after ~10 s instead of hanging the device.
-__device__ __forceinline__ void mbar_wait_parity_bounded(uint64_t* bar, unsigned parity) {
-    for (unsigned tries = 0;; ++tries) {
-        unsigned ok;
-        asm volatile(
-            "{\n\t.reg .pred P1;\n\t"
-            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%1], %2, %3;\n\t"
-            "selp.u32 %0, 1, 0, P1;\n}"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity), "r"(10000u)
-            : "memory");
-        if (ok) return;
-        if (tries > (1u << 20)) __trap();
-    }
-}
-
-// Non-blocking probe of an mbarrier phase (true once the phase with this
-// parity has completed).
-__device__ __forceinline__ bool mbar_test_parity(uint64_t* bar, unsigned parity) {
-    unsigned ok;
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 P1, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, P1;\n}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-
 // global -> shared bulk copy; dst/src 16-byte aligned, bytes a multiple of 16.
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
     asm volatile(
