@@ -84,14 +84,18 @@ CONFIGS = {"c2": c2_config, "c3": c3_config, "c1": c1_config, "c4": c4_config, "
 def cpu_sample_config(cfg):
     """The CPU leg's bounded sample of a workload: the whole grid when its FP64
     reference state (488 B/node) fits comfortably in host memory, else a
-    z-slab of it (the solids that intersect the slab are kept)."""
+    z-slab of it (the solids that intersect the slab are kept).  The reference
+    runs its default layout (alpha = 1): the GPU arm's alpha is a device-layout
+    hint, and the reference pads every field to a multiple of alpha (a 2^30
+    alpha would allocate ~230 GB per field; results are layout-invariant)."""
     import copy
     n = cfg.nx * cfg.ny * cfg.nz
     max_nodes = 40_000_000  # ~20 GB of FP64 reference state
-    if n <= max_nodes:
-        return cfg, f"the full {cfg.nx}x{cfg.ny}x{cfg.nz} grid"
-    nz = max(8, max_nodes // (cfg.nx * cfg.ny))
     sub = copy.deepcopy(cfg)
+    sub.alpha = 1
+    if n <= max_nodes:
+        return sub, f"the full {cfg.nx}x{cfg.ny}x{cfg.nz} grid"
+    nz = max(8, max_nodes // (cfg.nx * cfg.ny))
     sub.nz = nz
     keep = []
     for s in sub.solids:
