@@ -301,6 +301,47 @@ int lbmg_runner_tracer_density(const lbmg_runner* r, double* vol);
 int lbmg_rasterize_density(size_t n, const double* positions, int nx, int ny, int nz, int device,
                            double* vol);
 
+/* ---- the reference's free-function surface (unit parity, GPU) ----------- */
+/* step(SimState&, model, boundary, body_force, ctx, pool), solver.hpp:82-83 /
+ * solver.cpp:181-191: one single-region step without solids (stream, six face
+ * passes, moments, collision + forcing, t += 1) on the runner's state.  The
+ * runner must hold one in-process region and no solids (LBMG_ERR_STATE). */
+int lbmg_step(lbmg_runner* r, lbmg_status* status);
+/* The explicit SimState that step() advances (solver.hpp:29-45), canonical
+ * AoS FP64 (nodes*27): f = f(t); f_star = the face-pass scratch whose face
+ * entries seed the persistent face slots the stale outflow-edge reads use
+ * (NULL: f); t = the step counter.  rho*/u* read back as the moments of f
+ * until the next step.  Single in-process region, no solids or tracers. */
+int lbmg_runner_load_state(lbmg_runner* r, const double* f, const double* f_star, long t);
+
+/* The IB free functions of ib.hpp:77-128 on a sample batch, computed on
+ * device 0 in FP64 with the reference's operation order (support,
+ * interpolation, penalty and rigid motion are bit-exact; spreading uses FP64
+ * atomics, the reference's atomic mode; the totals a fixed-order tree).
+ * Sample arrays are AoS Vec3 (n*3); fields canonical AoS over the nx*ny*nz
+ * grid (u: nodes*3, rho: nodes, g: nodes*3); [z0, z1) is the owned slab of
+ * the seam rule (sample_active, ib.cpp:313-317; the whole grid: 0, nz). */
+/* kernel_support, ib.cpp:294-308: base (n*3), w (n*6: wx0 wx1 wy0 wy1 wz0 wz1), inside (n) */
+int lbmg_ib_kernel_support(size_t n, const double* positions, int nx, int ny, int nz, int* base, double* w,
+                           uint8_t* inside);
+/* interpolate_velocity, ib.cpp:321-343: sampled (n*3), flagged (n, may be NULL) */
+int lbmg_ib_interpolate_velocity(size_t n, const double* positions, const double* u, int nx, int ny, int nz,
+                                 int z0, int z1, double* sampled_velocity, uint8_t* flagged);
+/* penalty_forces, ib.cpp:345-365: force = rho(x_s) (u_b - u(x_s)) (flagged may be NULL) */
+int lbmg_ib_penalty_forces(size_t n, const double* positions, const double* boundary_velocity,
+                           const double* sampled_velocity, const uint8_t* flagged, const double* rho, int nx,
+                           int ny, int nz, int z0, int z1, double* penalty_force);
+/* spread_forces, ib.cpp:369-454 (atomic mode): g += the spread forces, owned planes only */
+int lbmg_ib_spread_forces(size_t n, const double* positions, const double* penalty_force, const uint8_t* flagged,
+                          int nx, int ny, int nz, int z0, int z1, double* g);
+/* update_rigid_motion, ib.cpp:456-489: positions, boundary velocities, flags at step t */
+int lbmg_ib_update_rigid_motion(size_t n, const double* reference_positions, const double* linear_velocity,
+                                const double* angular_velocity, const double* center, long t, int nx, int ny,
+                                int nz, double* positions, double* boundary_velocity, uint8_t* flagged);
+/* reaction_totals, ib.cpp:491-501: (F, T) of the samples with z in [z0, z1), torque about center */
+int lbmg_ib_reaction_totals(size_t n, const double* positions, const double* penalty_force, const double* center,
+                            int z0, int z1, double* force_torque);
+
 /* ---- kernel-level entry points (unit parity, GPU) ----------------------- */
 /* collide (collision.cpp:207-212) of n nodes on the device, fp32 arithmetic:
  * f (n*27), rho (n), u (n*3) host FP64 in, omega (n*27) host FP64 out. */

@@ -491,6 +491,140 @@ int ref_stream_and_faces(const lbmg_scene_config* c, const double* f_prev, doubl
     });
 }
 
+// step(SimState&, ...) (solver.hpp:82-83, solver.cpp:181-191) on an explicit
+// single-region state without solids: f, f_star (AoS FP64, nodes*27) in,
+// `steps` steps, then f(t+steps), rho*, u* of the last step out.
+int ref_step(const lbmg_scene_config* c, const double* f, const double* f_star, long t, long steps,
+             double* f_out, double* rho_out, double* u_out, lbmg_status* st) {
+    return guard([&] {
+        SceneConfig cfg = to_cfg(c);
+        const GridDims g = cfg.dims;
+        const std::size_t n = g.n_nodes();
+        SimState s = SimState::make(g, 1);
+        std::memcpy(s.f.data(), f, n * 27 * sizeof(double));
+        std::memcpy(s.f_star.data(), f_star, n * 27 * sizeof(double));
+        s.t = t;
+        DomainContext ctx = DomainContext::single(g, cfg.boundary.axis_periodic(0), cfg.boundary.axis_periodic(1),
+                                                  cfg.boundary.axis_periodic(2));
+        const CollisionModel model = cfg.make_model();
+        ThreadPool pool(1);
+        StepStatus status;
+        for (long k = 0; k < steps; ++k) {
+            status = step(s, model, cfg.boundary, cfg.body_force, ctx, pool);
+            if (!status.ok) break;
+        }
+        std::memcpy(f_out, s.f.data(), n * 27 * sizeof(double));
+        std::memcpy(rho_out, s.rho.data(), n * sizeof(double));
+        std::memcpy(u_out, s.u.data(), n * 3 * sizeof(double));
+        put_status(status, st);
+    });
+}
+
+namespace {
+SolidSampleSet make_set(size_t n, const double* pos, const double* ub, const double* sampled, const double* force,
+                        const uint8_t* flagged) {
+    SolidSampleSet set;
+    set.positions.resize(n);
+    set.reference_positions.assign(n, Vec3{});
+    set.boundary_velocity.assign(n, Vec3{});
+    set.sampled_velocity.assign(n, Vec3{});
+    set.penalty_force.assign(n, Vec3{});
+    set.flagged.assign(n, 0);
+    set.source_id.assign(n, 0);
+    for (std::size_t k = 0; k < n; ++k) {
+        set.positions[k] = v3(pos + 3 * k);
+        if (ub) set.boundary_velocity[k] = v3(ub + 3 * k);
+        if (sampled) set.sampled_velocity[k] = v3(sampled + 3 * k);
+        if (force) set.penalty_force[k] = v3(force + 3 * k);
+        if (flagged) set.flagged[k] = flagged[k];
+    }
+    return set;
+}
+FieldStore field(const double* v, std::size_t nodes, int beta) {
+    FieldStore fs(LayoutParams::make(1, beta, nodes));
+    std::memcpy(fs.data(), v, nodes * beta * sizeof(double));
+    return fs;
+}
+}  // namespace
+
+// The IB free functions (ib.hpp:96-128) on a single-region context; fields are
+// canonical AoS FP64 over the grid, sample arrays AoS Vec3.
+int ref_ib_interpolate_velocity(size_t n, const double* pos, const double* u, int nx, int ny, int nz,
+                                double* sampled, uint8_t* flagged) {
+    return guard([&] {
+        GridDims d{nx, ny, nz};
+        SolidSampleSet set = make_set(n, pos, nullptr, nullptr, nullptr, nullptr);
+        FieldStore fu = field(u, d.n_nodes(), 3);
+        DomainContext ctx = DomainContext::single(d, false, false, false);
+        ThreadPool pool(1);
+        interpolate_velocity(set, fu, ctx, pool);
+        for (std::size_t k = 0; k < n; ++k) {
+            for (int a = 0; a < 3; ++a) sampled[3 * k + a] = set.sampled_velocity[k][a];
+            flagged[k] = set.flagged[k];
+        }
+    });
+}
+
+int ref_ib_penalty_forces(size_t n, const double* pos, const double* ub, const double* sampled,
+                          const uint8_t* flagged, const double* rho, int nx, int ny, int nz, double* force) {
+    return guard([&] {
+        GridDims d{nx, ny, nz};
+        SolidSampleSet set = make_set(n, pos, ub, sampled, nullptr, flagged);
+        FieldStore fr = field(rho, d.n_nodes(), 1);
+        DomainContext ctx = DomainContext::single(d, false, false, false);
+        ThreadPool pool(1);
+        penalty_forces(set, fr, ctx, pool);
+        for (std::size_t k = 0; k < n; ++k)
+            for (int a = 0; a < 3; ++a) force[3 * k + a] = set.penalty_force[k][a];
+    });
+}
+
+int ref_ib_spread_forces(size_t n, const double* pos, const double* force, const uint8_t* flagged, int nx,
+                         int ny, int nz, int deterministic, double* g) {
+    return guard([&] {
+        GridDims d{nx, ny, nz};
+        SolidSampleSet set = make_set(n, pos, nullptr, nullptr, force, flagged);
+        FieldStore fg = field(g, d.n_nodes(), 3);
+        DomainContext ctx = DomainContext::single(d, false, false, false);
+        ThreadPool pool(1);
+        spread_forces(set, fg, ctx, deterministic ? AccumulationMode::Deterministic : AccumulationMode::Atomic, pool);
+        std::memcpy(g, fg.data(), d.n_nodes() * 3 * sizeof(double));
+    });
+}
+
+int ref_ib_update_rigid_motion(size_t n, const double* ref, const double* v, const double* w, const double* c,
+                               long t, int nx, int ny, int nz, double* pos, double* ub, uint8_t* flagged) {
+    return guard([&] {
+        SolidSampleSet set = make_set(n, ref, nullptr, nullptr, nullptr, nullptr);
+        for (std::size_t k = 0; k < n; ++k) set.reference_positions[k] = v3(ref + 3 * k);
+        RigidMotion m;
+        m.linear_velocity = v3(v);
+        m.angular_velocity = v3(w);
+        m.center = v3(c);
+        ThreadPool pool(1);
+        update_rigid_motion(set, m, t, {nx, ny, nz}, pool);
+        for (std::size_t k = 0; k < n; ++k) {
+            for (int a = 0; a < 3; ++a) {
+                pos[3 * k + a] = set.positions[k][a];
+                ub[3 * k + a] = set.boundary_velocity[k][a];
+            }
+            flagged[k] = set.flagged[k];
+        }
+    });
+}
+
+int ref_ib_reaction_totals(size_t n, const double* pos, const double* force, const double* center, int z0, int z1,
+                           double* out6) {
+    return guard([&] {
+        SolidSampleSet set = make_set(n, pos, nullptr, nullptr, force, nullptr);
+        ReactionTotals r = reaction_totals(set, v3(center), z0, z1);
+        for (int a = 0; a < 3; ++a) {
+            out6[a] = r.force[a];
+            out6[3 + a] = r.torque[a];
+        }
+    });
+}
+
 // Gathering oracle (tests/oracles.hpp:121-168) on a sample set with given
 // penalty forces: g (n_nodes*3), loops (n_nodes).
 int ref_gather_forces(size_t n, const double* pos, const double* force, const uint8_t* flagged,

@@ -75,6 +75,12 @@ def ref_lib():
         "ref_face_owner": (None, [CFG, U8P]),
         "ref_reorder_permutation": (I, [SZ, D, U32P, I, U32P]),
         "ref_kernel_support": (I, [D, I, I, I, C.POINTER(I), D]),
+        "ref_step": (I, [CFG, D, D, C.c_long, C.c_long, D, D, D, C.POINTER(_abi.StatusC)]),
+        "ref_ib_interpolate_velocity": (I, [SZ, D, D, I, I, I, D, U8P]),
+        "ref_ib_penalty_forces": (I, [SZ, D, D, D, U8P, D, I, I, I, D]),
+        "ref_ib_spread_forces": (I, [SZ, D, D, U8P, I, I, I, I, D]),
+        "ref_ib_update_rigid_motion": (I, [SZ, D, D, D, D, C.c_long, I, I, I, D, D, U8P]),
+        "ref_ib_reaction_totals": (I, [SZ, D, D, D, I, I, D]),
         "ref_stream_and_faces": (I, [CFG, D, D]),
         "ref_gather_forces": (I, [SZ, D, D, U8P, I, I, I, D, U32P]),
         "ref_tune_spec": (I, [P, I, I, C.POINTER(I), C.POINTER(I), C.POINTER(SZ), SZ, C.POINTER(SZ)]),
@@ -513,3 +519,66 @@ def oracle_split_domain(nz, m):
     if oracle_lib().orc_split_domain(nz, m, buf):
         raise ValueError("bad split")
     return [(buf[2 * r], buf[2 * r + 1]) for r in range(m)]
+
+
+def ref_step(cfg: SceneConfig, f, f_star, t, steps):
+    """lbm::step on an explicit single-region SimState: (f, rho, u, status)."""
+    fa = np.ascontiguousarray(f, dtype=np.float64)
+    fs = np.ascontiguousarray(f_star, dtype=np.float64)
+    n = fa.size // 27
+    fo, ro, uo = np.zeros((n, 27)), np.zeros(n), np.zeros((n, 3))
+    st = _abi.StatusC()
+    _check(ref_lib().ref_step(cfg.to_c().ptr, _dp(fa), _dp(fs), t, steps, _dp(fo), _dp(ro), _dp(uo), C.byref(st)))
+    return fo, ro, uo, {"ok": bool(st.ok), "mach_warning": bool(st.mach_warning), "step": int(st.step),
+                        "reason": st.reason.decode()}
+
+
+def _a3(a):
+    return np.ascontiguousarray(a, dtype=np.float64).reshape(-1, 3)
+
+
+def ref_ib_interpolate_velocity(positions, u, dims):
+    pos = _a3(positions)
+    out = np.zeros((len(pos), 3))
+    fl = np.zeros(len(pos), dtype=np.uint8)
+    _check(ref_lib().ref_ib_interpolate_velocity(len(pos), _dp(pos), _dp(np.ascontiguousarray(u, dtype=np.float64)),
+                                                 *dims, _dp(out), _u8(fl)))
+    return out, fl
+
+
+def ref_ib_penalty_forces(positions, ub, sampled, flagged, rho, dims):
+    pos = _a3(positions)
+    out = np.zeros((len(pos), 3))
+    _check(ref_lib().ref_ib_penalty_forces(len(pos), _dp(pos), _dp(_a3(ub)), _dp(_a3(sampled)),
+                                           _u8(np.ascontiguousarray(flagged, dtype=np.uint8)),
+                                           _dp(np.ascontiguousarray(rho, dtype=np.float64)), *dims, _dp(out)))
+    return out
+
+
+def ref_ib_spread_forces(positions, force, flagged, g, dims, deterministic=False):
+    pos = _a3(positions)
+    out = np.array(g, dtype=np.float64, copy=True, order="C").reshape(-1, 3)
+    _check(ref_lib().ref_ib_spread_forces(len(pos), _dp(pos), _dp(_a3(force)),
+                                          _u8(np.ascontiguousarray(flagged, dtype=np.uint8)), *dims,
+                                          int(deterministic), _dp(out)))
+    return out
+
+
+def ref_ib_update_rigid_motion(reference_positions, motion, t, dims):
+    ref = _a3(reference_positions)
+    n = len(ref)
+    pos, ub, fl = np.zeros((n, 3)), np.zeros((n, 3)), np.zeros(n, dtype=np.uint8)
+    v = np.ascontiguousarray(motion.linear_velocity, dtype=np.float64)
+    w = np.ascontiguousarray(motion.angular_velocity, dtype=np.float64)
+    c = np.ascontiguousarray(motion.center, dtype=np.float64)
+    _check(ref_lib().ref_ib_update_rigid_motion(n, _dp(ref), _dp(v), _dp(w), _dp(c), t, *dims, _dp(pos), _dp(ub),
+                                                _u8(fl)))
+    return pos, ub, fl
+
+
+def ref_ib_reaction_totals(positions, force, center, z0, z1):
+    out = np.zeros(6)
+    pos = _a3(positions)
+    _check(ref_lib().ref_ib_reaction_totals(len(pos), _dp(pos), _dp(_a3(force)),
+                                            _dp(np.ascontiguousarray(center, dtype=np.float64)), z0, z1, _dp(out)))
+    return out[:3], out[3:]

@@ -11,7 +11,8 @@ from .scene import (ConfigError, FaceSpec, MeshConfig, RigidMotion, SceneConfig,
                     load_scene_config, parse_scene_config)
 from .runner import (CudaError, Runner, Scene, StateError, StepStatus, TimingRow, build_scene,
                      collide_batch, device_count, dump_field, emit_tracers, lib, model_rates, morton3, rasterize_density,
-                     reorder_permutation, split_domain, TracerCloud)
+                     reorder_permutation, split_domain, TracerCloud, ib_kernel_support, ib_interpolate_velocity,
+                     ib_penalty_forces, ib_spread_forces, ib_update_rigid_motion, ib_reaction_totals)
 
 from . import autotune
 from .autotune import TuneOutcome, TuneSpec
@@ -22,5 +23,6 @@ __all__ = [
     "load_scene_config", "parse_scene_config", "CudaError", "Runner", "Scene", "StateError",
     "StepStatus", "TimingRow", "build_scene", "collide_batch", "device_count", "dump_field", "lib", "model_rates",
     "morton3", "reorder_permutation", "split_domain", "TracerEmitter", "TracerCloud", "emit_tracers",
-    "rasterize_density",
+    "rasterize_density", "ib_kernel_support", "ib_interpolate_velocity", "ib_penalty_forces", "ib_spread_forces",
+    "ib_update_rigid_motion", "ib_reaction_totals",
 ]

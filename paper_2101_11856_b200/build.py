@@ -25,7 +25,7 @@ COMMON = [
     "-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
     f"-I{ROOT / 'include'}", f"-I{CSRC}",
 ]
-SOURCES = ["fluid.cu", "kernels.cu", "tracers.cu", "scene.cpp", "runner.cpp", "capi.cpp"]
+SOURCES = ["fluid.cu", "kernels.cu", "ib_free.cu", "tracers.cu", "scene.cpp", "runner.cpp", "capi.cpp"]
 
 
 def _obj(src: str) -> Path:

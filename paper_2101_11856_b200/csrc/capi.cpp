@@ -519,6 +519,188 @@ long lbmg_runner_kernels_per_step(const lbmg_runner* r) {
     return r && r->impl ? r->impl->kernels_per_step_ : 0;
 }
 
+int lbmg_step(lbmg_runner* r, lbmg_status* status) {
+    return guarded([&] { put_status(R(r).step_once(), status); });
+}
+
+int lbmg_runner_load_state(lbmg_runner* r, const double* f, const double* f_star, long t) {
+    return guarded([&] {
+        if (!f) throw lbmg::ConfigError("load_state: f is required");
+        R(r).load_state(f, f_star, t);
+    });
+}
+
+extern "C++" {
+namespace {
+
+// Device scratch for the IB free functions: every buffer on one stream,
+// freed on scope exit; uploads/downloads complete before returning.
+struct Scratch {
+    cudaStream_t st = nullptr;
+    std::vector<void*> bufs;
+    explicit Scratch(int device) {
+        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+    }
+    ~Scratch() {
+        if (st) cudaStreamSynchronize(st);
+        for (void* p : bufs) cudaFree(p);
+        if (st) cudaStreamDestroy(st);
+    }
+    template <class T>
+    T* alloc(size_t count) {
+        void* p = nullptr;
+        if (cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1)) != cudaSuccess) {
+            cudaGetLastError();
+            throw OomError("IB free function: device allocation failed");
+        }
+        bufs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    template <class T>
+    T* up(const T* h, size_t count) {
+        T* d = alloc<T>(count);
+        if (count) cuda_check(cudaMemcpyAsync(d, h, sizeof(T) * count, cudaMemcpyHostToDevice, st), "upload");
+        return d;
+    }
+    template <class T>
+    void down(T* h, const T* d, size_t count) {
+        if (count) cuda_check(cudaMemcpyAsync(h, d, sizeof(T) * count, cudaMemcpyDeviceToHost, st), "download");
+    }
+    void sync() {
+        cuda_check(cudaGetLastError(), "IB free function launch");
+        cuda_check(cudaStreamSynchronize(st), "IB free function");
+    }
+};
+
+void check_grid(int nx, int ny, int nz) {
+    if (nx < 2 || ny < 2 || nz < 2) throw lbmg::ConfigError("grid: every extent must be >= 2");
+}
+
+void check_slab(int nz, int z0, int z1) {
+    if (z0 < 0 || z1 > nz || z0 >= z1) throw lbmg::ConfigError("slab: 0 <= z0 < z1 <= nz");
+}
+
+}  // namespace
+}  // extern "C++"
+
+
+int lbmg_ib_kernel_support(size_t n, const double* pos, int nx, int ny, int nz, int* base, double* w,
+                           uint8_t* inside) {
+    return guarded([&] {
+        check_grid(nx, ny, nz);
+        Scratch S(0);
+        const double* dp = S.up(pos, 3 * n);
+        int* db = S.alloc<int>(3 * n);
+        double* dw = S.alloc<double>(6 * n);
+        unsigned char* di = S.alloc<unsigned char>(n);
+        launch_ib_support_batch(n, dp, nx, ny, nz, db, dw, di, S.st);
+        if (base) S.down(base, db, 3 * n);
+        if (w) S.down(w, dw, 6 * n);
+        if (inside) S.down(inside, di, n);
+        S.sync();
+    });
+}
+
+int lbmg_ib_interpolate_velocity(size_t n, const double* pos, const double* u, int nx, int ny, int nz, int z0,
+                                 int z1, double* sampled, uint8_t* flagged) {
+    return guarded([&] {
+        check_grid(nx, ny, nz);
+        check_slab(nz, z0, z1);
+        const size_t nodes = size_t(nx) * ny * nz;
+        Scratch S(0);
+        const double* dp = S.up(pos, 3 * n);
+        const double* du = S.up(u, 3 * nodes);
+        double* ds = S.alloc<double>(3 * n);
+        unsigned char* df = S.alloc<unsigned char>(n);
+        launch_ib_interp_batch(n, dp, du, nx, ny, nz, z0, z1, ds, df, S.st);
+        S.down(sampled, ds, 3 * n);
+        if (flagged) S.down(flagged, df, n);
+        S.sync();
+    });
+}
+
+int lbmg_ib_penalty_forces(size_t n, const double* pos, const double* boundary_velocity,
+                           const double* sampled_velocity, const uint8_t* flagged, const double* rho, int nx, int ny,
+                           int nz, int z0, int z1, double* penalty_force) {
+    return guarded([&] {
+        check_grid(nx, ny, nz);
+        check_slab(nz, z0, z1);
+        const size_t nodes = size_t(nx) * ny * nz;
+        Scratch S(0);
+        const double* dp = S.up(pos, 3 * n);
+        const double* dub = S.up(boundary_velocity, 3 * n);
+        const double* dsa = S.up(sampled_velocity, 3 * n);
+        std::vector<unsigned char> zeros;
+        if (!flagged) zeros.assign(n, 0);
+        const unsigned char* dfl = S.up(flagged ? flagged : zeros.data(), n);
+        const double* dr = S.up(rho, nodes);
+        double* dfo = S.alloc<double>(3 * n);
+        launch_ib_penalty_batch(n, dp, dub, dsa, dfl, dr, nx, ny, nz, z0, z1, dfo, S.st);
+        S.down(penalty_force, dfo, 3 * n);
+        S.sync();
+    });
+}
+
+int lbmg_ib_spread_forces(size_t n, const double* pos, const double* penalty_force, const uint8_t* flagged, int nx,
+                          int ny, int nz, int z0, int z1, double* g) {
+    return guarded([&] {
+        check_grid(nx, ny, nz);
+        check_slab(nz, z0, z1);
+        const size_t nodes = size_t(nx) * ny * nz;
+        Scratch S(0);
+        const double* dp = S.up(pos, 3 * n);
+        const double* dfo = S.up(penalty_force, 3 * n);
+        std::vector<unsigned char> zeros;
+        if (!flagged) zeros.assign(n, 0);
+        const unsigned char* dfl = S.up(flagged ? flagged : zeros.data(), n);
+        double* dg = S.up(g, 3 * nodes);
+        launch_ib_spread_batch(n, dp, dfo, dfl, nx, ny, nz, z0, z1, dg, S.st);
+        S.down(g, dg, 3 * nodes);
+        S.sync();
+    });
+}
+
+int lbmg_ib_update_rigid_motion(size_t n, const double* reference_positions, const double* linear_velocity,
+                                const double* angular_velocity, const double* center, long t, int nx, int ny, int nz,
+                                double* pos, double* boundary_velocity, uint8_t* flagged) {
+    return guarded([&] {
+        check_grid(nx, ny, nz);
+        // centre(t) and Rodrigues R(t) on the host with the reference's
+        // expressions (ib.cpp:456-475, glibc cos/sin): bit-exact positions
+        const V3 v{linear_velocity[0], linear_velocity[1], linear_velocity[2]};
+        const V3 w{angular_velocity[0], angular_velocity[1], angular_velocity[2]};
+        const V3 c0{center[0], center[1], center[2]};
+        double row[kMotionRow];
+        motion_table_row(v, w, c0, t, row);
+        Scratch S(0);
+        const double* dref = S.up(reference_positions, 3 * n);
+        const double* drow = S.up(row, kMotionRow);
+        double* dp = S.alloc<double>(3 * n);
+        double* dub = S.alloc<double>(3 * n);
+        unsigned char* dfl = S.alloc<unsigned char>(n);
+        launch_ib_motion_batch(n, dref, drow, nx, ny, nz, dp, dub, dfl, S.st);
+        S.down(pos, dp, 3 * n);
+        S.down(boundary_velocity, dub, 3 * n);
+        if (flagged) S.down(flagged, dfl, n);
+        S.sync();
+    });
+}
+
+int lbmg_ib_reaction_totals(size_t n, const double* pos, const double* penalty_force, const double* center, int z0,
+                            int z1, double* force_torque) {
+    return guarded([&] {
+        Scratch S(0);
+        const double* dp = S.up(pos, 3 * n);
+        const double* dfo = S.up(penalty_force, 3 * n);
+        double* partial = S.alloc<double>(6 * size_t(ib_totals_batch_blocks(n)));
+        double* dout = S.alloc<double>(6);
+        launch_ib_totals_batch(n, dp, dfo, center, z0, z1, partial, dout, S.st);
+        S.down(force_torque, dout, 6);
+        S.sync();
+    });
+}
+
 int lbmg_collide_batch(const lbmg_scene_config* cfg, size_t n, const double* f, const double* rho,
                        const double* u, double* omega) {
     return guarded([&] {

@@ -119,6 +119,25 @@ void launch_cell_flags(const FluidParams& P, unsigned k0, unsigned k1, unsigned 
                        cudaStream_t st);
 void launch_relayout(const float* src, float* dst, const RegionGeo& gs, const RegionGeo& gd,
                      cudaStream_t st);
+// the IB free functions on sample batches (ib_free.cu)
+void launch_ib_support_batch(size_t n, const double* pos, int nx, int ny, int nz, int* base, double* w,
+                             unsigned char* inside, cudaStream_t st);
+void launch_ib_interp_batch(size_t n, const double* pos, const double* u, int nx, int ny, int nz, int z0, int z1,
+                            double* sampled, unsigned char* flagged, cudaStream_t st);
+void launch_ib_penalty_batch(size_t n, const double* pos, const double* ub, const double* sampled,
+                             const unsigned char* flagged, const double* rho, int nx, int ny, int nz, int z0, int z1,
+                             double* force, cudaStream_t st);
+void launch_ib_spread_batch(size_t n, const double* pos, const double* force, const unsigned char* flagged, int nx,
+                            int ny, int nz, int z0, int z1, double* g, cudaStream_t st);
+void launch_ib_motion_batch(size_t n, const double* ref, const double* row, int nx, int ny, int nz, double* pos,
+                            double* ub, unsigned char* flagged, cudaStream_t st);
+int ib_totals_batch_blocks(size_t n);
+void launch_ib_totals_batch(size_t n, const double* pos, const double* force, const double* center, int z0, int z1,
+                            double* partial, double* out, cudaStream_t st);
+// load a canonical AoS FP64 state: f (nodes*27) into buffer `buffer`, and the
+// persistent face slots of parity p from f_star (nodes*27)
+void launch_write_f(const FluidParams& P, int buffer, int parity, const double* f, cudaStream_t st);
+void launch_write_slots(const FluidParams& P, int parity, const double* f_star, cudaStream_t st);
 void launch_collide_batch(const ModelConst& m, unsigned n, const double* f, const double* rho,
                           const double* u, double* omega, cudaStream_t st);
 

@@ -506,6 +506,54 @@ __global__ void read_macro_kernel(const FluidParams P, unsigned k0, unsigned k1,
         for (int a = 0; a < 3; ++a) u[size_t(k - k0) * 3 + a] = double(P.p.u[k + a * g.ns]);
 }
 
+// Canonical AoS FP64 state -> device (Runner::load_state): f of every node
+// (DDF-shifted fp32, the readback's inverse) and rho/u as plain moments of f.
+__global__ void write_f_kernel(const FluidParams P, int buffer, int parity, const double* f) {
+    const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+    const RegionGeo& g = P.g;
+    if (k >= g.n) return;
+    float* fb = P.p.f[buffer];
+    double r = 0.0, m[3] = {0.0, 0.0, 0.0};
+    for (int i = 0; i < 27; ++i) {
+        const double v = f[size_t(k) * 27 + i];
+        fb[g.idx(k, i)] = float(v - weight_d(i));
+        r += v;
+        m[0] += cx(i) * v;
+        m[1] += cy(i) * v;
+        m[2] += cz(i) * v;
+    }
+    P.p.rho[k] = float(r);
+    for (int a = 0; a < 3; ++a) P.p.u[k + a * g.ns] = float(m[a] / r);
+    // the boundary planes' crossing populations into the halos step t reads
+    int x, y, lz;
+    decode(g, k, x, y, lz);
+    const unsigned hp = unsigned(y) * g.nx + x;
+    if (lz == 0 && P.p.send_lo[parity])
+        for (int i = 1; i <= 9; ++i) P.p.send_lo[parity][cross9(i, 2) * g.plane + hp] = fb[g.idx(k, i)];
+    if (lz == g.nzl - 1 && P.p.send_hi[parity])
+        for (int i = 18; i <= 26; ++i) P.p.send_hi[parity][cross9(i, 2) * g.plane + hp] = fb[g.idx(k, i)];
+}
+
+// f_star of the face nodes -> the persistent face slots of one parity (the
+// values the outflow stale-edge reads see)
+__global__ void write_slots_kernel(const FluidParams P, int parity, const double* f_star) {
+    const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+    const RegionGeo& g = P.g;
+    if (k >= g.n) return;
+    int x, y, lz;
+    decode(g, k, x, y, lz);
+    const int gz = g.gz0 + lz;
+    for (int f = 0; f < 6; ++f) {
+        float* sl = P.p.slot[parity][f];
+        if (!sl) continue;
+        const int a = face_axis(f), sd = face_side(f);
+        const int coord = a == 0 ? x : (a == 1 ? y : gz);
+        if (coord != (sd < 0 ? 0 : g.extent(a) - 1)) continue;
+        for (int i = 0; i < 27; ++i)
+            if (cc(i, a) == -sd) sl[g.slot_index(f, x, y, lz, i)] = float(f_star[size_t(k) * 27 + i] - weight_d(i));
+    }
+}
+
 // Cell flags: owner face per (node, direction).
 __global__ void cell_flags_kernel(const FluidParams P, unsigned k0, unsigned k1, unsigned char* out) {
     const unsigned k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
@@ -643,6 +691,14 @@ void launch_read_f(const FluidParams& P, int buffer, unsigned k0, unsigned k1, d
 
 void launch_read_macro(const FluidParams& P, unsigned k0, unsigned k1, double* rho, double* u, cudaStream_t st) {
     if (k1 > k0) read_macro_kernel<<<blocks_for(k1 - k0, 256), 256, 0, st>>>(P, k0, k1, rho, u);
+}
+
+void launch_write_f(const FluidParams& P, int buffer, int parity, const double* f, cudaStream_t st) {
+    write_f_kernel<<<blocks_for(P.g.n, 256), 256, 0, st>>>(P, buffer, parity, f);
+}
+
+void launch_write_slots(const FluidParams& P, int parity, const double* f_star, cudaStream_t st) {
+    write_slots_kernel<<<blocks_for(P.g.n, 256), 256, 0, st>>>(P, parity, f_star);
 }
 
 void launch_cell_flags(const FluidParams& P, unsigned k0, unsigned k1, unsigned char* out, cudaStream_t st) {

@@ -492,32 +492,7 @@ void Runner::upload_solids() {
 // computed on the host with the reference's expressions (glibc cos/sin).
 void Runner::motion_row(int solid, long t, double* row) const {
     const SolidInstance& s = scene_.solids[solid];
-    const double td = double(t);
-    const V3 center = s.center + s.linear_velocity * td;
-    const double wn = std::sqrt(dot(s.angular_velocity, s.angular_velocity));
-    double R[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
-    if (wn > 0.0) {
-        const V3 ax = s.angular_velocity * (1.0 / wn);
-        const double th = wn * td, ct = std::cos(th), st = std::sin(th), vt = 1.0 - ct;
-        R[0][0] = ct + ax.x * ax.x * vt;
-        R[0][1] = ax.x * ax.y * vt - ax.z * st;
-        R[0][2] = ax.x * ax.z * vt + ax.y * st;
-        R[1][0] = ax.y * ax.x * vt + ax.z * st;
-        R[1][1] = ct + ax.y * ax.y * vt;
-        R[1][2] = ax.y * ax.z * vt - ax.x * st;
-        R[2][0] = ax.z * ax.x * vt - ax.y * st;
-        R[2][1] = ax.z * ax.y * vt + ax.x * st;
-        R[2][2] = ct + ax.z * ax.z * vt;
-    }
-    row[0] = center.x;
-    row[1] = center.y;
-    row[2] = center.z;
-    for (int a = 0; a < 3; ++a)
-        for (int b = 0; b < 3; ++b) row[3 + 3 * a + b] = R[a][b];
-    for (int a = 0; a < 3; ++a) {
-        row[12 + a] = s.linear_velocity[a];
-        row[15 + a] = s.angular_velocity[a];
-    }
+    motion_table_row(s.linear_velocity, s.angular_velocity, s.center, t, row);
 }
 
 // Motion rows of steps t0 .. t0+rows-1, solid-major ([solid][step][row]: the
@@ -868,6 +843,44 @@ void Runner::finish_chunk(long t0, long) {
         }
         CK(cudaStreamSynchronize(stream()));
     }
+}
+
+Status Runner::step_once() {
+    if (regions_.size() != 1 || rank_mode_ || has_solids_)
+        throw StateError("step(): a single region without solids (solver.hpp:82-83; the Runner orchestrates the rest)");
+    return advance(1, nullptr);
+}
+
+void Runner::load_state(const double* f, const double* f_star, long t) {
+    if (regions_.size() != 1 || rank_mode_ || has_solids_ || has_tracers_)
+        throw StateError("load_state: a single in-process region without solids or tracers");
+    if (t < 0) throw ConfigError("load_state: the step counter must be >= 0");
+    CK(cudaSetDevice(device_));
+    Region& r = regions_[0];
+    const size_t bytes = sizeof(double) * 27 * size_t(r.geo.n);
+    double* d = static_cast<double*>(dalloc(bytes, false));
+    try {
+        DevCounters h{};
+        h.t = t;
+        CK(copy_sync(ctr_, &h, sizeof h, cudaMemcpyHostToDevice));
+        FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+        CK(copy_sync(d, f_star ? f_star : f, bytes, cudaMemcpyHostToDevice));
+        for (int p = 0; p < 2; ++p) launch_write_slots(P, p, d, stream());
+        CK(cudaStreamSynchronize(stream()));
+        CK(copy_sync(d, f, bytes, cudaMemcpyHostToDevice));
+        launch_write_f(P, fcur(r.geo, t), int(t & 1), d, stream());
+        CK(cudaStreamSynchronize(stream()));
+    } catch (...) {
+        dfree(d);
+        throw;
+    }
+    dfree(d);
+    t_ = t;
+    status_ = Status{};
+    totals_.clear();
+    fill_ghosts_full();
+    CK(cudaStreamSynchronize(stream()));
+    CK(cudaGetLastError());
 }
 
 void Runner::slab(int* z0, int* z1) const {

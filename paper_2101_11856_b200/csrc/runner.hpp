@@ -62,6 +62,14 @@ public:
     std::unique_ptr<Runner> clone() const;
 
     Status advance(long steps, std::vector<Timing>* timings);
+    // step(SimState&, ...) (solver.hpp:82-83): one single-region step without
+    // solids, on the state load_state set (or the one advance left)
+    Status step_once();
+    // SimState of a single-region runner without solids (solver.hpp:29-45):
+    // f(t) and the face-pass scratch f_star (its face entries seed the
+    // persistent face slots the stale outflow reads use; nullptr: f) as
+    // canonical AoS FP64, and the step counter t
+    void load_state(const double* f, const double* f_star, long t);
     long step_count() const { return t_; }
     const Status& status() const { return status_; }
     int region_count() const { return int(regions_.size()); }

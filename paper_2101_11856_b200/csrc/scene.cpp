@@ -454,4 +454,36 @@ void validate_config(const lbmg_scene_config& c) {
     make_rates(c);
 }
 
+// Rigid motion row of step t (ib.cpp:456-475): centre(t), Rodrigues R(t)
+// with the reference's expressions (glibc cos/sin), v, omega.
+void motion_table_row(const V3& linear_velocity, const V3& angular_velocity, const V3& center0, long t,
+                      double* row) {
+    const double td = double(t);
+    const V3 center = center0 + linear_velocity * td;
+    const double wn = std::sqrt(dot(angular_velocity, angular_velocity));
+    double R[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+    if (wn > 0.0) {
+        const V3 ax = angular_velocity * (1.0 / wn);
+        const double th = wn * td, ct = std::cos(th), st = std::sin(th), vt = 1.0 - ct;
+        R[0][0] = ct + ax.x * ax.x * vt;
+        R[0][1] = ax.x * ax.y * vt - ax.z * st;
+        R[0][2] = ax.x * ax.z * vt + ax.y * st;
+        R[1][0] = ax.y * ax.x * vt + ax.z * st;
+        R[1][1] = ct + ax.y * ax.y * vt;
+        R[1][2] = ax.y * ax.z * vt - ax.x * st;
+        R[2][0] = ax.z * ax.x * vt - ax.y * st;
+        R[2][1] = ax.z * ax.y * vt + ax.x * st;
+        R[2][2] = ct + ax.z * ax.z * vt;
+    }
+    row[0] = center.x;
+    row[1] = center.y;
+    row[2] = center.z;
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) row[3 + 3 * a + b] = R[a][b];
+    for (int a = 0; a < 3; ++a) {
+        row[12 + a] = linear_velocity[a];
+        row[15 + a] = angular_velocity[a];
+    }
+}
+
 }  // namespace lbmg

@@ -86,6 +86,11 @@ struct SolidInstance {
     SamplingReport report;
 };
 
+// Rigid motion row of step t (ib.cpp:456-475): centre(t)[3], R(t)[9], v[3],
+// omega[3] (kMotionRow doubles), computed with the reference's expressions.
+void motion_table_row(const V3& linear_velocity, const V3& angular_velocity, const V3& center0, long t,
+                      double* row);
+
 }  // namespace lbmg
 
 struct lbmg_scene {

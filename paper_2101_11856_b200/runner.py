@@ -94,6 +94,14 @@ def lib():
         "lbmg_runner_phase": (I, [P, I, I]),
         "lbmg_runner_sync": (I, [P, C.POINTER(_abi.StatusC)]),
         "lbmg_collide_batch": (I, [C.POINTER(_abi.SceneConfigC), SZ, D, D, D, D]),
+        "lbmg_step": (I, [P, C.POINTER(_abi.StatusC)]),
+        "lbmg_runner_load_state": (I, [P, D, D, C.c_long]),
+        "lbmg_ib_kernel_support": (I, [SZ, D, I, I, I, C.POINTER(I), D, U8P]),
+        "lbmg_ib_interpolate_velocity": (I, [SZ, D, D, I, I, I, I, I, D, U8P]),
+        "lbmg_ib_penalty_forces": (I, [SZ, D, D, D, U8P, D, I, I, I, I, I, D]),
+        "lbmg_ib_spread_forces": (I, [SZ, D, D, U8P, I, I, I, I, I, D]),
+        "lbmg_ib_update_rigid_motion": (I, [SZ, D, D, D, D, C.c_long, I, I, I, D, D, U8P]),
+        "lbmg_ib_reaction_totals": (I, [SZ, D, D, D, I, I, D]),
         "lbmg_runner_kernels_per_step": (C.c_long, [P]),
         "lbmg_runner_sync_interval": (C.c_long, [P]),
         "lbmg_runner_kernel_launches": (C.c_long, [P]),
@@ -316,6 +324,21 @@ class Runner:
                 timings.append(TimingRow(rows[k].phase.decode(), rows[k].step, rows[k].seconds))
         return StepStatus._from(st)
 
+    def step(self) -> StepStatus:
+        """step(SimState&, ...) (solver.hpp:82-83): one single-region step without solids."""
+        st = _abi.StatusC()
+        _check(lib().lbmg_step(self._h, C.byref(st)))
+        return StepStatus._from(st)
+
+    def load_state(self, f, f_star=None, t: int = 0):
+        """The explicit SimState step() advances: f(t) (nodes x 27, FP64 AoS), the
+        face-pass scratch f_star (seeds the persistent face slots; None: f), t."""
+        fa = np.ascontiguousarray(f, dtype=np.float64)
+        fs = None if f_star is None else np.ascontiguousarray(f_star, dtype=np.float64)
+        if fa.size != self._n_local() * 27 or (fs is not None and fs.size != fa.size):
+            raise ConfigError("load_state: f and f_star hold nodes x 27 values")
+        _check(lib().lbmg_runner_load_state(self._h, _dp(fa), None if fs is None else _dp(fs), t))
+
     def step_count(self) -> int:
         return int(lib().lbmg_runner_step_count(self._h))
 
@@ -502,3 +525,87 @@ def collide_batch(cfg: SceneConfig, f: np.ndarray, rho: np.ndarray, u: np.ndarra
     cs = cfg.to_c()
     _check(lib().lbmg_collide_batch(cs.ptr, len(rho), _dp(f), _dp(rho), _dp(u), _dp(out)))
     return out
+
+
+# ---- the IB free functions (ib.hpp:77-128) on the device ------------------
+
+def _v3(a):
+    return np.ascontiguousarray(a, dtype=np.float64).reshape(-1, 3)
+
+
+def _dims3(dims):
+    nx, ny, nz = (int(v) for v in dims)
+    return nx, ny, nz
+
+
+def ib_kernel_support(positions, dims):
+    """kernel_support (ib.cpp:294-308) per sample: (base (n,3) int32, w (n,6), inside (n,) bool)."""
+    pos = _v3(positions)
+    n = len(pos)
+    base = np.zeros((n, 3), dtype=np.int32)
+    w = np.zeros((n, 6))
+    inside = np.zeros(n, dtype=np.uint8)
+    _check(lib().lbmg_ib_kernel_support(n, _dp(pos), *_dims3(dims), base.ctypes.data_as(C.POINTER(C.c_int)), _dp(w),
+                                        _u8(inside)))
+    return base, w, inside.astype(bool)
+
+
+def ib_interpolate_velocity(positions, u, dims, slab=None):
+    """interpolate_velocity (ib.cpp:321-343): (sampled (n,3), flagged (n,) uint8)."""
+    pos = _v3(positions)
+    uu = np.ascontiguousarray(u, dtype=np.float64)
+    nx, ny, nz = _dims3(dims)
+    z0, z1 = slab or (0, nz)
+    out = np.zeros((len(pos), 3))
+    fl = np.zeros(len(pos), dtype=np.uint8)
+    _check(lib().lbmg_ib_interpolate_velocity(len(pos), _dp(pos), _dp(uu), nx, ny, nz, z0, z1, _dp(out), _u8(fl)))
+    return out, fl
+
+
+def ib_penalty_forces(positions, boundary_velocity, sampled_velocity, flagged, rho, dims, slab=None):
+    """penalty_forces (ib.cpp:345-365): rho(x_s) (u_b - u(x_s)), (n,3)."""
+    pos = _v3(positions)
+    ub, us = _v3(boundary_velocity), _v3(sampled_velocity)
+    fl = np.ascontiguousarray(flagged, dtype=np.uint8)
+    r = np.ascontiguousarray(rho, dtype=np.float64)
+    nx, ny, nz = _dims3(dims)
+    z0, z1 = slab or (0, nz)
+    out = np.zeros((len(pos), 3))
+    _check(lib().lbmg_ib_penalty_forces(len(pos), _dp(pos), _dp(ub), _dp(us), _u8(fl), _dp(r), nx, ny, nz, z0, z1,
+                                        _dp(out)))
+    return out
+
+
+def ib_spread_forces(positions, penalty_force, flagged, g, dims, slab=None):
+    """spread_forces (ib.cpp:369-454, atomic mode): returns g + the spread forces (nodes,3)."""
+    pos = _v3(positions)
+    fo = _v3(penalty_force)
+    fl = np.ascontiguousarray(flagged, dtype=np.uint8)
+    out = np.array(g, dtype=np.float64, copy=True, order="C").reshape(-1, 3)
+    nx, ny, nz = _dims3(dims)
+    z0, z1 = slab or (0, nz)
+    _check(lib().lbmg_ib_spread_forces(len(pos), _dp(pos), _dp(fo), _u8(fl), nx, ny, nz, z0, z1, _dp(out)))
+    return out
+
+
+def ib_update_rigid_motion(reference_positions, motion, t, dims):
+    """update_rigid_motion (ib.cpp:456-489): (positions, boundary_velocity, flagged) at step t."""
+    ref = _v3(reference_positions)
+    v = np.ascontiguousarray(motion.linear_velocity, dtype=np.float64)
+    w = np.ascontiguousarray(motion.angular_velocity, dtype=np.float64)
+    c = np.ascontiguousarray(motion.center, dtype=np.float64)
+    n = len(ref)
+    pos, ub = np.zeros((n, 3)), np.zeros((n, 3))
+    fl = np.zeros(n, dtype=np.uint8)
+    _check(lib().lbmg_ib_update_rigid_motion(n, _dp(ref), _dp(v), _dp(w), _dp(c), t, *_dims3(dims), _dp(pos), _dp(ub),
+                                             _u8(fl)))
+    return pos, ub, fl
+
+
+def ib_reaction_totals(positions, penalty_force, center, z0, z1):
+    """reaction_totals (ib.cpp:491-501): (force (3,), torque (3,))."""
+    pos, fo = _v3(positions), _v3(penalty_force)
+    c = np.ascontiguousarray(center, dtype=np.float64)
+    out = np.zeros(6)
+    _check(lib().lbmg_ib_reaction_totals(len(pos), _dp(pos), _dp(fo), _dp(c), z0, z1, _dp(out)))
+    return out[:3], out[3:]
