@@ -310,7 +310,7 @@ int lbmg_step(lbmg_runner* r, lbmg_status* status);
 /* The explicit SimState that step() advances (solver.hpp:29-45), canonical
  * AoS FP64 (nodes*27): f = f(t); f_star = the face-pass scratch whose face
  * entries seed the persistent face slots the stale outflow-edge reads use
- * (NULL: f); t = the step counter.  rho*/u* read back as the moments of f
+ * (NULL: f); t = the step counter.  rho* and u* read back as the moments of f
  * until the next step.  Single in-process region, no solids or tracers. */
 int lbmg_runner_load_state(lbmg_runner* r, const double* f, const double* f_star, long t);
 
