@@ -16,6 +16,11 @@ struct IbSolidDev {
     double* force;    // kIbHalves * n*3: one part per buffered step (ib_half)
     double* sampled;  // kIbHalves * n*3
     int nbuf;         // parts in use: the region's population buffer count
+    // samples the fused IB kernel runs over: static solids, the region's
+    // active ones (support inside the grid and touching the slab, fixed for a
+    // static set); nullptr = all n (moving solids, deterministic mode)
+    unsigned* active = nullptr;
+    unsigned n_active = 0;
     unsigned* source;
     unsigned char* flagged;
     // deterministic accumulation (ib_accumulation = deterministic): one
@@ -83,9 +88,16 @@ int totals_blocks(size_t n);
 int fused_blocks(size_t n);
 // every solid in one launch (device descriptors); totals row of solid k at
 // out_base[(t - chunk_t0) * out_stride + 6k]
+// A slab whose f the fused IB kernel may read: its geometry and population
+// buffers (own region, or an in-process neighbour across a seam).
+struct IbSlab {
+    RegionGeo g;
+    const float* f[3];
+};
 struct IbBatch {
+    IbSlab own, lo, hi;            // the region and its z neighbours (own where absent)
     const IbSolidDev* solids;      // device copy, n_solids
-    const unsigned* block_start;   // n_solids + 1 prefix of fused_blocks(n_k)
+    const unsigned* block_start;   // n_solids + 1 prefix of fused_blocks(samples run)
     const int* moving;             // n_solids
     unsigned n_solids;
     const double* table;           // motion rows, table_stride doubles per solid

@@ -250,31 +250,50 @@ __global__ void ib_motion_once_kernel(IbSolidDev S, const double* row, int nx, i
 }
 
 // ---------------------------------------------------------------------------
-// Fused IB step for a single-region run on the ghost layout (no seams), after
-// the ghost fill: one warp per sample.  Lane = corner * 4 + sub: the four
-// lanes of a corner pull 7/6 of its 27 post-BC populations f* straight from
-// the ghost-layer storage (every pull is a plain shifted read there) and
-// reduce rho*, j* by shuffles — the band pre-pass without a band list.  Then
-// interpolation (ib.cpp:321-343, FP64), penalty (ib.cpp:345-365), scatter
-// (ib.cpp:369-454, atomic mode: one lane per corner, fp32 RED into g), the
-// reaction totals (ib.cpp:491-501: per-block FP64 partials, the last block
-// sums them in block order -> deterministic) and, for moving solids, the
-// rigid motion to t+1 (ib.cpp:456-489).
-constexpr int kFusedWarps = 4;
-constexpr int kLanesPerSample = 8;                               // 8 corners x (lanes / 8) sub-lanes
-constexpr int kSubs = kLanesPerSample / 8;
-constexpr int kLoads = (27 + kSubs - 1) / kSubs;
+// Fused IB step on the ghost layout, after the ghost fill of this region and
+// of its neighbour slabs: per sample 8 lanes, one per support corner.  Each
+// lane pulls the corner's 27 post-BC populations f* straight from the
+// ghost-layer storage of the region that owns the corner's plane (its own, or
+// the neighbour's across a seam: in-process regions share the device, so a
+// seam costs no macro halo) and the lanes reduce rho*, j* by shuffles — the
+// band pre-pass without a band list.  Then interpolation (ib.cpp:321-343,
+// FP64), penalty (ib.cpp:345-365) for samples whose support touches the slab
+// (sample_active, ib.cpp:313-317), the scatter (ib.cpp:369-454, atomic mode)
+// onto owned nodes only (ib.cpp:377), pre-aggregated per CTA in a shared-
+// memory hash (block/Morton-sorted samples share support nodes) so one fp32
+// RED per distinct (node, component) reaches L2, the reaction totals
+// (ib.cpp:491-501: per-block FP64 partials, the last block sums them in block
+// order -> deterministic) and, for moving solids, the rigid motion to t+1
+// (ib.cpp:456-489).  Static solids run over the region's active samples only
+// (IbSolidDev::active, partitioned once by slab); moving ones over all.
+constexpr int kFusedWarps = 8;
+constexpr int kLanesPerSample = 8;
 constexpr int kFusedSamples = kFusedWarps * 32 / kLanesPerSample;
+constexpr int kScatterSlots = 4 * kFusedWarps * 32;  // hash slots (load <= 1/4)
+
+__device__ __forceinline__ const IbSlab& slab_of(const IbBatch& B, int gz, int z0, int z1) {
+    return gz < z0 ? B.lo : (gz >= z1 ? B.hi : B.own);
+}
 
 // All solids of the scene in ONE launch: blocks [block_start[k], block_start[k+1])
 // belong to solid k (per-solid totals reductions keep their own counters).
-__global__ void __launch_bounds__(kFusedWarps * 32, 8)
-    ib_fused_kernel(const __grid_constant__ FluidParams P, IbBatch B, int det) {
+__global__ void __launch_bounds__(kFusedWarps * 32, 3)
+    ib_fused_kernel(const __grid_constant__ FluidParams P, const __grid_constant__ IbBatch B, int det) {
     __shared__ double red[kFusedSamples][6];
+    __shared__ unsigned hkey[kScatterSlots];
+    __shared__ float hval[3][kScatterSlots];
     __shared__ bool last;
     DevCounters* ctr = P.ctr;
     if (ctr->diverged) return;
     const RegionGeo& g = P.g;
+    const bool smem = !det && !(B.probe & 8);  // (probe knob 8: direct global REDs)
+    if (smem) {
+        for (int j = threadIdx.x; j < kScatterSlots; j += blockDim.x) {
+            hkey[j] = 0xffffffffu;
+            hval[0][j] = hval[1][j] = hval[2][j] = 0.f;
+        }
+        __syncthreads();
+    }
     unsigned lo = 0, hi = B.n_solids;
     while (hi - lo > 1) {
         const unsigned mid = (lo + hi) >> 1;
@@ -292,88 +311,88 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     const int stride = B.out_stride;
     const unsigned lane = threadIdx.x & 31u;
     const unsigned slot = threadIdx.x / kLanesPerSample;  // sample slot in the block
-    const unsigned s = (blockIdx.x - b0) * kFusedSamples + slot;
-    const unsigned hl = lane % kLanesPerSample;          // lane within the sample's group
-    const int corner = int(hl / kSubs), sub = int(hl % kSubs);
-    const double* row = table + (ctr->t - ctr->chunk_t0) * kMotionRow;
+    const unsigned local = (blockIdx.x - b0) * kFusedSamples + slot;
+    const unsigned corner = lane % kLanesPerSample;
+    const long long t = ctr->t;
+    const double* row = table + (t - ctr->chunk_t0) * kMotionRow;
     double tot[6] = {0, 0, 0, 0, 0, 0};
-    const bool have = s < S.n;
-    const unsigned si = have ? s : 0u;
-    const double pos[3] = {S.pos[3 * si], S.pos[3 * si + 1], S.pos[3 * si + 2]};
-    const double ub[3] = {S.ub[3 * si], S.ub[3 * si + 1], S.ub[3 * si + 2]};  // (issued early)
+    const unsigned n_run = S.active ? S.n_active : S.n;
+    const bool have = local < n_run;
+    const unsigned s = have ? (S.active ? S.active[local] : local) : 0u;
+    const double pos[3] = {have ? S.pos[3 * s] : 0.0, have ? S.pos[3 * s + 1] : 0.0, have ? S.pos[3 * s + 2] : 0.0};
+    const double ub[3] = {have ? S.ub[3 * s] : 0.0, have ? S.ub[3 * s + 1] : 0.0,
+                          have ? S.ub[3 * s + 2] : 0.0};  // (issued early)
     const Support ks = kernel_support(pos, g.nx, g.ny, g.NZ);
-    if (have && hl == 0) S.flagged[s] = ks.inside ? 0 : 1;
-    const bool act = have && ks.inside;  // (single region: every support lies in the slab)
+    if (have && corner == 0) S.flagged[s] = ks.inside ? 0 : 1;
+    const int z0 = g.gz0, z1 = g.gz0 + g.nzl;
+    const bool act = have && ks.inside && sample_active(pos[2], g.NZ, z0, z1);
     // every lane runs the gather (shuffles need the full warp); inactive
-    // halves read node (0,0,0) and discard the result
+    // lanes read node (0,0,0) of the own slab and discard the result
     const int ox = corner & 1, oy = (corner >> 1) & 1, oz = corner >> 2;
+    const int gz = act ? ks.base[2] + oz : z0;
+    const IbSlab& R = slab_of(B, gz, z0, z1);
     const int x = act ? ks.base[0] + ox : 0, y = act ? ks.base[1] + oy : 0;
-    const int lz = act ? ks.base[2] + oz - g.gz0 : 0;
-    const float* fin = P.p.f[fcur(g, ctr->t)];
-    const long long sl = g.sidx(x, y, lz);
-    float v[kLoads];
+    const int lz = gz - R.g.gz0;
+    const float* fin = R.f[fcur(R.g, t)];
+    const long long sl = R.g.sidx(x, y, lz);
+    float v[27];
 #pragma unroll
-    for (int j = 0; j < kLoads; ++j) {  // all loads in flight at once
-        const int i = sub + kSubs * j;
-        v[j] = i < 27 ? __ldcg(&fin[g.gaddr((unsigned long long)(sl - g.soff(i)), i)]) : 0.f;
-    }
+    for (int i = 0; i < 27; ++i) v[i] = __ldcg(&fin[R.g.gaddr((unsigned long long)(sl - R.g.soff(i)), i)]);
     float r = 0.f, jx = 0.f, jy = 0.f, jz = 0.f;
 #pragma unroll
-    for (int j = 0; j < kLoads; ++j) {
-        const int i = sub + kSubs * j;
-        r += v[j];
-        jx += float(cx(i)) * v[j];
-        jy += float(cy(i)) * v[j];
-        jz += float(cz(i)) * v[j];
-    }
-#pragma unroll
-    for (int o = 1; o < kSubs; o <<= 1) {
-        r += __shfl_xor_sync(0xffffffffu, r, o);
-        jx += __shfl_xor_sync(0xffffffffu, jx, o);
-        jy += __shfl_xor_sync(0xffffffffu, jy, o);
-        jz += __shfl_xor_sync(0xffffffffu, jz, o);
+    for (int i = 0; i < 27; ++i) {
+        r += v[i];
+        jx += float(cx(i)) * v[i];
+        jy += float(cy(i)) * v[i];
+        jz += float(cz(i)) * v[i];
     }
     const float rho = 1.0f + r;
     const float inv = 1.0f / rho;
     const double wx = ox ? ks.w[0][1] : ks.w[0][0], wy = oy ? ks.w[1][1] : ks.w[1][0];
     const double wz = oz ? ks.w[2][1] : ks.w[2][0];
     const double w = __dmul_rn(__dmul_rn(wx, wy), wz);
-    double c4[4] = {sub == 0 ? w * double(jx * inv) : 0.0, sub == 0 ? w * double(jy * inv) : 0.0,
-                    sub == 0 ? w * double(jz * inv) : 0.0, sub == 0 ? w * double(rho) : 0.0};
+    double c4[4] = {w * double(jx * inv), w * double(jy * inv), w * double(jz * inv), w * double(rho)};
 #pragma unroll
-    for (int o = kSubs; o < kLanesPerSample; o <<= 1)
+    for (int o = 1; o < kLanesPerSample; o <<= 1)
 #pragma unroll
         for (int a = 0; a < 4; ++a) c4[a] += __shfl_xor_sync(0xffffffffu, c4[a], o);
     double us[3] = {0.0, 0.0, 0.0}, fg[3] = {0.0, 0.0, 0.0};
-    if (act) {
+    const bool own = act && gz >= z0 && gz < z1;
+    const unsigned k = own ? g.node(x, y, gz - z0) : 0u;
+    if (act)
         for (int a = 0; a < 3; ++a) {
             us[a] = c4[a];
             fg[a] = c4[3] * (ub[a] - us[a]);
         }
-        if (sub == 0 && det) {  // deterministic: a (node, contribution) record per corner
-            const unsigned rec = s * 8u + unsigned(corner);
-            S.rec_key[rec] = g.node(x, y, lz);
+    if (det) {  // deterministic: a (owned node | ~0u, contribution) record per corner
+        if (have) {
+            const unsigned rec = local * 8u + corner;
+            S.rec_key[rec] = own ? k : ~0u;
             S.rec_idx[rec] = rec;
-            for (int a = 0; a < 3; ++a) S.rec_val[3 * rec + a] = w * fg[a];
-        } else if (sub == 0 && !(moving & 2)) {  // scatter of this corner (owned: single region)
-            const unsigned k = g.node(x, y, lz);
-            atomicAdd(&P.p.gib[k], float(w * fg[0]));
-            atomicAdd(&P.p.gib[k + g.ns], float(w * fg[1]));
-            atomicAdd(&P.p.gib[k + 2u * g.ns], float(w * fg[2]));
-            if (!(moving & 4)) P.p.tflag[k] = ib_epoch(P.ctr->t);
+            for (int a = 0; a < 3; ++a) S.rec_val[3 * rec + a] = own ? w * fg[a] : 0.0;
+        }
+    } else if (own && !(moving & 2)) {
+        const float add[3] = {float(w * fg[0]), float(w * fg[1]), float(w * fg[2])};
+        if (smem) {
+            unsigned h = (k * 2654435761u) & (kScatterSlots - 1);
+            for (;;) {
+                const unsigned prev = atomicCAS(&hkey[h], 0xffffffffu, k);
+                if (prev == 0xffffffffu || prev == k) break;
+                h = (h + 1) & (kScatterSlots - 1);
+            }
+            for (int a = 0; a < 3; ++a) atomicAdd(&hval[a][h], add[a]);
+        } else {
+            for (int a = 0; a < 3; ++a) atomicAdd(&P.p.gib[k + a * g.ns], add[a]);
+            if (!(moving & 4)) P.p.tflag[k] = ib_epoch(t);
         }
     }
-    if (det && have && !act && sub == 0) {  // inactive sample: empty records
-        S.rec_key[s * 8u + unsigned(corner)] = ~0u;
-        S.rec_idx[s * 8u + unsigned(corner)] = s * 8u + unsigned(corner);
-    }
-    if (have && hl == 0) {
-        const size_t po = ib_half(S, ctr->t);
+    if (have && corner == 0) {
+        const size_t po = ib_half(S, t);
         for (int a = 0; a < 3; ++a) {
             S.sampled[po + 3 * s + a] = us[a];
             S.force[po + 3 * s + a] = fg[a];
         }
-        if (pos[2] >= double(g.gz0) && pos[2] < double(g.gz0 + g.nzl)) {
+        if (pos[2] >= double(z0) && pos[2] < double(z1)) {
             const double rr[3] = {pos[0] - row[0], pos[1] - row[1], pos[2] - row[2]};
             tot[0] = -fg[0];
             tot[1] = -fg[1];
@@ -384,12 +403,19 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
         }
         if (moving & 1) motion_apply(row + kMotionRow, S, s, g.nx, g.ny, g.NZ);
     }
-    if (hl == 0)
+    if (corner == 0)
         for (int a = 0; a < 6; ++a) red[slot][a] = tot[a];
     __syncthreads();
+    if (smem)  // one global RED per distinct (owned node, component) of the CTA
+        for (int j = threadIdx.x; j < kScatterSlots; j += blockDim.x) {
+            const unsigned key = hkey[j];
+            if (key == 0xffffffffu) continue;
+            for (int a = 0; a < 3; ++a) atomicAdd(&P.p.gib[key + a * g.ns], hval[a][j]);
+            if (!(moving & 4)) P.p.tflag[key] = ib_epoch(t);
+        }
     if (threadIdx.x < 6) {
         double acc = 0.0;
-        for (int w = 0; w < kFusedSamples; ++w) acc += red[w][threadIdx.x];
+        for (int w2 = 0; w2 < kFusedSamples; ++w2) acc += red[w2][threadIdx.x];
         partial[(blockIdx.x - b0) * 6 + threadIdx.x] = acc;
         __threadfence();
     }
@@ -411,7 +437,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
             for (int a = 0; a < 6; ++a) tree[a][threadIdx.x] += tree[a][threadIdx.x + off];
         __syncthreads();
     }
-    if (threadIdx.x < 6) out_base[(ctr->t - ctr->chunk_t0) * stride + threadIdx.x] = tree[threadIdx.x][0];
+    if (threadIdx.x < 6) out_base[(t - ctr->chunk_t0) * stride + threadIdx.x] = tree[threadIdx.x][0];
     if (threadIdx.x == 0) *done = 0u;
 }
 
@@ -649,9 +675,11 @@ int fused_blocks(size_t n) { return int((n + kFusedSamples - 1) / kFusedSamples)
 void launch_ib_fused(const FluidParams& P, IbBatch B, unsigned total_blocks, const IbSolidDev* host_solids,
                      cudaStream_t st, bool deterministic) {
     if (total_blocks == 0) return;
-    static const int probe = [] {  // timing probe: LBMG_IB_NOSCATTER=1 skips the scatter into g
-        const char* e = std::getenv("LBMG_IB_NOSCATTER");  // 1: no scatter, 2: scatter without force flags
-        return e ? (std::atoi(e) == 1 ? 2 : (std::atoi(e) == 2 ? 4 : 0)) : 0;
+    static const int probe = [] {  // timing probes: LBMG_IB_NOSCATTER=1 skips the scatter into g,
+        const char* e = std::getenv("LBMG_IB_NOSCATTER");  // 2: scatter without force flags;
+        const char* d = std::getenv("LBMG_IB_SCATTER");     // LBMG_IB_SCATTER=global: no shared-memory pre-aggregation
+        return (e ? (std::atoi(e) == 1 ? 2 : (std::atoi(e) == 2 ? 4 : 0)) : 0) |
+               (d && std::string(d) == "global" ? 8 : 0);
     }();
     B.probe = probe;
     ib_fused_kernel<<<total_blocks, kFusedWarps * 32, 0, st>>>(P, B, deterministic ? 1 : 0);

@@ -366,7 +366,7 @@ void Runner::build_regions(int) {
             r.ptr.band_count = static_cast<unsigned*>(dalloc(sizeof(unsigned)));
             r.partial = static_cast<double*>(dalloc(sizeof(double) * 6 * 256));
             size_t blocks = 1;
-            for (const auto& so : scene_.solids) blocks += size_t(fused_blocks(so.samples.size()));
+            for (const auto& so : scene_.solids) blocks += size_t(std::max(1, fused_blocks(so.samples.size())));
             r.fused_partial = static_cast<double*>(dalloc(sizeof(double) * 6 * blocks));
             r.fused_done = static_cast<unsigned*>(dalloc(sizeof(unsigned) * scene_.solids.size()));
         }
@@ -468,23 +468,64 @@ void Runner::upload_solids() {
             }
             r.solids.push_back(d);
         }
-        // the fused IB kernel's batch: every solid in one launch
         const size_t ns = r.solids.size();
         if (ns) {
-            std::vector<unsigned> start(ns + 1, 0);
             std::vector<int> mv(ns);
-            for (size_t k = 0; k < ns; ++k) {
-                start[k + 1] = start[k] + unsigned(fused_blocks(r.solids[k].n));
-                mv[k] = moving_[k] ? 1 : 0;
-            }
+            for (size_t k = 0; k < ns; ++k) mv[k] = moving_[k] ? 1 : 0;
             r.batch_solids = static_cast<IbSolidDev*>(dalloc(sizeof(IbSolidDev) * ns));
             r.batch_start = static_cast<unsigned*>(dalloc(sizeof(unsigned) * (ns + 1)));
             r.batch_moving = static_cast<int*>(dalloc(sizeof(int) * ns));
+            CK(copy_sync(r.batch_moving, mv.data(), sizeof(int) * ns, cudaMemcpyHostToDevice));
+        }
+    }
+    build_active_lists();
+}
+
+// The fused IB kernel's batch of each region (every solid in one launch):
+// a static solid runs over the samples whose support lies inside the grid
+// and touches the region's slab (kernel_support / sample_active,
+// ib.cpp:294-317: fixed for a static set, so the slabs partition the work
+// instead of every region replaying every sample); a moving one, and every
+// solid in deterministic mode (its records are indexed by sample), over all.
+// The inactive samples' outputs stay zero, as the reference writes them.
+void Runner::build_active_lists() {
+    if (!has_solids_) return;
+    const bool det = scene_.cfg.ib_mode == LBMG_IB_DETERMINISTIC;
+    for (auto& r : regions_) {
+        const size_t ns = r.solids.size();
+        std::vector<unsigned> start(ns + 1, 0);
+        for (size_t k = 0; k < ns; ++k) {
+            IbSolidDev& d = r.solids[k];
+            if (d.active) {
+                dfree(d.active);
+                d.active = nullptr;
+            }
+            d.n_active = 0;
+            if (!moving_[k] && !det && d.n) {
+                std::vector<double> pos(3 * size_t(d.n));
+                CK(copy_sync(pos.data(), d.pos, sizeof(double) * pos.size(), cudaMemcpyDeviceToHost));
+                std::vector<unsigned> act;
+                const int n3[3] = {nx_, ny_, nz_};
+                for (unsigned q = 0; q < d.n; ++q) {
+                    bool inside = true;
+                    for (int a = 0; a < 3; ++a)
+                        if (pos[3 * q + a] < 0.0 || pos[3 * q + a] > double(n3[a] - 1)) inside = false;
+                    const int bz = std::max(0, std::min(int(std::floor(pos[3 * q + 2])), nz_ - 2));
+                    if (inside && bz + 1 >= r.z0 && bz < r.z1) act.push_back(q);
+                }
+                d.active = static_cast<unsigned*>(dalloc(sizeof(unsigned) * std::max<size_t>(act.size(), 1), false));
+                if (!act.empty())
+                    CK(copy_sync(d.active, act.data(), sizeof(unsigned) * act.size(), cudaMemcpyHostToDevice));
+                d.n_active = unsigned(act.size());
+            }
+            // (at least one block: it writes the solid's totals row of the region)
+            start[k + 1] = start[k] + unsigned(std::max(1, fused_blocks(d.active ? d.n_active : d.n)));
+        }
+        if (ns) {
             CK(copy_sync(r.batch_solids, r.solids.data(), sizeof(IbSolidDev) * ns, cudaMemcpyHostToDevice));
             CK(copy_sync(r.batch_start, start.data(), sizeof(unsigned) * (ns + 1), cudaMemcpyHostToDevice));
-            CK(copy_sync(r.batch_moving, mv.data(), sizeof(int) * ns, cudaMemcpyHostToDevice));
-            r.batch_blocks = start[ns];
         }
+        r.batch_blocks = start[ns];
     }
 }
 
@@ -609,14 +650,20 @@ bool Runner::overlap_off() {
     return off;
 }
 
-// Single region on the ghost layout: ghost fill first, then one fused IB
-// kernel per solid (no band list, no seams), then the fluid kernel.
+// In-process regions on the ghost layout: the ghost fills first, then one
+// fused IB kernel per region (every solid; support nodes across a seam are
+// read from the neighbour slab's buffers on the same device), then the fluid
+// kernels.  Rank mode (one slab per process) keeps the split pipeline and its
+// macro halo.
 bool Runner::fused_ib() const {
     static const bool off = [] {
         const char* e = std::getenv("LBMG_IB_FUSED");
         return e && std::string(e) == "0";
     }();
-    return has_solids_ && !off && variant_ib_ == 0 && !rank_mode_ && regions_.size() == 1 && regions_[0].geo.ghost;
+    if (!has_solids_ || off || variant_ib_ != 0 || rank_mode_) return false;
+    for (const auto& r : regions_)
+        if (!r.geo.ghost) return false;
+    return true;
 }
 
 // One step on the runner's stream.  Timing events (advance with timings):
@@ -628,7 +675,7 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
     if (ev) CK(cudaEventRecord((*ev)[0], st));
     // ghost fill || fused IB when no IB support node can touch a ghost slot
     // (a fork/join inside the captured graph); timed runs keep them serial
-    const bool overlap = !ev && fused_ib() && ib_overlap_ok_ && !overlap_off();
+    const bool overlap = !ev && fused_ib() && regions_.size() == 1 && ib_overlap_ok_ && !overlap_off();
     cudaStream_t fst = st;
     if (overlap) {
         CK(cudaEventRecord(fork_, st));
@@ -643,21 +690,32 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
     if (overlap) CK(cudaEventRecord(join_, side_));
     if (ev) CK(cudaEventRecord((*ev)[1], st));
     if (fused_ib()) {
-        Region& r = regions_[0];
-        FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
-        const int ns = int(scene_.solids.size());
-        IbBatch B{};
-        B.solids = r.batch_solids;
-        B.block_start = r.batch_start;
-        B.moving = r.batch_moving;
-        B.n_solids = unsigned(ns);
-        B.table = motion_tab_;
-        B.table_stride = size_t(cap_ + 2) * kMotionRow;
-        B.partial = r.fused_partial;
-        B.done = r.fused_done;
-        B.out_base = totals_dev_;
-        B.out_stride = ns * 6;
-        launch_ib_fused(P, B, r.batch_blocks, r.solids.data(), st, scene_.cfg.ib_mode == LBMG_IB_DETERMINISTIC);
+        const int ns = int(scene_.solids.size()), m = int(regions_.size());
+        auto slab = [&](const Region& q) {
+            IbSlab sl{};
+            sl.g = q.geo;
+            for (int b = 0; b < 3; ++b) sl.f[b] = q.ptr.f[b];
+            return sl;
+        };
+        for (int ri = 0; ri < m; ++ri) {
+            Region& r = regions_[ri];
+            FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+            IbBatch B{};
+            B.own = slab(r);
+            B.lo = ri > 0 ? slab(regions_[ri - 1]) : B.own;  // (support never wraps: kernel_support clamps)
+            B.hi = ri + 1 < m ? slab(regions_[ri + 1]) : B.own;
+            B.solids = r.batch_solids;
+            B.block_start = r.batch_start;
+            B.moving = r.batch_moving;
+            B.n_solids = unsigned(ns);
+            B.table = motion_tab_;
+            B.table_stride = size_t(cap_ + 2) * kMotionRow;
+            B.partial = r.fused_partial;
+            B.done = r.fused_done;
+            B.out_base = totals_dev_ + size_t(ri) * ns * 6;
+            B.out_stride = m * ns * 6;
+            launch_ib_fused(P, B, r.batch_blocks, r.solids.data(), st, scene_.cfg.ib_mode == LBMG_IB_DETERMINISTIC);
+        }
     } else if (has_solids_) {
         enqueue_ib_pre();
         enqueue_ib_mid();
@@ -1083,6 +1141,7 @@ void Runner::set_layout(int ell, size_t alpha) {
             CK(copy_sync(d.flagged, f2.data(), n, cudaMemcpyHostToDevice));
         }
     ell_ = ell;
+    build_active_lists();  // the sample order changed
     invalidate_graphs();
 }
 

@@ -166,6 +166,7 @@ private:
     void link_halos();
     void init_fields();
     void upload_solids();
+    void build_active_lists();
     void fill_motion_table(long t0, long rows, bool sync);
     void motion_row(int solid, long t, double* row) const;
     void enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev);
