@@ -253,47 +253,33 @@ __global__ void ib_motion_once_kernel(IbSolidDev S, const double* row, int nx, i
 // Fused IB step on the ghost layout, after the ghost fill of this region and
 // of its neighbour slabs: per sample 8 lanes, one per support corner.  Each
 // lane pulls the corner's 27 post-BC populations f* straight from the
-// ghost-layer storage of the region that owns the corner's plane (its own, or
-// the neighbour's across a seam: in-process regions share the device, so a
-// seam costs no macro halo) and the lanes reduce rho*, j* by shuffles — the
-// band pre-pass without a band list.  Then interpolation (ib.cpp:321-343,
-// FP64), penalty (ib.cpp:345-365) for samples whose support touches the slab
-// (sample_active, ib.cpp:313-317), the scatter (ib.cpp:369-454, atomic mode)
-// onto owned nodes only (ib.cpp:377), pre-aggregated per CTA in a shared-
-// memory hash (block/Morton-sorted samples share support nodes) so one fp32
-// RED per distinct (node, component) reaches L2, the reaction totals
+// ghost-layer storage of the slab that owns the corner's plane (its own, or
+// the in-process neighbour's across a seam: no macro halo) — all 27 loads in
+// flight at once — and the lanes reduce rho*, j* by shuffles: the band
+// pre-pass without a band list.  Then interpolation (ib.cpp:321-343, FP64),
+// penalty (ib.cpp:345-365) for samples whose support touches the slab
+// (sample_active, ib.cpp:313-317), the scatter (ib.cpp:369-454, atomic mode:
+// one fp32 RED per corner, owned nodes only, ib.cpp:377), the reaction totals
 // (ib.cpp:491-501: per-block FP64 partials, the last block sums them in block
 // order -> deterministic) and, for moving solids, the rigid motion to t+1
 // (ib.cpp:456-489).  Static solids run over the region's active samples only
 // (IbSolidDev::active, partitioned once by slab); moving ones over all.
-constexpr int kFusedWarps = 8;
+// (Measured alternatives, slower on C2 and configs[3]: 8-warp CTAs with a
+// shared-memory pre-aggregated scatter — 2.8 vs 1.9 ms on configs[3] — and a
+// per-CTA dedup of support nodes in shared memory — 5.0 ms.)
+constexpr int kFusedWarps = 4;
 constexpr int kLanesPerSample = 8;
 constexpr int kFusedSamples = kFusedWarps * 32 / kLanesPerSample;
-constexpr int kScatterSlots = 4 * kFusedWarps * 32;  // hash slots (load <= 1/4)
-
-__device__ __forceinline__ const IbSlab& slab_of(const IbBatch& B, int gz, int z0, int z1) {
-    return gz < z0 ? B.lo : (gz >= z1 ? B.hi : B.own);
-}
 
 // All solids of the scene in ONE launch: blocks [block_start[k], block_start[k+1])
 // belong to solid k (per-solid totals reductions keep their own counters).
-__global__ void __launch_bounds__(kFusedWarps * 32, 3)
+__global__ void __launch_bounds__(kFusedWarps * 32, 8)
     ib_fused_kernel(const __grid_constant__ FluidParams P, const __grid_constant__ IbBatch B, int det) {
     __shared__ double red[kFusedSamples][6];
-    __shared__ unsigned hkey[kScatterSlots];
-    __shared__ float hval[3][kScatterSlots];
     __shared__ bool last;
     DevCounters* ctr = P.ctr;
     if (ctr->diverged) return;
     const RegionGeo& g = P.g;
-    const bool smem = !det && !(B.probe & 8);  // (probe knob 8: direct global REDs)
-    if (smem) {
-        for (int j = threadIdx.x; j < kScatterSlots; j += blockDim.x) {
-            hkey[j] = 0xffffffffu;
-            hval[0][j] = hval[1][j] = hval[2][j] = 0.f;
-        }
-        __syncthreads();
-    }
     unsigned lo = 0, hi = B.n_solids;
     while (hi - lo > 1) {
         const unsigned mid = (lo + hi) >> 1;
@@ -330,11 +316,10 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 3)
     // lanes read node (0,0,0) of the own slab and discard the result
     const int ox = corner & 1, oy = (corner >> 1) & 1, oz = corner >> 2;
     const int gz = act ? ks.base[2] + oz : z0;
-    const IbSlab& R = slab_of(B, gz, z0, z1);
+    const IbSlab& R = gz < z0 ? B.lo : (gz >= z1 ? B.hi : B.own);
     const int x = act ? ks.base[0] + ox : 0, y = act ? ks.base[1] + oy : 0;
-    const int lz = gz - R.g.gz0;
     const float* fin = R.f[fcur(R.g, t)];
-    const long long sl = R.g.sidx(x, y, lz);
+    const long long sl = R.g.sidx(x, y, gz - R.g.gz0);
     float v[27];
 #pragma unroll
     for (int i = 0; i < 27; ++i) v[i] = __ldcg(&fin[R.g.gaddr((unsigned long long)(sl - R.g.soff(i)), i)]);
@@ -372,19 +357,8 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 3)
             for (int a = 0; a < 3; ++a) S.rec_val[3 * rec + a] = own ? w * fg[a] : 0.0;
         }
     } else if (own && !(moving & 2)) {
-        const float add[3] = {float(w * fg[0]), float(w * fg[1]), float(w * fg[2])};
-        if (smem) {
-            unsigned h = (k * 2654435761u) & (kScatterSlots - 1);
-            for (;;) {
-                const unsigned prev = atomicCAS(&hkey[h], 0xffffffffu, k);
-                if (prev == 0xffffffffu || prev == k) break;
-                h = (h + 1) & (kScatterSlots - 1);
-            }
-            for (int a = 0; a < 3; ++a) atomicAdd(&hval[a][h], add[a]);
-        } else {
-            for (int a = 0; a < 3; ++a) atomicAdd(&P.p.gib[k + a * g.ns], add[a]);
-            if (!(moving & 4)) P.p.tflag[k] = ib_epoch(t);
-        }
+        for (int a = 0; a < 3; ++a) atomicAdd(&P.p.gib[k + a * g.ns], float(w * fg[a]));
+        if (!(moving & 4)) P.p.tflag[k] = ib_epoch(t);
     }
     if (have && corner == 0) {
         const size_t po = ib_half(S, t);
@@ -406,13 +380,6 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 3)
     if (corner == 0)
         for (int a = 0; a < 6; ++a) red[slot][a] = tot[a];
     __syncthreads();
-    if (smem)  // one global RED per distinct (owned node, component) of the CTA
-        for (int j = threadIdx.x; j < kScatterSlots; j += blockDim.x) {
-            const unsigned key = hkey[j];
-            if (key == 0xffffffffu) continue;
-            for (int a = 0; a < 3; ++a) atomicAdd(&P.p.gib[key + a * g.ns], hval[a][j]);
-            if (!(moving & 4)) P.p.tflag[key] = ib_epoch(t);
-        }
     if (threadIdx.x < 6) {
         double acc = 0.0;
         for (int w2 = 0; w2 < kFusedSamples; ++w2) acc += red[w2][threadIdx.x];
@@ -676,10 +643,8 @@ void launch_ib_fused(const FluidParams& P, IbBatch B, unsigned total_blocks, con
                      cudaStream_t st, bool deterministic) {
     if (total_blocks == 0) return;
     static const int probe = [] {  // timing probes: LBMG_IB_NOSCATTER=1 skips the scatter into g,
-        const char* e = std::getenv("LBMG_IB_NOSCATTER");  // 2: scatter without force flags;
-        const char* d = std::getenv("LBMG_IB_SCATTER");     // LBMG_IB_SCATTER=global: no shared-memory pre-aggregation
-        return (e ? (std::atoi(e) == 1 ? 2 : (std::atoi(e) == 2 ? 4 : 0)) : 0) |
-               (d && std::string(d) == "global" ? 8 : 0);
+        const char* e = std::getenv("LBMG_IB_NOSCATTER");  // 2: scatter without force flags
+        return e ? (std::atoi(e) == 1 ? 2 : (std::atoi(e) == 2 ? 4 : 0)) : 0;
     }();
     B.probe = probe;
     ib_fused_kernel<<<total_blocks, kFusedWarps * 32, 0, st>>>(P, B, deterministic ? 1 : 0);

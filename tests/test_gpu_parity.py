@@ -501,6 +501,7 @@ def test_rank_mode_matches_in_process_regions(make, world):
     steps = 23
     rs = _rank_mode_run(cfg, world, steps)
     ref = lbm.Runner(lbm.build_scene(cfg), regions=world)
+    ref.set_variant(0, 1)  # the split IB pipeline rank mode runs (in-process regions default to the fused kernel)
     ref.advance(steps)
     f_ref, rho_ref = ref.gather_f(), ref.gather_rho()
     f_rank = np.concatenate([r.gather_f() for r in rs])
