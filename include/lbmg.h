@@ -161,6 +161,17 @@ int lbmg_split_domain(int nz, int m, int* z0z1);
  * regions > 1 places every z-slab region on `device` (in-process halo
  * exchange through device memory); world/rank mode is lbmg_runner_create_rank. */
 int lbmg_runner_create(const lbmg_scene* scene, int regions, int device, lbmg_runner** out);
+/* Runner(const Scene&, int regions, unsigned threads) across devices of one
+ * process: region (z-slab) r on devices[r % n_devices].  Peer access between
+ * neighbouring slabs' devices is enabled: each slab's fluid kernel stores its
+ * 9 crossing populations straight into the neighbours' halo buffers and the
+ * fused IB kernel reads support nodes across a seam from the neighbour's
+ * storage (NVLink); one stream per slab, cross-device events order a step.
+ * Repeating a device (e.g. {0, 0}) runs the same orchestration on one GPU. */
+int lbmg_runner_create_devices(const lbmg_scene* scene, int regions, int n_devices, const int* devices,
+                               lbmg_runner** out);
+/* Device of region r (-1 when out of range). */
+int lbmg_runner_region_device(const lbmg_runner* r, int region);
 /* One region (z-slab `rank` of `world`) of a multi-process run: halos are
  * exchanged by the caller through lbmg_runner_halo_* (NCCL send/recv). */
 int lbmg_runner_create_rank(const lbmg_scene* scene, int world, int rank, int device,

@@ -250,6 +250,28 @@ int lbmg_runner_create(const lbmg_scene* scene, int regions, int device, lbmg_ru
     });
 }
 
+int lbmg_runner_create_devices(const lbmg_scene* scene, int regions, int n_devices, const int* devices,
+                               lbmg_runner** out) {
+    return guarded([&] {
+        if (!scene || !out) throw lbmg::ConfigError("runner: scene and out are required");
+        if (n_devices < 1 || !devices) throw lbmg::ConfigError("devices: at least one device");
+        std::vector<int> devs(devices, devices + n_devices);
+        auto r = new lbmg_runner;
+        try {
+            r->impl = std::make_unique<Runner>(*scene, regions, devs[0], 0, 0, devs);
+        } catch (...) {
+            delete r;
+            throw;
+        }
+        *out = r;
+    });
+}
+
+int lbmg_runner_region_device(const lbmg_runner* r, int region) {
+    if (!r || !r->impl || region < 0 || region >= r->impl->region_count()) return -1;
+    return r->impl->region_device(region);
+}
+
 int lbmg_runner_create_rank(const lbmg_scene* scene, int world, int rank, int device, lbmg_runner** out) {
     return guarded([&] {
         if (!scene) throw StateError("null scene");

@@ -164,6 +164,7 @@ struct RegionPtrs {
     float* msend_lo;
     float* msend_hi;
     unsigned* band_count;  // IB band nodes this step
+    unsigned* queue;       // tile queues of the staged fluid launches: counters [4], CTAs done [4]
 };
 
 // Physical population buffer of f(t) (the A/B pair: nbuf = 2).
@@ -176,8 +177,6 @@ struct DevCounters {
     unsigned mach;             // sticky Mach warning
     long long diverged_step;   // step at which divergence was detected
     long long chunk_t0;        // first step of the current advance chunk
-    unsigned tile_ctr[4];      // tile queues of the staged fluid launches of a step
-    unsigned tile_done[4];     // CTAs finished per queue (the last one rewinds it)
 };
 
 // IB force-flag epoch of step t: 1..255 (a zeroed flag byte never matches)

@@ -389,9 +389,9 @@ __global__ void __launch_bounds__(T, 512 / T)
     uint64_t* const full = reinterpret_cast<uint64_t*>(smem_raw + kStages * kStageBytes);
     DevCounters* ctr = P.ctr;
     if (ctr->diverged) {  // CTA-uniform; still counted for the queue rewind
-        if (threadIdx.x == 0 && atomicAdd(&ctr->tile_done[slot], 1u) == gridDim.x - 1) {
-            ctr->tile_ctr[slot] = 0u;
-            ctr->tile_done[slot] = 0u;
+        if (threadIdx.x == 0 && atomicAdd(&P.p.queue[4 + slot], 1u) == gridDim.x - 1) {
+            P.p.queue[slot] = 0u;
+            P.p.queue[4 + slot] = 0u;
         }
         return;
     }
@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(T, 512 / T)
     // fill of this step): all CTAs sweep the arrays together, so DRAM pages
     // stay open across CTAs and the window edges two neighbouring tiles share
     // are fetched once and hit in L2 for the other.
-    unsigned* const next_tile = &ctr->tile_ctr[slot];
+    unsigned* const next_tile = &P.p.queue[slot];
     // tile id per (stage, phase parity): the refill for phase k+1 writes the
     // other parity slot than the one phase-k readers use (no WAR hazard)
     __shared__ unsigned stage_tile[kStages][2];
@@ -574,9 +574,9 @@ __global__ void __launch_bounds__(T, 512 / T)
     __syncthreads();
     if (tid == 0) {
         __threadfence();
-        if (atomicAdd(&ctr->tile_done[slot], 1u) == gridDim.x - 1) {
-            ctr->tile_ctr[slot] = 0u;
-            ctr->tile_done[slot] = 0u;
+        if (atomicAdd(&P.p.queue[4 + slot], 1u) == gridDim.x - 1) {
+            P.p.queue[slot] = 0u;
+            P.p.queue[4 + slot] = 0u;
             __threadfence();
             if (end_step && !ctr->diverged) ctr->t += 1;  // step_end_kernel folded in
         }

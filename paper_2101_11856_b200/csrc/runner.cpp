@@ -60,6 +60,18 @@ int log2i(size_t v) {
     return s;
 }
 
+// Current-device guard: regions may live on different devices.
+struct DevGuard {
+    int prev = -1, want;
+    explicit DevGuard(int d) : want(d) {
+        cudaGetDevice(&prev);
+        if (prev != want) cuda_check(cudaSetDevice(want), "cudaSetDevice");
+    }
+    ~DevGuard() {
+        if (prev >= 0 && prev != want) cudaSetDevice(prev);
+    }
+};
+
 // equilibrium, collision.cpp:148-157 (FP64, reference operation order).
 double feq(int i, double rho, const double u[3]) {
     const double usq = 1.5 * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
@@ -75,16 +87,33 @@ double feq(int i, double rho, const double u[3]) {
 // device-to-device (or pageable host-to-device) cudaMemcpy may return before
 // the data has landed.
 cudaError_t Runner::copy_sync(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) const {
-    cudaStream_t st = stream();
+    int dev = device_;
+    if (multi_dev_) {  // the stream of the device that holds the device side
+        cudaPointerAttributes a{};
+        const void* dside = kind == cudaMemcpyHostToDevice ? dst : src;
+        if (cudaPointerGetAttributes(&a, dside) == cudaSuccess && a.type == cudaMemoryTypeDevice) dev = a.device;
+        cudaGetLastError();
+    }
+    DevGuard g(dev);
+    cudaStream_t st = dev_stream(dev);
     cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, st);
     if (e != cudaSuccess) return e;
     return cudaStreamSynchronize(st);
 }
 
+cudaStream_t Runner::dev_stream(int dev) const {
+    if (dev == device_ || !multi_dev_) return stream();
+    for (const auto& r : regions_)
+        if (r.dev == dev && r.st) return r.st;
+    return stream();
+}
+
 FluidParams Runner::Region::params() const { return FluidParams{geo, {}, {}, ptr, nullptr}; }
 
-void* Runner::dalloc(size_t bytes, bool zero) {
+void* Runner::dalloc(size_t bytes, bool zero, int dev) {
     if (bytes == 0) bytes = 16;
+    if (dev < 0) dev = device_;
+    DevGuard g(dev);
     void* p = nullptr;
     cudaError_t e = cudaMalloc(&p, bytes);
     if (e != cudaSuccess) {
@@ -93,8 +122,9 @@ void* Runner::dalloc(size_t bytes, bool zero) {
                        cudaGetErrorString(e));
     }
     if (zero) {  // on the runner's stream (non-blocking streams skip the legacy one), complete on return
-        CK(cudaMemsetAsync(p, 0, bytes, stream()));
-        CK(cudaStreamSynchronize(stream()));
+        cudaStream_t zs = dev_stream(dev);
+        CK(cudaMemsetAsync(p, 0, bytes, zs));
+        CK(cudaStreamSynchronize(zs));
     }
     allocs_.push_back(p);
     return p;
@@ -107,7 +137,8 @@ void Runner::dfree(void* p) {
     cudaFree(p);
 }
 
-Runner::Runner(const lbmg_scene& scene, int regions, int device, int world, int rank) {
+Runner::Runner(const lbmg_scene& scene, int regions, int device, int world, int rank,
+               const std::vector<int>& devices) {
     scene_ = scene;
     scene_.cfg.solids = scene_.solid_cfgs.empty() ? nullptr : scene_.solid_cfgs.data();
     scene_.cfg.n_solids = int(scene_.solid_cfgs.size());
@@ -192,6 +223,57 @@ Runner::Runner(const lbmg_scene& scene, int regions, int device, int world, int 
     const int first = rank_mode_ ? rank_ : 0;
     const int count = rank_mode_ ? 1 : m_global_;
     regions_.resize(count);
+    devices_ = devices;
+    if (!devices.empty()) {
+        if (rank_mode_) throw ConfigError("devices: rank mode places its one slab with `device`");
+        if (!scene_.emitters.empty())
+            throw ConfigError("tracers: emitters need a single-stream runner (no per-region devices)");
+        int ndev = 0;
+        CK(cudaGetDeviceCount(&ndev));
+        for (int d : devices)
+            if (d < 0 || d >= ndev) throw ConfigError("devices: no CUDA device " + std::to_string(d));
+        if (!scene_.solids.empty() && !(nx_ % 4 == 0 && ghost_layout_enabled()))
+            throw ConfigError("devices: solids on several devices need the ghost layout (nx % 4 == 0)");
+        multi_dev_ = true;
+        device_ = devices[0];
+        CK(cudaSetDevice(device_));
+    }
+    for (int r = 0; r < count; ++r) {
+        Region& R = regions_[r];
+        R.dev = multi_dev_ ? devices[size_t(r) % devices.size()] : device_;
+        if (multi_dev_) {
+            DevGuard g(R.dev);
+            CK(cudaStreamCreateWithFlags(&R.st, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&R.ev_fill, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&R.ev_fluid, cudaEventDisableTiming));
+        }
+    }
+    if (multi_dev_) {
+        CK(cudaEventCreateWithFlags(&ev_step_, cudaEventDisableTiming));
+        // peer access: neighbouring slabs (halo stores, IB seam reads) and
+        // every slab with the home device (step counters, motion and totals)
+        auto peer = [](int a, int b) {
+            if (a == b) return;
+            int ok = 0;
+            CK(cudaDeviceCanAccessPeer(&ok, a, b));
+            if (!ok)
+                throw ConfigError("devices: no peer access between devices " + std::to_string(a) + " and " +
+                                  std::to_string(b));
+            DevGuard g(a);
+            const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            else CK(e);
+        };
+        for (int r = 0; r < count; ++r) {
+            const int lo = r > 0 ? r - 1 : count - 1, hi = r + 1 < count ? r + 1 : 0;
+            for (int q : {lo, hi}) {
+                peer(regions_[r].dev, regions_[q].dev);
+                peer(regions_[q].dev, regions_[r].dev);
+            }
+            peer(regions_[r].dev, device_);
+            peer(device_, regions_[r].dev);
+        }
+    }
     for (int r = 0; r < count; ++r) {
         regions_[r].z0 = slabs[first + r][0];
         regions_[r].z1 = slabs[first + r][1];
@@ -257,8 +339,17 @@ Runner::~Runner() {
     if (pinned_down_) cudaFreeHost(pinned_down_);
     if (pinned_temit_) cudaFreeHost(pinned_temit_);
     if (pinned_tstate_) cudaFreeHost(pinned_tstate_);
+    for (auto& r : regions_) {
+        if (r.st) cudaStreamSynchronize(r.st);
+    }
     for (void* p : allocs_) cudaFree(p);
     allocs_.clear();
+    for (auto& r : regions_) {
+        if (r.st) cudaStreamDestroy(r.st);
+        if (r.ev_fill) cudaEventDestroy(r.ev_fill);
+        if (r.ev_fluid) cudaEventDestroy(r.ev_fluid);
+    }
+    if (ev_step_) cudaEventDestroy(ev_step_);
     if (stream_) cudaStreamDestroy(stream_);
     if (side_) cudaStreamDestroy(side_);
     if (fork_) cudaEventDestroy(fork_);
@@ -345,7 +436,7 @@ void Runner::compute_geo(Region& r) const {
 
 void Runner::alloc_f(Region& r) {
     for (int p = 0; p < r.geo.nbuf; ++p) {
-        r.f[p] = static_cast<float*>(dalloc(sizeof(float) * f_alloc_floats(r.geo), false));
+        r.f[p] = static_cast<float*>(dalloc(sizeof(float) * f_alloc_floats(r.geo), false, r.dev));
         r.ptr.f[p] = r.f[p];
     }
 }
@@ -355,20 +446,21 @@ void Runner::build_regions(int) {
         compute_geo(r);
         RegionGeo& g = r.geo;
         alloc_f(r);
-        r.ptr.rho = static_cast<float*>(dalloc(sizeof(float) * g.ns));
-        r.ptr.u = static_cast<float*>(dalloc(sizeof(float) * 3ull * g.ns));
+        r.ptr.queue = static_cast<unsigned*>(dalloc(sizeof(unsigned) * 8, true, r.dev));
+        r.ptr.rho = static_cast<float*>(dalloc(sizeof(float) * g.ns, true, r.dev));
+        r.ptr.u = static_cast<float*>(dalloc(sizeof(float) * 3ull * g.ns, true, r.dev));
         if (has_solids_) {
-            r.ptr.gib = static_cast<float*>(dalloc(sizeof(float) * 3ull * g.ns));
-            r.ptr.tflag = static_cast<unsigned char*>(dalloc(g.ns + 64));
-            r.stamp = static_cast<unsigned*>(dalloc(sizeof(unsigned) * g.ns));
+            r.ptr.gib = static_cast<float*>(dalloc(sizeof(float) * 3ull * g.ns, true, r.dev));
+            r.ptr.tflag = static_cast<unsigned char*>(dalloc(g.ns + 64, true, r.dev));
+            r.stamp = static_cast<unsigned*>(dalloc(sizeof(unsigned) * g.ns, true, r.dev));
             const size_t cap = std::max<size_t>(1, std::min<size_t>(g.n, 8 * total_samples_));
-            r.band = static_cast<unsigned*>(dalloc(sizeof(unsigned) * cap));
-            r.ptr.band_count = static_cast<unsigned*>(dalloc(sizeof(unsigned)));
-            r.partial = static_cast<double*>(dalloc(sizeof(double) * 6 * 256));
+            r.band = static_cast<unsigned*>(dalloc(sizeof(unsigned) * cap, true, r.dev));
+            r.ptr.band_count = static_cast<unsigned*>(dalloc(sizeof(unsigned), true, r.dev));
+            r.partial = static_cast<double*>(dalloc(sizeof(double) * 6 * 256, true, r.dev));
             size_t blocks = 1;
             for (const auto& so : scene_.solids) blocks += size_t(std::max(1, fused_blocks(so.samples.size())));
-            r.fused_partial = static_cast<double*>(dalloc(sizeof(double) * 6 * blocks));
-            r.fused_done = static_cast<unsigned*>(dalloc(sizeof(unsigned) * scene_.solids.size()));
+            r.fused_partial = static_cast<double*>(dalloc(sizeof(double) * 6 * blocks, true, r.dev));
+            r.fused_done = static_cast<unsigned*>(dalloc(sizeof(unsigned) * scene_.solids.size(), true, r.dev));
         }
         for (int f = 0; f < 6; ++f) {
             const int a = face_axis(f);
@@ -376,26 +468,26 @@ void Runner::build_regions(int) {
             if (a == 2) present = present && ((f == 4 && r.z0 == 0) || (f == 5 && r.z1 == nz_));
             for (int p = 0; p < 2; ++p)
                 r.ptr.slot[p][f] =
-                    present ? static_cast<float*>(dalloc(sizeof(float) * 9ull * g.slot_plane(f))) : nullptr;
+                    present ? static_cast<float*>(dalloc(sizeof(float) * 9ull * g.slot_plane(f), true, r.dev)) : nullptr;
         }
         const size_t hb = sizeof(float) * 9ull * g.plane;
         for (int p = 0; p < 2; ++p) {
-            if (r.has_lo) r.recv_lo[p] = static_cast<float*>(dalloc(hb));
-            if (r.has_hi) r.recv_hi[p] = static_cast<float*>(dalloc(hb));
+            if (r.has_lo) r.recv_lo[p] = static_cast<float*>(dalloc(hb, true, r.dev));
+            if (r.has_hi) r.recv_hi[p] = static_cast<float*>(dalloc(hb, true, r.dev));
             r.ptr.recv_lo[p] = r.recv_lo[p];
             r.ptr.recv_hi[p] = r.recv_hi[p];
             if (rank_mode_) {
-                if (r.has_lo) r.own_send_lo[p] = static_cast<float*>(dalloc(hb));
-                if (r.has_hi) r.own_send_hi[p] = static_cast<float*>(dalloc(hb));
+                if (r.has_lo) r.own_send_lo[p] = static_cast<float*>(dalloc(hb, true, r.dev));
+                if (r.has_hi) r.own_send_hi[p] = static_cast<float*>(dalloc(hb, true, r.dev));
             }
         }
         if (has_solids_) {
             const size_t mb = sizeof(float) * 4ull * g.plane;
-            if (r.has_lo) r.mrecv_lo = static_cast<float*>(dalloc(mb));
-            if (r.has_hi) r.mrecv_hi = static_cast<float*>(dalloc(mb));
+            if (r.has_lo) r.mrecv_lo = static_cast<float*>(dalloc(mb, true, r.dev));
+            if (r.has_hi) r.mrecv_hi = static_cast<float*>(dalloc(mb, true, r.dev));
             if (rank_mode_) {
-                if (r.has_lo) r.own_msend_lo = static_cast<float*>(dalloc(mb));
-                if (r.has_hi) r.own_msend_hi = static_cast<float*>(dalloc(mb));
+                if (r.has_lo) r.own_msend_lo = static_cast<float*>(dalloc(mb, true, r.dev));
+                if (r.has_hi) r.own_msend_hi = static_cast<float*>(dalloc(mb, true, r.dev));
             }
             r.ptr.mrecv_lo = r.mrecv_lo;
             r.ptr.mrecv_hi = r.mrecv_hi;
@@ -437,22 +529,22 @@ void Runner::upload_solids() {
             IbSolidDev d{};
             const size_t n = s.samples.size();
             d.n = unsigned(n);
-            d.pos = static_cast<double*>(dalloc(sizeof(double) * 3 * n));
-            d.ref = static_cast<double*>(dalloc(sizeof(double) * 3 * n));
-            d.ub = static_cast<double*>(dalloc(sizeof(double) * 3 * n));
-            d.force = static_cast<double*>(dalloc(sizeof(double) * 3 * kIbHalves * n));  // parts (ib_half)
-            d.sampled = static_cast<double*>(dalloc(sizeof(double) * 3 * kIbHalves * n));
+            d.pos = static_cast<double*>(dalloc(sizeof(double) * 3 * n, true, r.dev));
+            d.ref = static_cast<double*>(dalloc(sizeof(double) * 3 * n, true, r.dev));
+            d.ub = static_cast<double*>(dalloc(sizeof(double) * 3 * n, true, r.dev));
+            d.force = static_cast<double*>(dalloc(sizeof(double) * 3 * kIbHalves * n, true, r.dev));  // parts (ib_half)
+            d.sampled = static_cast<double*>(dalloc(sizeof(double) * 3 * kIbHalves * n, true, r.dev));
             d.nbuf = r.geo.nbuf;
-            d.source = static_cast<unsigned*>(dalloc(sizeof(unsigned) * n));
-            d.flagged = static_cast<unsigned char*>(dalloc(n));
+            d.source = static_cast<unsigned*>(dalloc(sizeof(unsigned) * n, true, r.dev));
+            d.flagged = static_cast<unsigned char*>(dalloc(n, true, r.dev));
             if (scene_.cfg.ib_mode == LBMG_IB_DETERMINISTIC && n) {
-                d.rec_key = static_cast<unsigned*>(dalloc(sizeof(unsigned) * 8 * n));
-                d.rec_idx = static_cast<unsigned*>(dalloc(sizeof(unsigned) * 8 * n));
-                d.key_sorted = static_cast<unsigned*>(dalloc(sizeof(unsigned) * 8 * n));
-                d.idx_sorted = static_cast<unsigned*>(dalloc(sizeof(unsigned) * 8 * n));
-                d.rec_val = static_cast<double*>(dalloc(sizeof(double) * 24 * n));
+                d.rec_key = static_cast<unsigned*>(dalloc(sizeof(unsigned) * 8 * n, true, r.dev));
+                d.rec_idx = static_cast<unsigned*>(dalloc(sizeof(unsigned) * 8 * n, true, r.dev));
+                d.key_sorted = static_cast<unsigned*>(dalloc(sizeof(unsigned) * 8 * n, true, r.dev));
+                d.idx_sorted = static_cast<unsigned*>(dalloc(sizeof(unsigned) * 8 * n, true, r.dev));
+                d.rec_val = static_cast<double*>(dalloc(sizeof(double) * 24 * n, true, r.dev));
                 d.sort_temp_bytes = ib_det_temp_bytes(unsigned(n));
-                d.sort_temp = dalloc(d.sort_temp_bytes);
+                d.sort_temp = dalloc(d.sort_temp_bytes, true, r.dev);
             }
             std::vector<double> pos(3 * n), ref(3 * n);
             for (size_t k = 0; k < n; ++k)
@@ -472,9 +564,9 @@ void Runner::upload_solids() {
         if (ns) {
             std::vector<int> mv(ns);
             for (size_t k = 0; k < ns; ++k) mv[k] = moving_[k] ? 1 : 0;
-            r.batch_solids = static_cast<IbSolidDev*>(dalloc(sizeof(IbSolidDev) * ns));
-            r.batch_start = static_cast<unsigned*>(dalloc(sizeof(unsigned) * (ns + 1)));
-            r.batch_moving = static_cast<int*>(dalloc(sizeof(int) * ns));
+            r.batch_solids = static_cast<IbSolidDev*>(dalloc(sizeof(IbSolidDev) * ns, true, r.dev));
+            r.batch_start = static_cast<unsigned*>(dalloc(sizeof(unsigned) * (ns + 1), true, r.dev));
+            r.batch_moving = static_cast<int*>(dalloc(sizeof(int) * ns, true, r.dev));
             CK(copy_sync(r.batch_moving, mv.data(), sizeof(int) * ns, cudaMemcpyHostToDevice));
         }
     }
@@ -513,7 +605,7 @@ void Runner::build_active_lists() {
                     const int bz = std::max(0, std::min(int(std::floor(pos[3 * q + 2])), nz_ - 2));
                     if (inside && bz + 1 >= r.z0 && bz < r.z1) act.push_back(q);
                 }
-                d.active = static_cast<unsigned*>(dalloc(sizeof(unsigned) * std::max<size_t>(act.size(), 1), false));
+                d.active = static_cast<unsigned*>(dalloc(sizeof(unsigned) * std::max<size_t>(act.size(), 1), false, r.dev));
                 if (!act.empty())
                     CK(copy_sync(d.active, act.data(), sizeof(unsigned) * act.size(), cudaMemcpyHostToDevice));
                 d.n_active = unsigned(act.size());
@@ -562,8 +654,10 @@ void Runner::init_fields() {
     ip.NX = nx_;
     ip.NY = ny_;
     for (auto& r : regions_) {
+        DevGuard dg(r.dev);
         FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
-        launch_init(P, ip, stream());
+        launch_init(P, ip, rst(r));
+        CK(cudaStreamSynchronize(rst(r)));  // (init writes the neighbours' halo inputs)
     }
     fill_ghosts_full();
     CK(cudaGetLastError());
@@ -574,8 +668,11 @@ void Runner::init_fields() {
             double h[kMotionRow];
             motion_row(int(s), 0, h);
             CK(copy_sync(row, h, sizeof h, cudaMemcpyHostToDevice));
-            for (auto& r : regions_) launch_ib_motion_once(r.solids[s], row, nx_, ny_, nz_, stream());
-            CK(cudaStreamSynchronize(stream()));
+            for (auto& r : regions_) {
+                DevGuard dg(r.dev);
+                launch_ib_motion_once(r.solids[s], row, nx_, ny_, nz_, rst(r));
+                CK(cudaStreamSynchronize(rst(r)));
+            }
         }
         dfree(row);
     }
@@ -637,8 +734,10 @@ void Runner::enqueue_fluid(bool write_macro, int part) {
 void Runner::fill_ghosts_full() {
     for (auto& r : regions_)
         if (r.geo.ghost) {
+            DevGuard dg(r.dev);
             FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
-            launch_ghost_fill(P, stream(), true);
+            launch_ghost_fill(P, rst(r), true);
+            if (multi_dev_) CK(cudaStreamSynchronize(r.st));
         }
 }
 
@@ -669,7 +768,74 @@ bool Runner::fused_ib() const {
 // One step on the runner's stream.  Timing events (advance with timings):
 // [0] boundary = ghost fill (the six face passes, wraps, halos) [1] ib [2]
 // fluid = the fused stream/moments/collision kernel [3] step end [4].
+// One step with every region on its own stream (and device): the home stream
+// orders the step (chunk inputs, then step_end after every region's fluid
+// kernel); each region waits for it, fills its ghost slots, waits for its
+// neighbours' fills (its IB reads their f* across the seams), runs the fused
+// IB and the fluid kernel, whose boundary planes store straight into the
+// neighbours' halo buffers (peer memory).
+void Runner::enqueue_step_multi(bool write_macro) {
+    cudaStream_t hs = stream();
+    const int m = int(regions_.size());
+    {
+        DevGuard dg(device_);
+        CK(cudaEventRecord(ev_step_, hs));
+    }
+    for (auto& r : regions_) {
+        DevGuard dg(r.dev);
+        CK(cudaStreamWaitEvent(r.st, ev_step_, 0));
+        FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+        if (r.geo.ghost) launch_ghost_fill(P, r.st);
+        CK(cudaEventRecord(r.ev_fill, r.st));
+    }
+    if (has_solids_) {
+        const int ns = int(scene_.solids.size());
+        auto slab = [&](const Region& q) {
+            IbSlab sl{};
+            sl.g = q.geo;
+            for (int b = 0; b < 3; ++b) sl.f[b] = q.ptr.f[b];
+            return sl;
+        };
+        for (int ri = 0; ri < m; ++ri) {
+            Region& r = regions_[ri];
+            DevGuard dg(r.dev);
+            if (ri > 0) CK(cudaStreamWaitEvent(r.st, regions_[ri - 1].ev_fill, 0));
+            if (ri + 1 < m) CK(cudaStreamWaitEvent(r.st, regions_[ri + 1].ev_fill, 0));
+            FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+            IbBatch B{};
+            B.own = slab(r);
+            B.lo = ri > 0 ? slab(regions_[ri - 1]) : B.own;
+            B.hi = ri + 1 < m ? slab(regions_[ri + 1]) : B.own;
+            B.solids = r.batch_solids;
+            B.block_start = r.batch_start;
+            B.moving = r.batch_moving;
+            B.n_solids = unsigned(ns);
+            B.table = motion_tab_;
+            B.table_stride = size_t(cap_ + 2) * kMotionRow;
+            B.partial = r.fused_partial;
+            B.done = r.fused_done;
+            B.out_base = totals_dev_ + size_t(ri) * ns * 6;
+            B.out_stride = m * ns * 6;
+            launch_ib_fused(P, B, r.batch_blocks, r.solids.data(), r.st,
+                            scene_.cfg.ib_mode == LBMG_IB_DETERMINISTIC);
+        }
+    }
+    for (auto& r : regions_) {
+        DevGuard dg(r.dev);
+        FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+        launch_fluid(P, 0, write_macro, r.st, false, false);
+        CK(cudaEventRecord(r.ev_fluid, r.st));
+    }
+    DevGuard dg(device_);
+    for (auto& r : regions_) CK(cudaStreamWaitEvent(hs, r.ev_fluid, 0));
+    launch_step_end(ctr_, hs);
+}
+
 void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
+    if (multi_dev_) {
+        enqueue_step_multi(write_macro);
+        return;
+    }
     cudaStream_t st = stream();
     write_macro = write_macro || has_tracers_;  // the tracers sample u* of every step
     if (ev) CK(cudaEventRecord((*ev)[0], st));
@@ -799,11 +965,15 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
         std::vector<std::array<cudaEvent_t, 5>> evs;
         // every step graph is captured and instantiated before the first one
         // runs, so no later advance() pays a capture inside its own time
-        if (!timings) ensure_graphs();
+        if (!timings && !multi_dev_) ensure_graphs();
         for (long j = 0; j < chunk;) {
             const bool last = done + j == steps - 1;
             if (last && snap_pending_) CK(cudaStreamWaitEvent(st, snap_done_, 0));
-            if (timings) {
+            if (multi_dev_) {  // eager launches: the step spans several streams and devices
+                enqueue_step_multi(last);
+                launches_ += long(regions_.size()) * (has_solids_ ? 3 : 2) + 1;
+                ++j;
+            } else if (timings) {
                 std::vector<cudaEvent_t> e(5);
                 for (auto& x : e) CK(cudaEventCreate(&x));
                 enqueue_step(last, &e);
@@ -883,8 +1053,10 @@ void Runner::finish_chunk(long t0, long) {
         status_.reason = "divergence: non-positive or non-finite density";
         // rho*/u* of the diverging step from f(t) (solver.cpp:113-122)
         for (auto& r : regions_) {
+            DevGuard dg(r.dev);
             FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
-            launch_macro(P, t_, stream());
+            launch_macro(P, t_, rst(r));
+            CK(cudaStreamSynchronize(rst(r)));
         }
         // the reference returns before update_rigid_motion(t+1)
         if (has_solids_) {
@@ -894,8 +1066,11 @@ void Runner::finish_chunk(long t0, long) {
                 double hrow[kMotionRow];
                 motion_row(int(s), t_, hrow);
                 CK(copy_sync(row, hrow, sizeof hrow, cudaMemcpyHostToDevice));
-                for (auto& r : regions_) launch_ib_motion_once(r.solids[s], row, nx_, ny_, nz_, stream());
-                CK(cudaStreamSynchronize(stream()));
+                for (auto& r : regions_) {
+                    DevGuard dg(r.dev);
+                    launch_ib_motion_once(r.solids[s], row, nx_, ny_, nz_, rst(r));
+                    CK(cudaStreamSynchronize(rst(r)));
+                }
             }
             dfree(row);
         }
@@ -915,19 +1090,20 @@ void Runner::load_state(const double* f, const double* f_star, long t) {
     if (t < 0) throw ConfigError("load_state: the step counter must be >= 0");
     CK(cudaSetDevice(device_));
     Region& r = regions_[0];
+    DevGuard dg(r.dev);
     const size_t bytes = sizeof(double) * 27 * size_t(r.geo.n);
-    double* d = static_cast<double*>(dalloc(bytes, false));
+    double* d = static_cast<double*>(dalloc(bytes, false, r.dev));
     try {
         DevCounters h{};
         h.t = t;
         CK(copy_sync(ctr_, &h, sizeof h, cudaMemcpyHostToDevice));
         FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
         CK(copy_sync(d, f_star ? f_star : f, bytes, cudaMemcpyHostToDevice));
-        for (int p = 0; p < 2; ++p) launch_write_slots(P, p, d, stream());
-        CK(cudaStreamSynchronize(stream()));
+        for (int p = 0; p < 2; ++p) launch_write_slots(P, p, d, rst(r));
+        CK(cudaStreamSynchronize(rst(r)));
         CK(copy_sync(d, f, bytes, cudaMemcpyHostToDevice));
-        launch_write_f(P, fcur(r.geo, t), int(t & 1), d, stream());
-        CK(cudaStreamSynchronize(stream()));
+        launch_write_f(P, fcur(r.geo, t), int(t & 1), d, rst(r));
+        CK(cudaStreamSynchronize(rst(r)));
     } catch (...) {
         dfree(d);
         throw;
@@ -949,28 +1125,30 @@ void Runner::slab(int* z0, int* z1) const {
 void Runner::gather(int what, double* out) const {
     const size_t beta = what == 0 ? 1 : (what == 1 ? 3 : 27);
     const unsigned chunk = 1u << 20;
-    double* stage = nullptr;
-    CK(cudaMalloc(&stage, sizeof(double) * beta * chunk));
     const size_t base_plane = size_t(regions_.front().z0) * regions_.front().geo.plane;
-    try {
-        for (const auto& r : regions_) {
+    for (const auto& r : regions_) {
+        DevGuard dg(r.dev);
+        cudaStream_t st = rst(r);
+        double* stage = nullptr;
+        CK(cudaMalloc(&stage, sizeof(double) * beta * chunk));
+        try {
             FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
             const size_t off = size_t(r.z0) * r.geo.plane - base_plane;
             for (unsigned k0 = 0; k0 < r.geo.n; k0 += chunk) {
                 const unsigned k1 = std::min(r.geo.n, k0 + chunk);
-                if (what == 2) launch_read_f(P, fcur(r.geo, t_), k0, k1, stage, stream());
-                else launch_read_macro(P, k0, k1, what == 0 ? stage : nullptr, what == 1 ? stage : nullptr, stream());
+                if (what == 2) launch_read_f(P, fcur(r.geo, t_), k0, k1, stage, st);
+                else launch_read_macro(P, k0, k1, what == 0 ? stage : nullptr, what == 1 ? stage : nullptr, st);
                 CK(cudaGetLastError());
                 CK(cudaMemcpyAsync(out + (off + k0) * beta, stage, sizeof(double) * beta * (k1 - k0),
-                                   cudaMemcpyDeviceToHost, stream()));
-                CK(cudaStreamSynchronize(stream()));
+                                   cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
             }
+        } catch (...) {
+            cudaFree(stage);
+            throw;
         }
-    } catch (...) {
         cudaFree(stage);
-        throw;
     }
-    cudaFree(stage);
 }
 
 void Runner::snapshot_begin() {
@@ -978,6 +1156,19 @@ void Runner::snapshot_begin() {
     if (snap_pending_) CK(cudaEventSynchronize(snap_done_));
     size_t n = 0;
     for (const auto& r : regions_) n += r.geo.n;
+    if (multi_dev_) {  // slabs on several devices: a synchronous gather into pinned memory
+        if (!snap_host_) {
+            CK(cudaMallocHost(&snap_host_, sizeof(double) * 4 * n));
+            CK(cudaEventCreateWithFlags(&snap_done_, cudaEventDisableTiming));
+        }
+        for (auto& r : regions_) CK(cudaStreamSynchronize(r.st));
+        gather(0, snap_host_);
+        gather(1, snap_host_ + n);
+        CK(cudaEventRecord(snap_done_, stream()));
+        snap_pending_ = true;
+        snap_step_ = t_;
+        return;
+    }
     if (!snap_dev_) {
         snap_dev_ = static_cast<double*>(dalloc(sizeof(double) * 4 * n, false));
         CK(cudaMallocHost(&snap_host_, sizeof(double) * 4 * n));
@@ -1035,11 +1226,12 @@ void Runner::samples(int region, int solid, double* pos, double* ub, double* for
 void Runner::cell_flags(uint8_t* out) const {
     const size_t base_plane = size_t(regions_.front().z0) * regions_.front().geo.plane;
     for (const auto& r : regions_) {
+        DevGuard dg(r.dev);
         unsigned char* d = nullptr;
         CK(cudaMalloc(&d, size_t(r.geo.n) * 27));
         FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
-        launch_cell_flags(P, 0, r.geo.n, d, stream());
-        CK(cudaStreamSynchronize(stream()));
+        launch_cell_flags(P, 0, r.geo.n, d, rst(r));
+        CK(cudaStreamSynchronize(rst(r)));
         const size_t off = size_t(r.z0) * r.geo.plane - base_plane;
         cudaError_t e = copy_sync(out + off * 27, d, size_t(r.geo.n) * 27, cudaMemcpyDeviceToHost);
         cudaFree(d);
@@ -1054,6 +1246,8 @@ void Runner::set_layout(int ell, size_t alpha) {
     if (alpha < 1) throw ConfigError("layout: alpha and beta must be >= 1");
     CK(cudaSetDevice(device_));
     CK(cudaStreamSynchronize(stream()));
+    for (auto& r : regions_)
+        if (r.st) CK(cudaStreamSynchronize(r.st));
     const Layout old = layout_;
     layout_.alpha_req = alpha;
     for (auto& r : regions_) {
@@ -1066,11 +1260,12 @@ void Runner::set_layout(int ell, size_t alpha) {
         // new layout (the one holding step t first)
         float* nf[3] = {nullptr, nullptr, nullptr};
         const int src = fcur(go, t_);
+        DevGuard dg(r.dev);
         for (int b = 0; b < gn.nbuf; ++b) {
-            nf[b] = static_cast<float*>(dalloc(sizeof(float) * f_alloc_floats(gn), false));
-            launch_relayout(r.f[src], nf[b], go, gn, stream());
+            nf[b] = static_cast<float*>(dalloc(sizeof(float) * f_alloc_floats(gn), false, r.dev));
+            launch_relayout(r.f[src], nf[b], go, gn, rst(r));
         }
-        CK(cudaStreamSynchronize(stream()));
+        CK(cudaStreamSynchronize(rst(r)));
         for (int b = 0; b < 3; ++b) {
             if (b < go.nbuf) dfree(r.f[b]);
             r.f[b] = nf[b];
@@ -1147,6 +1342,8 @@ void Runner::set_layout(int ell, size_t alpha) {
 
 void Runner::set_variant(int fluid, int ib) {
     if (fluid < 0 || fluid > 1 || ib < 0 || ib > 1) throw ConfigError("set_variant: fluid and ib variants are 0 or 1");
+    if (multi_dev_ && has_solids_ && (ib != 0 || fluid != 0))
+        throw ConfigError("set_variant: slabs on several devices run the staged fluid kernel and the fused IB kernel");
     variant_ib_ = ib;
     if (fluid != variant_fluid_) {
         variant_fluid_ = fluid;
@@ -1196,7 +1393,7 @@ double Runner::measure_cost(int ell, size_t alpha, int warmup, int n_steps) {
 
 std::unique_ptr<Runner> Runner::clone() const {
     auto c = std::make_unique<Runner>(scene_, rank_mode_ ? 1 : m_global_, device_, rank_mode_ ? m_global_ : 0,
-                                      rank_);
+                                      rank_, devices_);
     c->variant_ib_ = variant_ib_;
     if (cta_) c->set_cta(cta_);
     if (variant_fluid_ != c->variant_fluid_) c->set_variant(variant_fluid_, variant_ib_);
@@ -1207,14 +1404,18 @@ std::unique_ptr<Runner> Runner::clone() const {
 
 void Runner::copy_state_from(const Runner& o) {
     CK(cudaStreamSynchronize(o.stream()));
+    for (const auto& r : o.regions_)
+        if (r.st) CK(cudaStreamSynchronize(r.st));
     cudaStream_t st = stream();
-    auto cp = [st](void* d, const void* s, size_t b) {
-        if (d && s && b) CK(cudaMemcpyAsync(d, s, b, cudaMemcpyDeviceToDevice, st));
+    auto cp = [&st](void* d, const void* s, size_t b) {
+        if (d && s && b) CK(cudaMemcpyAsync(d, s, b, cudaMemcpyDefault, st));
     };
     for (size_t ri = 0; ri < regions_.size(); ++ri) {
         Region& d = regions_[ri];
         const Region& s = o.regions_[ri];
         const RegionGeo& g = d.geo;
+        DevGuard dg(d.dev);
+        st = rst(d);
         for (int b = 0; b < g.nbuf; ++b) cp(d.f[b], s.f[b], sizeof(float) * 27ull * g.n_pad);
         for (int p = 0; p < 2; ++p) {
             cp(d.recv_lo[p], s.recv_lo[p], sizeof(float) * 9ull * g.plane);
@@ -1241,7 +1442,10 @@ void Runner::copy_state_from(const Runner& o) {
                 cp(a.flagged, b.flagged, n);
             }
         }
+        CK(cudaStreamSynchronize(st));
     }
+    CK(cudaSetDevice(device_));
+    st = stream();
     cp(ctr_, o.ctr_, sizeof(DevCounters));
     if (has_tracers_) {
         tracer_reserve(o.tn_);

@@ -53,8 +53,13 @@ struct Layout {
 class Runner {
 public:
     // world/rank: rank mode (one slab of `world`, external halo exchange).
-    // world == 0: in-process mode with `regions` slabs on one device.
-    Runner(const lbmg_scene& scene, int regions, int device, int world, int rank);
+    // world == 0: in-process mode with `regions` slabs, on `device`, or —
+    // when `devices` is given — region r on devices[r % devices.size()]
+    // (peer access between neighbouring slabs' devices: the halo stores and
+    // the IB seam reads go over NVLink; one stream per region, cross-device
+    // events per step).
+    Runner(const lbmg_scene& scene, int regions, int device, int world, int rank,
+           const std::vector<int>& devices = {});
     ~Runner();
     Runner(const Runner&) = delete;
     Runner& operator=(const Runner&) = delete;
@@ -117,6 +122,8 @@ public:
     void tracers(double* pos, int64_t* birth) const;
     void tracer_density(double* vol) const;
     void set_stream(cudaStream_t s) { ext_stream_ = s; invalidate_graphs(); }
+    int region_device(int r) const { return regions_.at(size_t(r)).dev; }
+    bool multi_device() const { return multi_dev_; }
     cudaStream_t stream() const { return ext_stream_ ? ext_stream_ : stream_; }
 
     // rank mode
@@ -132,6 +139,9 @@ private:
     };
     struct Region {
         int z0 = 0, z1 = 0;
+        int dev = 0;                       // CUDA device of the slab
+        cudaStream_t st = nullptr;         // its stream (multi-device mode)
+        cudaEvent_t ev_fill = nullptr, ev_fluid = nullptr;
         bool has_lo = false, has_hi = false;
         RegionGeo geo{};
         RegionPtrs ptr{};
@@ -157,7 +167,10 @@ private:
         FluidParams params() const;
     };
 
-    void* dalloc(size_t bytes, bool zero = true);
+    void* dalloc(size_t bytes, bool zero = true, int dev = -1);
+    cudaStream_t rst(const Region& r) const { return multi_dev_ ? r.st : stream(); }
+    cudaStream_t dev_stream(int dev) const;
+    void enqueue_step_multi(bool write_macro);
     cudaError_t copy_sync(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) const;
     void dfree(void* p);
     void build_regions(int device);
@@ -228,6 +241,9 @@ private:
     long snap_step_ = 0;
     static constexpr int kMultiSteps = 8;
     cudaGraphExec_t graph_[3] = {nullptr, nullptr, nullptr};
+    bool multi_dev_ = false;          // regions on their own streams (and devices)
+    std::vector<int> devices_;        // as given to the constructor (clone)
+    cudaEvent_t ev_step_ = nullptr;   // home stream: step inputs / previous step end
     long graph_kernels_[3] = {0, 0, 0};  // kernel nodes per graph launch
     long launches_ = 0;                  // engine kernels launched by advance()
 

@@ -60,6 +60,8 @@ def lib():
         "lbmg_split_domain": (I, [I, I, C.POINTER(I)]),
         "lbmg_runner_create": (I, [P, I, I, C.POINTER(P)]),
         "lbmg_runner_create_rank": (I, [P, I, I, I, C.POINTER(P)]),
+        "lbmg_runner_create_devices": (I, [P, I, I, C.POINTER(I), C.POINTER(P)]),
+        "lbmg_runner_region_device": (I, [P, I]),
         "lbmg_runner_destroy": (None, [P]),
         "lbmg_runner_clone": (I, [P, C.POINTER(P)]),
         "lbmg_runner_set_stream": (I, [P, P]),
@@ -289,7 +291,10 @@ class Runner:
     """lbm::Runner (runner.hpp:25-83) on the B200 engine."""
 
     def __init__(self, scene: Scene, regions: Optional[int] = None, device: int = 0, *,
-                 world: int = 0, rank: int = 0, _handle=None):
+                 world: int = 0, rank: int = 0, devices: Optional[List[int]] = None, _handle=None):
+        """regions z-slabs in this process: on `device`, or — with `devices` —
+        region r on devices[r % len(devices)] (peer-access halos, one stream
+        per slab); world/rank: one slab of a multi-process run."""
         self.scene = scene
         if _handle is not None:
             self._h = _handle
@@ -297,6 +302,10 @@ class Runner:
         h = C.c_void_p()
         if world > 0:
             _check(lib().lbmg_runner_create_rank(scene._h, world, rank, device, C.byref(h)))
+        elif devices:
+            m = scene.cfg.regions if regions is None else regions
+            arr = (C.c_int * len(devices))(*devices)
+            _check(lib().lbmg_runner_create_devices(scene._h, m, len(devices), arr, C.byref(h)))
         else:
             m = scene.cfg.regions if regions is None else regions
             _check(lib().lbmg_runner_create(scene._h, m, device, C.byref(h)))
@@ -354,6 +363,9 @@ class Runner:
 
     def region_count(self) -> int:
         return lib().lbmg_runner_region_count(self._h)
+
+    def region_device(self, region: int) -> int:
+        return int(lib().lbmg_runner_region_device(self._h, region))
 
     def set_layout(self, block_edge: int, alpha: int):
         _check(lib().lbmg_runner_set_layout(self._h, block_edge, alpha))
