@@ -357,24 +357,32 @@ __global__ void __launch_bounds__(kBulkThreads, FORM == 2 ? 4 : 3) fluid_bulk_ke
 //                      while the CTA computes the current one (two nodes per
 //                      thread, packed FFMA2 collision, 64-bit stores).  Lanes on
 //                      ghost/pad slots compute but do not store.
-// grid: x over a face's nodes, y = face * 9 + direction slot (block-uniform)
-__global__ void __launch_bounds__(256) ghost_fill_kernel(const __grid_constant__ FluidParams P) {
+// 1-D grid over the concatenated entry list: faces 0..5 in order, each
+// 9 direction slots x the face's nodes (no idle blocks for the smaller faces)
+__global__ void __launch_bounds__(256) ghost_fill_kernel(const __grid_constant__ FluidParams P, int full) {
     DevCounters* ctr = P.ctr;
     if (ctr->diverged) return;
     const RegionGeo& g = P.g;
-    const int f = int(blockIdx.y) / 9;
-    const unsigned j = blockIdx.y - 9u * unsigned(f);
-    const unsigned F = f < 2 ? unsigned(g.ny) * g.nzl : (f < 4 ? unsigned(g.nx) * g.nzl : g.plane);
-    const unsigned q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= F) return;
+    unsigned e = blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned FX = unsigned(g.ny) * g.nzl, FY = unsigned(g.nx) * g.nzl, FZ = g.plane;
+    int f = 0;
+    unsigned F = FX;
+    for (; f < 6; ++f) {
+        F = f < 2 ? FX : (f < 4 ? FY : FZ);
+        if (e < 9u * F) break;
+        e -= 9u * F;
+    }
+    if (f == 6) return;
+    const unsigned j = e / F, q = e - j * F;
     const long long t = ctr->t;
+    const bool fl = full != 0;
     switch (f) {
-        case 0: ghost_fill_entry<0>(P, t, q, j); break;
-        case 1: ghost_fill_entry<1>(P, t, q, j); break;
-        case 2: ghost_fill_entry<2>(P, t, q, j); break;
-        case 3: ghost_fill_entry<3>(P, t, q, j); break;
-        case 4: ghost_fill_entry<4>(P, t, q, j); break;
-        default: ghost_fill_entry<5>(P, t, q, j); break;
+        case 0: ghost_fill_entry<0>(P, t, q, j, fl); break;
+        case 1: ghost_fill_entry<1>(P, t, q, j, fl); break;
+        case 2: ghost_fill_entry<2>(P, t, q, j, fl); break;
+        case 3: ghost_fill_entry<3>(P, t, q, j, fl); break;
+        case 4: ghost_fill_entry<4>(P, t, q, j, fl); break;
+        default: ghost_fill_entry<5>(P, t, q, j, fl); break;
     }
 }
 
@@ -829,10 +837,11 @@ void launch_fluid_form(const FluidParams& P, int part, int write_macro, cudaStre
 }  // namespace
 
 // part: 0 every node, 1 the two halo planes (edge), 2 the rest (bulk).
-void launch_ghost_fill(const FluidParams& P, cudaStream_t st, bool) {
+void launch_ghost_fill(const FluidParams& P, cudaStream_t st, bool full) {
     const RegionGeo& g = P.g;
-    const unsigned fmax = std::max(std::max(unsigned(g.ny) * g.nzl, unsigned(g.nx) * g.nzl), g.plane);
-    ghost_fill_kernel<<<dim3(blocks_for(fmax, 256), 54), 256, 0, st>>>(P);
+    const unsigned long long entries =
+        18ull * (unsigned long long)(unsigned(g.ny) * g.nzl + unsigned(g.nx) * g.nzl + g.plane);
+    ghost_fill_kernel<<<blocks_for(entries, 256), 256, 0, st>>>(P, full ? 1 : 0);
 }
 
 bool launch_fluid(const FluidParams& P, int part, int write_macro, cudaStream_t st, bool fill, bool end_step) {

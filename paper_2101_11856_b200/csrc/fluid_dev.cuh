@@ -135,8 +135,12 @@ __device__ __forceinline__ bool slot_readable(const FluidParams& P, int x, int y
 // bounce-back (f*_i = f_{i'}(N), boundary.cpp:98-100), inlet
 // (feq(1, u_in)_i), periodic wrap / z halo (plain pull) — the outflow chain
 // through pull_source().
+// Inlet entries are constants (feq(1, u_in)_i): a full fill (init, layout
+// change, loaded state) writes their ghost slots in both population buffers;
+// the per-step fill only refreshes their (rare) outflow-readable face slots.
 template <int F>
-__device__ __forceinline__ void ghost_fill_entry(const FluidParams& P, long long t, unsigned q, unsigned j) {
+__device__ __forceinline__ void ghost_fill_entry(const FluidParams& P, long long t, unsigned q, unsigned j,
+                                                 bool full = true) {
     const int p = int(t & 1);
     const RegionGeo& g = P.g;
     constexpr int A = face_axis(F), S = face_side(F);
@@ -175,8 +179,18 @@ __device__ __forceinline__ void ghost_fill_entry(const FluidParams& P, long long
         else val = fin[g.gaddr(g.sidx(sx, sy, lzs), i)];
     } else {
         const int cond = P.faces.cond[own];
+        if (cond == kInlet) {
+            val = P.faces.inlet[own][i];
+            // the face slot of this step stays per step: at t = 0 the stale
+            // read of an inlet entry must see the initial f*, later the constant
+            if (slot_readable(P, x, y, g.gz0 + lz)) P.p.slot[p ^ 1][own][g.slot_index(own, x, y, lz, i)] = val;
+            if (full) {
+                const unsigned long long gs = g.gaddr((unsigned long long)((long long)sn - g.soff(i)), i);
+                for (int b = 0; b < g.nbuf; ++b) P.p.f[b][gs] = val;
+            }
+            return;
+        }
         if (cond == kNoSlip) val = fin[g.gaddr(sn, 27 - i)];
-        else if (cond == kInlet) val = P.faces.inlet[own][i];
         else val = *pull_source(P, t, x, y, lz, i);
         if (slot_readable(P, x, y, g.gz0 + lz)) P.p.slot[p ^ 1][own][g.slot_index(own, x, y, lz, i)] = val;
     }
