@@ -414,7 +414,6 @@ void Runner::compute_geo(Region& r) const {
         // and kWin - 1 - off_min above its last one
         g.base = round_up(g.PX + 1040u, 256u);
         unsigned slots = round_up(g.base + unsigned(g.nzl + 2) * g.PP + g.PX + 2080u, 256u);
-        if (const char* e = std::getenv("LBMG_A_PAD")) slots += 256u * unsigned(std::atoi(e));  // layout probe
         size_t areq = layout_.alpha_req;
         if (const char* e = std::getenv("LBMG_GHOST_ALPHA")) areq = std::strtoull(e, nullptr, 10);  // layout probes
         // alpha below one 256-slot tile (incl. the reference default 1) has no
