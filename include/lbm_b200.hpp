@@ -271,6 +271,11 @@ public:
     Runner(const Scene& scene, int regions, unsigned /*threads_per_region*/, int device = 0) {
         detail::check(lbmg_runner_create(scene.h_, regions, device, &h_));
     }
+    // Runner(scene, regions, threads) with region r on devices[r % size]
+    // (lbmg_runner_create_devices: halos by NVLink peer stores)
+    Runner(const Scene& scene, int regions, const std::vector<int>& devices) {
+        detail::check(lbmg_runner_create_devices(scene.h_, regions, int(devices.size()), devices.data(), &h_));
+    }
     Runner(const Runner&) = delete;
     Runner& operator=(const Runner&) = delete;
     Runner(Runner&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
@@ -281,7 +286,7 @@ public:
         if (!timings) {
             detail::check(lbmg_runner_advance(h_, steps, &st, nullptr, 0, nullptr));
         } else {
-            std::vector<lbmg_timing_row> rows(std::size_t(steps > 0 ? steps : 1) * 4);
+            std::vector<lbmg_timing_row> rows(std::size_t(steps > 0 ? steps : 1) * 5);  // <= 5 phases per step
             std::size_t n = 0;
             detail::check(lbmg_runner_advance(h_, steps, &st, rows.data(), rows.size(), &n));
             for (std::size_t k = 0; k < n; ++k) timings->push_back({rows[k].phase, rows[k].step, rows[k].seconds});
@@ -373,6 +378,14 @@ public:
         return vol;
     }
 
+    int region_device(int region) const { return lbmg_runner_region_device(h_, region); }
+
+    // SimState (solver.hpp:29-45) of a single-region runner without solids:
+    // f(t), the face-pass scratch f* (empty: f) and t
+    void load_state(const FieldStore& f, const FieldStore& f_star, long t) {
+        detail::check(lbmg_runner_load_state(h_, f.data(), f_star.size() ? f_star.data() : nullptr, t));
+    }
+
     lbmg_runner* handle() { return h_; }
 
 private:
@@ -386,6 +399,114 @@ private:
     }
     lbmg_runner* h_ = nullptr;
 };
+
+// step(SimState&, ...) (solver.hpp:82-83): one single-region step on the
+// state the runner holds (load_state / the last advance).
+inline StepStatus step(Runner& runner) {
+    lbmg_status st;
+    detail::check(lbmg_step(runner.handle(), &st));
+    return {st.ok != 0, st.mach_warning != 0, st.step, st.reason};
+}
+
+// ---- IB free functions (ib.hpp:47-128) on the device, host arrays in/out ----
+
+struct SolidSampleSet {  // ib.hpp:47-60 (per-sample arrays)
+    std::vector<Vec3> positions, boundary_velocity, penalty_force, sampled_velocity, reference_positions;
+    std::vector<std::uint32_t> source_id;
+    std::vector<std::uint8_t> flagged;
+    std::size_t size() const { return positions.size(); }
+};
+
+struct KernelSupport {  // ib.hpp:75-82
+    int base[3] = {0, 0, 0};
+    double wx[2] = {0, 0}, wy[2] = {0, 0}, wz[2] = {0, 0};
+    bool inside = true;
+    double weight(int ox, int oy, int oz) const { return wx[ox] * wy[oy] * wz[oz]; }
+};
+
+// The slab a call owns (DomainContext::global + owned planes, domain.hpp:17-24).
+struct SlabContext {
+    GridDims global;
+    int z0 = 0, z1 = -1;  // owned global planes [z0, z1); z1 < 0: the whole grid
+    int end() const { return z1 < 0 ? global.nz : z1; }
+};
+
+namespace detail {
+inline std::vector<double> flat3(const std::vector<Vec3>& v) {
+    std::vector<double> o(3 * v.size());
+    for (std::size_t k = 0; k < v.size(); ++k) put3(&o[3 * k], v[k]);
+    return o;
+}
+inline void unflat3(const std::vector<double>& o, std::vector<Vec3>& v) {
+    v.resize(o.size() / 3);
+    for (std::size_t k = 0; k < v.size(); ++k) v[k] = {o[3 * k], o[3 * k + 1], o[3 * k + 2]};
+}
+}  // namespace detail
+
+inline KernelSupport kernel_support(const Vec3& pos, const GridDims& global) {  // ib.cpp:294-308
+    double p[3];
+    detail::put3(p, pos);
+    int base[3];
+    double w[6];
+    std::uint8_t inside = 0;
+    detail::check(lbmg_ib_kernel_support(1, p, global.nx, global.ny, global.nz, base, w, &inside));
+    KernelSupport ks;
+    for (int a = 0; a < 3; ++a) ks.base[a] = base[a];
+    ks.wx[0] = w[0], ks.wx[1] = w[1], ks.wy[0] = w[2], ks.wy[1] = w[3], ks.wz[0] = w[4], ks.wz[1] = w[5];
+    ks.inside = inside != 0;
+    return ks;
+}
+
+inline void interpolate_velocity(SolidSampleSet& set, const FieldStore& u, const SlabContext& ctx) {  // ib.cpp:321-343
+    const auto pos = detail::flat3(set.positions);
+    std::vector<double> sampled(pos.size());
+    set.flagged.resize(set.size());
+    detail::check(lbmg_ib_interpolate_velocity(set.size(), pos.data(), u.data(), ctx.global.nx, ctx.global.ny,
+                                               ctx.global.nz, ctx.z0, ctx.end(), sampled.data(), set.flagged.data()));
+    detail::unflat3(sampled, set.sampled_velocity);
+}
+
+inline void penalty_forces(SolidSampleSet& set, const FieldStore& rho, const SlabContext& ctx) {  // ib.cpp:345-365
+    const auto pos = detail::flat3(set.positions), ub = detail::flat3(set.boundary_velocity),
+               us = detail::flat3(set.sampled_velocity);
+    std::vector<double> force(pos.size());
+    detail::check(lbmg_ib_penalty_forces(set.size(), pos.data(), ub.data(), us.data(),
+                                         set.flagged.empty() ? nullptr : set.flagged.data(), rho.data(),
+                                         ctx.global.nx, ctx.global.ny, ctx.global.nz, ctx.z0, ctx.end(),
+                                         force.data()));
+    detail::unflat3(force, set.penalty_force);
+}
+
+inline void spread_forces(const SolidSampleSet& set, FieldStore& g, const SlabContext& ctx) {  // ib.cpp:369-454
+    const auto pos = detail::flat3(set.positions), force = detail::flat3(set.penalty_force);
+    detail::check(lbmg_ib_spread_forces(set.size(), pos.data(), force.data(),
+                                        set.flagged.empty() ? nullptr : set.flagged.data(), ctx.global.nx,
+                                        ctx.global.ny, ctx.global.nz, ctx.z0, ctx.end(), g.data()));
+}
+
+inline void update_rigid_motion(SolidSampleSet& set, const RigidMotion& m, long t, const GridDims& global) {
+    // ib.cpp:456-489
+    const auto ref = detail::flat3(set.reference_positions);
+    double v[3], w[3], c[3];
+    detail::put3(v, m.linear_velocity);
+    detail::put3(w, m.angular_velocity);
+    detail::put3(c, m.center);
+    std::vector<double> pos(ref.size()), ub(ref.size());
+    set.flagged.resize(ref.size() / 3);
+    detail::check(lbmg_ib_update_rigid_motion(ref.size() / 3, ref.data(), v, w, c, t, global.nx, global.ny,
+                                              global.nz, pos.data(), ub.data(), set.flagged.data()));
+    detail::unflat3(pos, set.positions);
+    detail::unflat3(ub, set.boundary_velocity);
+}
+
+inline ReactionTotals reaction_totals(const SolidSampleSet& set, const Vec3& center, int z0, int z1) {
+    // ib.cpp:491-501
+    const auto pos = detail::flat3(set.positions), force = detail::flat3(set.penalty_force);
+    double c[3], out[6];
+    detail::put3(c, center);
+    detail::check(lbmg_ib_reaction_totals(set.size(), pos.data(), force.data(), c, z0, z1, out));
+    return {{out[0], out[1], out[2]}, {out[3], out[4], out[5]}};
+}
 
 // rasterize_density (tracer.hpp:43, tracer.cpp:67-92) on device 0.
 inline std::vector<double> rasterize_density(const TracerCloud& cloud, const GridDims& dims) {

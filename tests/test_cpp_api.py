@@ -63,3 +63,21 @@ def test_cpp_tune_snapshot_example_runs(tmp_path):
     for t in (10, 20, 30):
         dims, beta, rho = refpy.ref_load_field(tmp_path / f"rho_{t}.lbf", 32 * 24 * 24)
         assert dims == (32, 24, 24) and beta == 1 and abs(rho.mean() - 1.0) < 1e-2
+
+
+def test_cpp_unit_calls_example_compiles(tmp_path):
+    assert _build_example(tmp_path, "unit_calls").exists()
+
+
+@pytest.mark.gpu
+def test_cpp_unit_calls_example_runs(tmp_path):
+    exe = _build_example(tmp_path, "unit_calls")
+    res = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert res.returncode == 0, res.stderr
+    out = res.stdout
+    assert "step ok=1 t=8 max_df=0.000e+00" in out, out
+    uerr = float(out.split("uerr=")[1].split()[0])
+    spread = float(out.split("spread_err=")[1].split()[0])
+    react = float(out.split("reaction_err=")[1].split()[0])
+    assert "ib samples=64" in out and uerr <= 1e-15 and spread <= 1e-12 and react <= 1e-12, out
+    assert "devices regions=2 dev1=0 max_drho=0.000e+00" in out, out
