@@ -8,6 +8,7 @@
 //               alpha = 2^la; alpha >= n_pad is plain SoA.  A/B by step parity.
 //   rho, u      fp32 rho* and u* (u as 3 SoA planes of stride ns)
 //   gib, tflag  fp32 IB force density (3 SoA planes) + one epoch byte per node
+//   cflag       (ghost layout) one epoch byte per 64-slot storage chunk
 //   slot[2][6]  per-face persistent f* of the 9 populations each face
 //               reconstructs (needed for the stale outflow-edge read,
 //               SURVEY App. A.3), A/B by parity
@@ -159,12 +160,29 @@ struct RegionPtrs {
     // fluid kernel add a gib it already zeroed (+0), so only the true band
     // nodes of this step pay the gib loads.
     unsigned char* tflag;
+    // ghost layout: ib_epoch(step) per 64-slot storage chunk holding a node
+    // the IB scattered into at that step (same epoch rule as tflag).  The
+    // staged fluid kernel bulk-copies a tile's chunk bytes with its windows,
+    // so tiles without IB force never load gib or a per-node flag.
+    unsigned char* cflag;
     const float* mrecv_lo;  // (rho,u) of the ghost planes, 4*plane
     const float* mrecv_hi;
     float* msend_lo;
     float* msend_hi;
     unsigned* band_count;  // IB band nodes this step
     unsigned* queue;       // tile queues of the staged fluid launches: counters [4], CTAs done [4]
+    // Per-step ghost fill as a copy program (ghost layout): per step parity,
+    // fill_n[p] (src, dst) records = what ghost_fill_entry would read and
+    // write that step, resolved once (fill_ghosts_full); null: the general kernel
+    const float* inlet_g;  // 6 x 27 inlet constants (record sources)
+    const struct FillRec* fill_plan[2];
+    unsigned fill_n[2];
+};
+
+// One record of the fill program: *dst = *src.
+struct FillRec {
+    const float* src;
+    float* dst;
 };
 
 // Physical population buffer of f(t) (the A/B pair: nbuf = 2).
@@ -228,6 +246,28 @@ __device__ __forceinline__ void decode(const RegionGeo& g, unsigned k, int& x, i
     const unsigned q2 = g.div_ny.div(q);
     y = int(q - q2 * unsigned(g.ny));
     lz = int(q2);
+}
+
+// Storage chunk (64 slots: one warp's 32 node pairs of a staged tile) of a
+// ghost-layout node: the unit of cflag.  (256-slot chunks — about one grid
+// row — made the fluid kernel load and zero 7x more gib than the band needs
+// on C2: 207 vs 177 us without force.)
+constexpr int kForceChunkShift = 6;
+
+// Mark owned node k = (x, y, lz) as carrying IB force this step: its epoch
+// byte (compact-layout kernels) or its storage chunk's (ghost layout).
+__device__ __forceinline__ void mark_force(const FluidParams& P, unsigned k, int x, int y, int lz, unsigned char ep) {
+    if (P.g.ghost) P.p.cflag[P.g.sidx(x, y, lz) >> kForceChunkShift] = ep;
+    else P.p.tflag[k] = ep;
+}
+__device__ __forceinline__ void mark_force(const FluidParams& P, unsigned k, unsigned char ep) {
+    if (P.g.ghost) {
+        int x, y, lz;
+        decode(P.g, k, x, y, lz);
+        P.p.cflag[P.g.sidx(x, y, lz) >> kForceChunkShift] = ep;
+    } else {
+        P.p.tflag[k] = ep;
+    }
 }
 #endif
 

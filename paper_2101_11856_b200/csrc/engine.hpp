@@ -114,6 +114,10 @@ void launch_ib_fused(const FluidParams& P, IbBatch B, unsigned total_blocks, con
 // ghost slots of this step: full = every entry (after init / relayout),
 // otherwise only what the previous fluid step did not push
 void launch_ghost_fill(const FluidParams& P, cudaStream_t st, bool full = false);
+// Resolve the per-step fill of step parity p into copy records (out may be
+// null: count only); synchronous, returns the record count.
+unsigned launch_fill_plan(const FluidParams& P, int p, FillRec* out, unsigned cap, unsigned* count_dev,
+                          cudaStream_t st);
 // table: motion rows per step from DevCounters::chunk_t0; stride in doubles per step
 void launch_ib_totals(const FluidParams& P, const IbSolidDev& S, const double* table, double* partial,
                       double* out_base, int stride, cudaStream_t st);

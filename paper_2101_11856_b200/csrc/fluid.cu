@@ -386,6 +386,82 @@ __global__ void __launch_bounds__(256) ghost_fill_kernel(const __grid_constant__
     }
 }
 
+// The fill program of step parity p: same enumeration as ghost_fill_kernel;
+// records are appended per warp (out == null: count only).
+__global__ void __launch_bounds__(256) ghost_plan_kernel(const __grid_constant__ FluidParams P, int p, FillRec* out,
+                                                         unsigned cap, unsigned* count) {
+    const RegionGeo& g = P.g;
+    unsigned e = blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned FX = unsigned(g.ny) * g.nzl, FY = unsigned(g.nx) * g.nzl, FZ = g.plane;
+    int f = 0;
+    unsigned F = FX;
+    for (; f < 6; ++f) {
+        F = f < 2 ? FX : (f < 4 ? FY : FZ);
+        if (e < 9u * F) break;
+        e -= 9u * F;
+    }
+    FillRec rec[2];
+    int n = 0;
+    if (f < 6) {
+        const unsigned j = e / F, q = e - j * F;
+        switch (f) {
+            case 0: n = ghost_plan_entry<0>(P, p, q, j, rec); break;
+            case 1: n = ghost_plan_entry<1>(P, p, q, j, rec); break;
+            case 2: n = ghost_plan_entry<2>(P, p, q, j, rec); break;
+            case 3: n = ghost_plan_entry<3>(P, p, q, j, rec); break;
+            case 4: n = ghost_plan_entry<4>(P, p, q, j, rec); break;
+            default: n = ghost_plan_entry<5>(P, p, q, j, rec); break;
+        }
+    }
+    // warp-aggregated append: the ghost records of a warp (consecutive face
+    // nodes) stay contiguous, so the copy kernel keeps their coalescing
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned b0 = __ballot_sync(kFull, n > 0), b1 = __ballot_sync(kFull, n > 1);
+    const unsigned total = __popc(b0) + __popc(b1);
+    unsigned base = 0;
+    if (lane == 0 && total) base = atomicAdd(count, total);
+    base = __shfl_sync(kFull, base, 0);
+    if (out == nullptr) return;
+    // layout: all first records of the warp in lane order, then the second ones
+    const unsigned pos0 = base + __popc(b0 & ((1u << lane) - 1u));
+    const unsigned pos1 = base + __popc(b0) + __popc(b1 & ((1u << lane) - 1u));
+    if (n > 0 && pos0 < cap) out[pos0] = rec[0];
+    if (n > 1 && pos1 < cap) out[pos1] = rec[1];
+}
+
+// Per-step ghost fill through the program of this step's parity: every
+// record is one independent load + store (no decode, no ownership logic);
+// kFillPer records per thread with all loads in flight before the stores.
+constexpr int kFillPer = 4;
+__global__ void __launch_bounds__(256) ghost_copy_kernel(const __grid_constant__ FluidParams P) {
+    DevCounters* ctr = P.ctr;
+    if (ctr->diverged) return;
+    const int p = int(ctr->t & 1);
+    const FillRec* __restrict__ rec = P.p.fill_plan[p];
+    const unsigned n = P.p.fill_n[p];
+    const unsigned b = blockIdx.x * (blockDim.x * kFillPer) + threadIdx.x;
+    const float* src[kFillPer];
+    float* dst[kFillPer];
+#pragma unroll
+    for (int k = 0; k < kFillPer; ++k) {
+        const unsigned e = b + unsigned(k) * blockDim.x;
+        if (e < n) {
+            const ulonglong2 r = __ldg(reinterpret_cast<const ulonglong2*>(rec + e));
+            src[k] = reinterpret_cast<const float*>(r.x);
+            dst[k] = reinterpret_cast<float*>(r.y);
+        } else {
+            src[k] = nullptr;
+            dst[k] = nullptr;
+        }
+    }
+    float v[kFillPer];
+#pragma unroll
+    for (int k = 0; k < kFillPer; ++k) v[k] = src[k] != nullptr ? __ldcg(src[k]) : 0.f;
+#pragma unroll
+    for (int k = 0; k < kFillPer; ++k)
+        if (dst[k] != nullptr) *dst[k] = v[k];
+}
+
 template <int KIND, int POLICY, bool STD, int T>
 __global__ void __launch_bounds__(T, 512 / T)
     fluid_ghost_kernel(const __grid_constant__ FluidParams P, int z_a, int z_b, int slot, int write_macro, int dbg,
@@ -424,6 +500,9 @@ __global__ void __launch_bounds__(T, 512 / T)
     // other parity slot than the one phase-k readers use (no WAR hazard)
     __shared__ unsigned stage_tile[kStages][2];
     __shared__ unsigned reads_done[kStages];
+    // the tile's IB force-chunk epochs (cflag), bulk-copied with its windows
+    __shared__ __align__(16) unsigned char force_s[kStages][16];
+    const unsigned char* const cflag = P.p.cflag;
 
     // claim the next tile into stage s (elected thread); past the end the
     // stage's phase completes empty so the consumers see the end marker
@@ -436,7 +515,9 @@ __global__ void __launch_bounds__(T, 512 / T)
         }
         const long long k0 = (long long)org + (long long)tile * kTile;
         float* dst = stage0 + s * (kStageBytes / 4);
-        mbar_arrive_expect_tx(&full[s], kStageBytes);
+        mbar_arrive_expect_tx(&full[s], kStageBytes + (cflag != nullptr ? 16u : 0u));
+        if (cflag != nullptr)  // the 16 chunk bytes around the tile's (a tile spans <= 16 aligned chunks)
+            tma_load_1d(force_s[s], cflag + (((unsigned long long)k0 >> kForceChunkShift) & ~15ull), 16u, &full[s]);
         static_for<0, 27>([&](auto I) {
             constexpr int i = decltype(I)::value;
             // the window may straddle a CSoA block boundary: two segments
@@ -490,11 +571,9 @@ __global__ void __launch_bounds__(T, 512 / T)
         const int x = col - 2, y = r - 1, lz = int(pl) - 1;
         // pairs are all-ghost or all-owned (nx, PX even)
         const bool valid = sl >= sb && sl < se && x >= 0 && x < g.nx && y >= 0;
-        // IB force flag of the pair's 32-node group, loaded early (consumed
-        // after the moments, so its latency hides behind the shared-memory reads)
-        const unsigned kf = valid ? (unsigned(lz) * g.ny + unsigned(y)) * g.nx + unsigned(x) : 0u;
-        const unsigned tflag2 =
-            P.p.tflag != nullptr ? __ldcg(reinterpret_cast<const unsigned short*>(P.p.tflag + kf)) : 0u;
+        // IB force epoch of the pair's storage chunk (staged with the tile:
+        // read before this warp releases the stage)
+        const bool forced = cflag != nullptr && force_s[s][(sl >> kForceChunkShift) & 15u] == epoch;
         float2 fs[27];
         static_for<0, 27>([&](auto I) {
             constexpr int i = decltype(I)::value;
@@ -503,6 +582,17 @@ __global__ void __launch_bounds__(T, 512 / T)
             if constexpr (d % 2 == 0) fs[i] = *reinterpret_cast<const float2*>(w);
             else fs[i] = make_float2(w[0], w[1]);
         });
+        // ptxas sinks the gib loads next to their use (the collision epilogue:
+        // 127 live registers), so a forced warp would wait a full DRAM round
+        // trip there; pulling the lines into L2 here — before the stage
+        // release branch, which the scheduler does not move them across —
+        // turns that into an L2 hit
+        if (forced && valid) {
+            const unsigned kp = (unsigned(lz) * g.ny + unsigned(y)) * g.nx + unsigned(x);
+            prefetch_l2_line(P.p.gib + kp);
+            prefetch_l2_line(P.p.gib + kp + g.ns);
+            prefetch_l2_line(P.p.gib + kp + 2u * g.ns);
+        }
         __syncwarp();
         if ((tid & 31u) == 0) {
             __threadfence_block();  // this warp's reads of stage s are done
@@ -520,14 +610,22 @@ __global__ void __launch_bounds__(T, 512 / T)
         float2 gx = make_float2(P.m.body[0], P.m.body[0]);
         float2 gy = make_float2(P.m.body[1], P.m.body[1]);
         float2 gz = make_float2(P.m.body[2], P.m.body[2]);
-        if (P.p.tflag != nullptr && ((tflag2 & 0xffu) == epoch || (tflag2 >> 8) == epoch)) {
+        // (gib is zero wherever the IB did not scatter this step: every
+        // scattered node is zeroed here when consumed, so a forced chunk's
+        // other nodes add +0 and need no store)
+        if (forced) {
             float* gib = P.p.gib;
-            gx = __fadd2_rn(gx, __ldcg(reinterpret_cast<const float2*>(gib + k)));
-            gy = __fadd2_rn(gy, __ldcg(reinterpret_cast<const float2*>(gib + k + g.ns)));
-            gz = __fadd2_rn(gz, __ldcg(reinterpret_cast<const float2*>(gib + k + 2u * g.ns)));
-            *reinterpret_cast<float2*>(gib + k) = make_float2(0.f, 0.f);
-            *reinterpret_cast<float2*>(gib + k + g.ns) = make_float2(0.f, 0.f);
-            *reinterpret_cast<float2*>(gib + k + 2u * g.ns) = make_float2(0.f, 0.f);
+            const float2 a = __ldcg(reinterpret_cast<const float2*>(gib + k));
+            const float2 b = __ldcg(reinterpret_cast<const float2*>(gib + k + g.ns));
+            const float2 c = __ldcg(reinterpret_cast<const float2*>(gib + k + 2u * g.ns));
+            gx = __fadd2_rn(gx, a);
+            gy = __fadd2_rn(gy, b);
+            gz = __fadd2_rn(gz, c);
+            if (a.x != 0.f || a.y != 0.f || b.x != 0.f || b.y != 0.f || c.x != 0.f || c.y != 0.f) {
+                *reinterpret_cast<float2*>(gib + k) = make_float2(0.f, 0.f);
+                *reinterpret_cast<float2*>(gib + k + g.ns) = make_float2(0.f, 0.f);
+                *reinterpret_cast<float2*>(gib + k + 2u * g.ns) = make_float2(0.f, 0.f);
+            }
         }
         if (dbg & 3) {  // bandwidth probes: 1 = staged loads only, 2 = loads + stores (no collision)
             if ((dbg & 3) == 2)
@@ -839,9 +937,28 @@ void launch_fluid_form(const FluidParams& P, int part, int write_macro, cudaStre
 // part: 0 every node, 1 the two halo planes (edge), 2 the rest (bulk).
 void launch_ghost_fill(const FluidParams& P, cudaStream_t st, bool full) {
     const RegionGeo& g = P.g;
+    if (!full && P.p.fill_plan[0] != nullptr) {
+        const unsigned n = std::max(P.p.fill_n[0], P.p.fill_n[1]);
+        if (n) ghost_copy_kernel<<<blocks_for(n, 256u * kFillPer), 256, 0, st>>>(P);
+        return;
+    }
     const unsigned long long entries =
         18ull * (unsigned long long)(unsigned(g.ny) * g.nzl + unsigned(g.nx) * g.nzl + g.plane);
     ghost_fill_kernel<<<blocks_for(entries, 256), 256, 0, st>>>(P, full ? 1 : 0);
+}
+
+unsigned launch_fill_plan(const FluidParams& P, int p, FillRec* out, unsigned cap, unsigned* count_dev,
+                          cudaStream_t st) {
+    const RegionGeo& g = P.g;
+    const unsigned long long entries =
+        18ull * (unsigned long long)(unsigned(g.ny) * g.nzl + unsigned(g.nx) * g.nzl + g.plane);
+    CUDA_OK(cudaMemsetAsync(count_dev, 0, sizeof(unsigned), st));
+    ghost_plan_kernel<<<blocks_for(entries, 256), 256, 0, st>>>(P, p, out, cap, count_dev);
+    CUDA_OK(cudaGetLastError());
+    unsigned n = 0;
+    CUDA_OK(cudaMemcpyAsync(&n, count_dev, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    return n;
 }
 
 bool launch_fluid(const FluidParams& P, int part, int write_macro, cudaStream_t st, bool fill, bool end_step) {

@@ -78,7 +78,8 @@ __host__ __device__ constexpr int win_shift(int i) { return (4 - cx(i)) & 3; }
 // face pass `owner` reconstructs (same chain as reconstruct(): bounce-back
 // source, inlet constant in kernel-parameter space, stale slot of a later
 // face, or the streamed source of the outflow neighbour).  Never a ghost slot.
-__device__ __forceinline__ const float* pull_source(const FluidParams& P, long long t, int x, int y, int lz, int i) {
+__device__ __forceinline__ const float* pull_source(const FluidParams& P, long long t, int x, int y, int lz, int i,
+                                                   const float* inlet_g = nullptr) {
     const RegionGeo& g = P.g;
     const StepView v = make_view(P, t);
     const int p = v.p;
@@ -99,7 +100,7 @@ __device__ __forceinline__ const float* pull_source(const FluidParams& P, long l
     for (int guard = 0; guard < 7; ++guard) {
         const int cond = P.faces.cond[f];
         if (cond == kNoSlip) return v.fin + g.at(x, y, lz, opposite(i));
-        if (cond == kInlet) return &P.faces.inlet[f][i];
+        if (cond == kInlet) return inlet_g != nullptr ? inlet_g + 27 * f + i : &P.faces.inlet[f][i];
         const int a = face_axis(f), s = face_side(f);
         if (a == 0) x -= s;
         else if (a == 1) y -= s;
@@ -195,6 +196,61 @@ __device__ __forceinline__ void ghost_fill_entry(const FluidParams& P, long long
         if (slot_readable(P, x, y, g.gz0 + lz)) P.p.slot[p ^ 1][own][g.slot_index(own, x, y, lz, i)] = val;
     }
     fin[g.gaddr((unsigned long long)((long long)sn - g.soff(i)), i)] = val;
+}
+
+// The per-step (full = false) work of ghost_fill_entry<F> at step parity p as
+// copy records (the addresses it would read and write); returns how many (0..2).
+template <int F>
+__device__ __forceinline__ int ghost_plan_entry(const FluidParams& P, int p, unsigned q, unsigned j, FillRec (&rec)[2]) {
+    const RegionGeo& g = P.g;
+    constexpr int A = face_axis(F), S = face_side(F);
+    int x, y, lz;
+    if constexpr (A == 0) {
+        const unsigned qq = g.div_ny.div(q);
+        y = int(q - qq * unsigned(g.ny));
+        lz = int(qq);
+        x = S < 0 ? 0 : g.nx - 1;
+    } else {
+        const unsigned qq = g.div_nx.div(q);
+        x = int(q - qq * unsigned(g.nx));
+        if constexpr (A == 1) {
+            lz = int(qq);
+            y = S < 0 ? 0 : g.ny - 1;
+        } else {
+            y = int(qq);
+            lz = S < 0 ? 0 : g.nzl - 1;
+        }
+    }
+    const int ja = int(j % 3u) - 1, jb = int(j / 3u) - 1;
+    const int c0 = A == 0 ? -S : ja, c1 = A == 0 ? ja : (A == 1 ? -S : jb), c2 = A == 2 ? -S : jb;
+    const int i = tensor_dir((c0 + 1) + 3 * (c1 + 1) + 9 * (c2 + 1));
+    const int own = owner_face(g, x, y, g.gz0 + lz, i);
+    const unsigned sn = g.sidx(x, y, lz);
+    float* fin = P.p.f[fcur(g, p)];
+    const float* src;
+    int n = 0;
+    if (own == kNoOwner) {
+        int sx = x - c0, sy = y - c1;
+        sx += sx < 0 ? g.nx : (sx >= g.nx ? -g.nx : 0);
+        sy += sy < 0 ? g.ny : (sy >= g.ny ? -g.ny : 0);
+        const int lzs = lz - c2;
+        const unsigned hp = cross9(i, 2) * g.plane + unsigned(sy) * g.nx + unsigned(sx);
+        if (lzs < 0) src = P.p.recv_lo[p] + hp;
+        else if (lzs >= g.nzl) src = P.p.recv_hi[p] + hp;
+        else src = fin + g.gaddr(g.sidx(sx, sy, lzs), i);
+    } else {
+        const int cond = P.faces.cond[own];
+        const bool keep = slot_readable(P, x, y, g.gz0 + lz);
+        float* sdst = keep ? P.p.slot[p ^ 1][own] + g.slot_index(own, x, y, lz, i) : nullptr;
+        if (cond == kInlet) {  // ghost slots hold the constant since the full fill
+            if (keep) rec[n++] = FillRec{P.p.inlet_g + 27 * own + i, sdst};
+            return n;
+        }
+        src = cond == kNoSlip ? fin + g.gaddr(sn, 27 - i) : pull_source(P, p, x, y, lz, i, P.p.inlet_g);
+        if (keep) rec[n++] = FillRec{src, sdst};
+    }
+    rec[n++] = FillRec{src, fin + g.gaddr((unsigned long long)((long long)sn - g.soff(i)), i)};
+    return n;
 }
 
 

@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kSpreadThreads) ib_spread_kernel(const FluidPa
                             atomicAdd(&P.p.gib[key], float(w * fg[0]));
                             atomicAdd(&P.p.gib[key + g.ns], float(w * fg[1]));
                             atomicAdd(&P.p.gib[key + 2u * g.ns], float(w * fg[2]));
-                            P.p.tflag[key] = ib_epoch(P.ctr->t);
+                            mark_force(P, key, ib_epoch(P.ctr->t));
                             continue;
                         }
                         unsigned h = (key * 2654435761u) & (kHashSlots - 1);
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kSpreadThreads) ib_spread_kernel(const FluidPa
         atomicAdd(&P.p.gib[key], hval[0][j]);
         atomicAdd(&P.p.gib[key + g.ns], hval[1][j]);
         atomicAdd(&P.p.gib[key + 2u * g.ns], hval[2][j]);
-        P.p.tflag[key] = ib_epoch(P.ctr->t);
+        mark_force(P, key, ib_epoch(P.ctr->t));
     }
 }
 
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
         }
     } else if (own && !(moving & 2)) {
         for (int a = 0; a < 3; ++a) atomicAdd(&P.p.gib[k + a * g.ns], float(w * fg[a]));
-        if (!(moving & 4)) P.p.tflag[k] = ib_epoch(t);
+        if (!(moving & 4)) mark_force(P, k, x, y, gz - z0, ib_epoch(t));
     }
     if (have && corner == 0) {
         const size_t po = ib_half(S, t);
@@ -604,7 +604,7 @@ __global__ void ib_det_segment_kernel(const FluidParams P, IbSolidDev S, unsigne
     P.p.gib[k] += float(acc[0]);
     P.p.gib[k + g.ns] += float(acc[1]);
     P.p.gib[k + 2u * g.ns] += float(acc[2]);
-    P.p.tflag[k] = ib_epoch(P.ctr->t);
+    mark_force(P, k, ib_epoch(P.ctr->t));
 }
 
 size_t ib_det_temp_bytes(unsigned n_samples) {

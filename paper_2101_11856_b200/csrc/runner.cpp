@@ -451,6 +451,11 @@ void Runner::build_regions(int) {
         if (has_solids_) {
             r.ptr.gib = static_cast<float*>(dalloc(sizeof(float) * 3ull * g.ns, true, r.dev));
             r.ptr.tflag = static_cast<unsigned char*>(dalloc(g.ns + 64, true, r.dev));
+            {  // per 64-slot chunk of the ghost layout (upper bound of its slot count, any alpha)
+                const size_t px = size_t(nx_) + 4, pp = px * (size_t(ny_) + 1);
+                const size_t slots = px + 1040 + 256 + size_t(g.nzl + 2) * pp + px + 2080 + 256;
+                r.ptr.cflag = static_cast<unsigned char*>(dalloc((slots >> 6) + 64, true, r.dev));
+            }
             r.stamp = static_cast<unsigned*>(dalloc(sizeof(unsigned) * g.ns, true, r.dev));
             const size_t cap = std::max<size_t>(1, std::min<size_t>(g.n, 8 * total_samples_));
             r.band = static_cast<unsigned*>(dalloc(sizeof(unsigned) * cap, true, r.dev));
@@ -737,7 +742,47 @@ void Runner::fill_ghosts_full() {
             FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
             launch_ghost_fill(P, rst(r), true);
             if (multi_dev_) CK(cudaStreamSynchronize(r.st));
+            build_fill_plan(r);
         }
+}
+
+// The per-step ghost fill of each step parity as a copy program: resolved
+// once here (geometry, layout and buffers are fixed until the next full
+// fill), replayed by ghost_copy_kernel every step (LBMG_FILL_PLAN=0: the
+// general per-entry kernel, for A/B).
+void Runner::build_fill_plan(Region& r) {
+    static const bool off = [] {
+        const char* e = std::getenv("LBMG_FILL_PLAN");
+        return e && std::string(e) == "0";
+    }();
+    r.ptr.fill_plan[0] = r.ptr.fill_plan[1] = nullptr;
+    r.ptr.fill_n[0] = r.ptr.fill_n[1] = 0;
+    if (off || !r.geo.ghost || r.geo.nbuf != 2) return;
+    DevGuard dg(r.dev);
+    cudaStream_t st = rst(r);
+    if (!r.inlet_g) {
+        r.inlet_g = static_cast<float*>(dalloc(sizeof(float) * 6 * 27, false, r.dev));
+        CK(cudaMemcpyAsync(r.inlet_g, &faces_.inlet[0][0], sizeof(float) * 6 * 27, cudaMemcpyHostToDevice, st));
+        r.plan_count = static_cast<unsigned*>(dalloc(sizeof(unsigned), true, r.dev));
+    }
+    r.ptr.inlet_g = r.inlet_g;
+    FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+    if (!r.plan[0]) {  // the record count depends on the face geometry only
+        const unsigned n = std::max(launch_fill_plan(P, 0, nullptr, 0, r.plan_count, st),
+                                    launch_fill_plan(P, 1, nullptr, 0, r.plan_count, st));
+        r.plan_cap = std::max(n, 1u);
+        for (int p = 0; p < 2; ++p)
+            r.plan[p] = static_cast<FillRec*>(dalloc(sizeof(FillRec) * r.plan_cap, false, r.dev));
+    }
+    unsigned n[2];
+    for (int p = 0; p < 2; ++p) {
+        n[p] = launch_fill_plan(P, p, r.plan[p], r.plan_cap, r.plan_count, st);
+        if (n[p] > r.plan_cap) throw std::runtime_error("fill plan: record count changed");
+    }
+    for (int p = 0; p < 2; ++p) {
+        r.ptr.fill_plan[p] = r.plan[p];
+        r.ptr.fill_n[p] = n[p];
+    }
 }
 
 bool Runner::overlap_off() {

@@ -145,6 +145,10 @@ private:
         bool has_lo = false, has_hi = false;
         RegionGeo geo{};
         RegionPtrs ptr{};
+        FillRec* plan[2] = {nullptr, nullptr};  // per-step ghost fill programs (fill_ghosts_full)
+        unsigned plan_cap = 0;
+        unsigned* plan_count = nullptr;
+        float* inlet_g = nullptr;
         float* f[3] = {nullptr, nullptr, nullptr};
         float* recv_lo[2] = {nullptr, nullptr};
         float* recv_hi[2] = {nullptr, nullptr};
@@ -188,6 +192,7 @@ private:
     bool fused_ib() const;
     static bool overlap_off();
     void fill_ghosts_full();
+    void build_fill_plan(Region& r);
     void enqueue_fluid(bool write_macro, int part);
     void invalidate_graphs();
     void ensure_graphs();

@@ -60,6 +60,11 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
         : "memory");
 }
 
+// global -> L2 prefetch of the line holding p (no register, no completion)
+__device__ __forceinline__ void prefetch_l2_line(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // global -> L2 bulk prefetch (no destination, no completion tracking)
 __device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
