@@ -248,6 +248,37 @@ __device__ __forceinline__ void decode(const RegionGeo& g, unsigned k, int& x, i
     lz = int(q2);
 }
 
+// Per-step ghost fill through the copy program of this step's parity
+// (RegionPtrs::fill_plan): this thread's kFillPer records first + k * stride,
+// every record one independent load + store, all loads in flight before the
+// stores.  Shared by ghost_copy_kernel and the merged IB + fill launch.
+constexpr int kFillPer = 4;
+__device__ __forceinline__ void fill_copy_records(const FluidParams& P, unsigned first, unsigned stride) {
+    const int p = int(P.ctr->t & 1);
+    const FillRec* __restrict__ rec = P.p.fill_plan[p];
+    const unsigned n = P.p.fill_n[p];
+    const float* src[kFillPer];
+    float* dst[kFillPer];
+#pragma unroll
+    for (int k = 0; k < kFillPer; ++k) {
+        const unsigned e = first + unsigned(k) * stride;
+        if (e < n) {
+            const ulonglong2 r = __ldg(reinterpret_cast<const ulonglong2*>(rec + e));
+            src[k] = reinterpret_cast<const float*>(r.x);
+            dst[k] = reinterpret_cast<float*>(r.y);
+        } else {
+            src[k] = nullptr;
+            dst[k] = nullptr;
+        }
+    }
+    float v[kFillPer];
+#pragma unroll
+    for (int k = 0; k < kFillPer; ++k) v[k] = src[k] != nullptr ? __ldcg(src[k]) : 0.f;
+#pragma unroll
+    for (int k = 0; k < kFillPer; ++k)
+        if (dst[k] != nullptr) *dst[k] = v[k];
+}
+
 // Storage chunk (64 slots: one warp's 32 node pairs of a staged tile) of a
 // ghost-layout node: the unit of cflag.  (256-slot chunks — about one grid
 // row — made the fluid kernel load and zero 7x more gib than the band needs

@@ -107,9 +107,14 @@ struct IbBatch {
     double* out_base;
     int out_stride;
     int probe;
+    unsigned fill_from;            // blocks >= fill_from replay the ghost-fill program (0: none)
 };
 void launch_ib_fused(const FluidParams& P, IbBatch B, unsigned total_blocks, const IbSolidDev* host_solids,
                      cudaStream_t st, bool deterministic = false);
+// The same launch with the ghost-fill program appended as extra blocks (one
+// launch instead of a fill || IB fork/join; only when no support node can
+// touch a ghost slot and the region has a fill program).  Atomic mode.
+void launch_ib_fused_fill(const FluidParams& P, IbBatch B, unsigned total_blocks, cudaStream_t st);
 
 // ghost slots of this step: full = every entry (after init / relayout),
 // otherwise only what the previous fluid step did not push

@@ -429,37 +429,11 @@ __global__ void __launch_bounds__(256) ghost_plan_kernel(const __grid_constant__
     if (n > 1 && pos1 < cap) out[pos1] = rec[1];
 }
 
-// Per-step ghost fill through the program of this step's parity: every
-// record is one independent load + store (no decode, no ownership logic);
-// kFillPer records per thread with all loads in flight before the stores.
-constexpr int kFillPer = 4;
+// Per-step ghost fill through the program of this step's parity (no decode,
+// no ownership logic; fill_copy_records).
 __global__ void __launch_bounds__(256) ghost_copy_kernel(const __grid_constant__ FluidParams P) {
-    DevCounters* ctr = P.ctr;
-    if (ctr->diverged) return;
-    const int p = int(ctr->t & 1);
-    const FillRec* __restrict__ rec = P.p.fill_plan[p];
-    const unsigned n = P.p.fill_n[p];
-    const unsigned b = blockIdx.x * (blockDim.x * kFillPer) + threadIdx.x;
-    const float* src[kFillPer];
-    float* dst[kFillPer];
-#pragma unroll
-    for (int k = 0; k < kFillPer; ++k) {
-        const unsigned e = b + unsigned(k) * blockDim.x;
-        if (e < n) {
-            const ulonglong2 r = __ldg(reinterpret_cast<const ulonglong2*>(rec + e));
-            src[k] = reinterpret_cast<const float*>(r.x);
-            dst[k] = reinterpret_cast<float*>(r.y);
-        } else {
-            src[k] = nullptr;
-            dst[k] = nullptr;
-        }
-    }
-    float v[kFillPer];
-#pragma unroll
-    for (int k = 0; k < kFillPer; ++k) v[k] = src[k] != nullptr ? __ldcg(src[k]) : 0.f;
-#pragma unroll
-    for (int k = 0; k < kFillPer; ++k)
-        if (dst[k] != nullptr) *dst[k] = v[k];
+    if (P.ctr->diverged) return;
+    fill_copy_records(P, blockIdx.x * (blockDim.x * kFillPer) + threadIdx.x, blockDim.x);
 }
 
 template <int KIND, int POLICY, bool STD, int T>

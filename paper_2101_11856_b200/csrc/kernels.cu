@@ -279,6 +279,10 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     __shared__ bool last;
     DevCounters* ctr = P.ctr;
     if (ctr->diverged) return;
+    if (B.fill_from != 0 && blockIdx.x >= B.fill_from) {  // merged launch: the ghost-fill blocks
+        fill_copy_records(P, (blockIdx.x - B.fill_from) * (blockDim.x * kFillPer) + threadIdx.x, blockDim.x);
+        return;
+    }
     const RegionGeo& g = P.g;
     unsigned lo = 0, hi = B.n_solids;
     while (hi - lo > 1) {
@@ -650,6 +654,13 @@ void launch_ib_fused(const FluidParams& P, IbBatch B, unsigned total_blocks, con
     ib_fused_kernel<<<total_blocks, kFusedWarps * 32, 0, st>>>(P, B, deterministic ? 1 : 0);
     if (deterministic)
         for (unsigned k = 0; k < B.n_solids; ++k) launch_ib_det_reduce(P, host_solids[k], st);
+}
+void launch_ib_fused_fill(const FluidParams& P, IbBatch B, unsigned total_blocks, cudaStream_t st) {
+    const unsigned n = P.p.fill_n[0] > P.p.fill_n[1] ? P.p.fill_n[0] : P.p.fill_n[1];
+    const unsigned per = kFusedWarps * 32 * kFillPer;
+    B.probe = 0;
+    B.fill_from = total_blocks;
+    ib_fused_kernel<<<total_blocks + (n + per - 1) / per, kFusedWarps * 32, 0, st>>>(P, B, 0);
 }
 int totals_blocks(size_t n) {
     size_t b = (n + kTotThreads - 1) / kTotThreads;

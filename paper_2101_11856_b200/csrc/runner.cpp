@@ -886,18 +886,27 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
     // ghost fill || fused IB when no IB support node can touch a ghost slot
     // (a fork/join inside the captured graph); timed runs keep them serial
     const bool overlap = !ev && fused_ib() && regions_.size() == 1 && ib_overlap_ok_ && !overlap_off();
+    // ... and with a fill program in atomic mode, both in ONE launch (the
+    // fill records as extra blocks of the IB kernel: no fork/join, one launch
+    // gap less; LBMG_IB_MERGE=0 keeps the fork/join)
+    static const bool merge_off = [] {
+        const char* e = std::getenv("LBMG_IB_MERGE");
+        return e && std::string(e) == "0";
+    }();
+    const bool merged = overlap && !merge_off && scene_.cfg.ib_mode != LBMG_IB_DETERMINISTIC &&
+                        regions_[0].ptr.fill_plan[0] != nullptr;
     cudaStream_t fst = st;
-    if (overlap) {
+    if (overlap && !merged) {
         CK(cudaEventRecord(fork_, st));
         CK(cudaStreamWaitEvent(side_, fork_, 0));
         fst = side_;
     }
     for (auto& r : regions_)
-        if (r.geo.ghost) {
+        if (r.geo.ghost && !merged) {
             FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
             launch_ghost_fill(P, fst);
         }
-    if (overlap) CK(cudaEventRecord(join_, side_));
+    if (overlap && !merged) CK(cudaEventRecord(join_, side_));
     if (ev) CK(cudaEventRecord((*ev)[1], st));
     if (fused_ib()) {
         const int ns = int(scene_.solids.size()), m = int(regions_.size());
@@ -924,13 +933,14 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
             B.done = r.fused_done;
             B.out_base = totals_dev_ + size_t(ri) * ns * 6;
             B.out_stride = m * ns * 6;
-            launch_ib_fused(P, B, r.batch_blocks, r.solids.data(), st, scene_.cfg.ib_mode == LBMG_IB_DETERMINISTIC);
+            if (merged) launch_ib_fused_fill(P, B, r.batch_blocks, st);
+            else launch_ib_fused(P, B, r.batch_blocks, r.solids.data(), st, scene_.cfg.ib_mode == LBMG_IB_DETERMINISTIC);
         }
     } else if (has_solids_) {
         enqueue_ib_pre();
         enqueue_ib_mid();
     }
-    if (overlap) CK(cudaStreamWaitEvent(st, join_, 0));
+    if (overlap && !merged) CK(cudaStreamWaitEvent(st, join_, 0));
     if (ev) CK(cudaEventRecord((*ev)[2], st));
     bool ended = false;
     for (auto& r : regions_) {
