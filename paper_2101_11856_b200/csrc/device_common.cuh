@@ -176,7 +176,9 @@ struct RegionPtrs {
     // write that step, resolved once (fill_ghosts_full); null: the general kernel
     const float* inlet_g;  // 6 x 27 inlet constants (record sources)
     const struct FillRec* fill_plan[2];
-    unsigned fill_n[2];
+    unsigned fill_runs[2];  // [0, fill_runs[p]): runs of 32 consecutive records (src + k -> dst + k)
+    unsigned fill_n[2];     // [fill_eoff, fill_eoff + fill_n[p]): single records
+    unsigned fill_eoff;
 };
 
 // One record of the fill program: *dst = *src.
@@ -249,26 +251,52 @@ __device__ __forceinline__ void decode(const RegionGeo& g, unsigned k, int& x, i
 }
 
 // Per-step ghost fill through the copy program of this step's parity
-// (RegionPtrs::fill_plan): this thread's kFillPer records first + k * stride,
-// every record one independent load + store, all loads in flight before the
-// stores.  Shared by ghost_copy_kernel and the merged IB + fill launch.
+// (RegionPtrs::fill_plan), block bid of nthr threads: the first blocks copy
+// whole runs (one warp per 32-float run: one broadcast descriptor, coalesced
+// 128-byte load and store — the y/z faces), the rest single records
+// (x faces, edges, face slots).  kFillPer items per warp / thread with every
+// load in flight before the stores.  Shared by ghost_copy_kernel and the
+// merged IB + fill launch.
 constexpr int kFillPer = 4;
-__device__ __forceinline__ void fill_copy_records(const FluidParams& P, unsigned first, unsigned stride) {
+__device__ __forceinline__ unsigned fill_run_blocks(const RegionPtrs& p, unsigned nthr) {
+    const unsigned g = p.fill_runs[0] > p.fill_runs[1] ? p.fill_runs[0] : p.fill_runs[1];
+    const unsigned per = (nthr / 32u) * kFillPer;
+    return (g + per - 1) / per;
+}
+__device__ __forceinline__ void fill_copy_block(const FluidParams& P, unsigned bid, unsigned tid, unsigned nthr) {
     const int p = int(P.ctr->t & 1);
     const FillRec* __restrict__ rec = P.p.fill_plan[p];
-    const unsigned n = P.p.fill_n[p];
+    const unsigned rb = fill_run_blocks(P.p, nthr);
     const float* src[kFillPer];
     float* dst[kFillPer];
+    if (bid < rb) {
+        const unsigned lane = tid & 31u, w = bid * (nthr / 32u) + tid / 32u, ng = P.p.fill_runs[p];
 #pragma unroll
-    for (int k = 0; k < kFillPer; ++k) {
-        const unsigned e = first + unsigned(k) * stride;
-        if (e < n) {
-            const ulonglong2 r = __ldg(reinterpret_cast<const ulonglong2*>(rec + e));
-            src[k] = reinterpret_cast<const float*>(r.x);
-            dst[k] = reinterpret_cast<float*>(r.y);
-        } else {
-            src[k] = nullptr;
-            dst[k] = nullptr;
+        for (int k = 0; k < kFillPer; ++k) {
+            const unsigned e = w * kFillPer + unsigned(k);
+            if (e < ng) {
+                const ulonglong2 r = __ldg(reinterpret_cast<const ulonglong2*>(rec + e));
+                src[k] = reinterpret_cast<const float*>(r.x) + lane;
+                dst[k] = reinterpret_cast<float*>(r.y) + lane;
+            } else {
+                src[k] = nullptr;
+                dst[k] = nullptr;
+            }
+        }
+    } else {
+        const unsigned first = (bid - rb) * nthr * kFillPer + tid, n = P.p.fill_n[p];
+        rec += P.p.fill_eoff;
+#pragma unroll
+        for (int k = 0; k < kFillPer; ++k) {
+            const unsigned e = first + unsigned(k) * nthr;
+            if (e < n) {
+                const ulonglong2 r = __ldg(reinterpret_cast<const ulonglong2*>(rec + e));
+                src[k] = reinterpret_cast<const float*>(r.x);
+                dst[k] = reinterpret_cast<float*>(r.y);
+            } else {
+                src[k] = nullptr;
+                dst[k] = nullptr;
+            }
         }
     }
     float v[kFillPer];
@@ -277,6 +305,13 @@ __device__ __forceinline__ void fill_copy_records(const FluidParams& P, unsigned
 #pragma unroll
     for (int k = 0; k < kFillPer; ++k)
         if (dst[k] != nullptr) *dst[k] = v[k];
+}
+// blocks of nthr threads the fill program needs (host side too)
+inline unsigned fill_blocks(const RegionPtrs& p, unsigned nthr) {
+    const unsigned g = p.fill_runs[0] > p.fill_runs[1] ? p.fill_runs[0] : p.fill_runs[1];
+    const unsigned e = p.fill_n[0] > p.fill_n[1] ? p.fill_n[0] : p.fill_n[1];
+    const unsigned pr = (nthr / 32u) * kFillPer, pe = nthr * kFillPer;
+    return (g + pr - 1) / pr + (e + pe - 1) / pe;
 }
 
 // Storage chunk (64 slots: one warp's 32 node pairs of a staged tile) of a

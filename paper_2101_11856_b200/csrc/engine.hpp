@@ -108,6 +108,7 @@ struct IbBatch {
     int out_stride;
     int probe;
     unsigned fill_from;            // blocks >= fill_from replay the ghost-fill program (0: none)
+    IbSolidDev solo;               // solids[0] when n_solids == 1 (read from parameter space)
 };
 void launch_ib_fused(const FluidParams& P, IbBatch B, unsigned total_blocks, const IbSolidDev* host_solids,
                      cudaStream_t st, bool deterministic = false);
@@ -119,10 +120,11 @@ void launch_ib_fused_fill(const FluidParams& P, IbBatch B, unsigned total_blocks
 // ghost slots of this step: full = every entry (after init / relayout),
 // otherwise only what the previous fluid step did not push
 void launch_ghost_fill(const FluidParams& P, cudaStream_t st, bool full = false);
-// Resolve the per-step fill of step parity p into copy records (out may be
-// null: count only); synchronous, returns the record count.
-unsigned launch_fill_plan(const FluidParams& P, int p, FillRec* out, unsigned cap, unsigned* count_dev,
-                          cudaStream_t st);
+// Resolve the per-step fill of step parity p into copy records: runs at
+// out[0..), single records at out[eoff..) (out may be null: count only);
+// synchronous, counts = {runs, single records}.
+void launch_fill_plan(const FluidParams& P, int p, FillRec* out, unsigned eoff, unsigned* count_dev,
+                      unsigned counts[2], cudaStream_t st);
 // table: motion rows per step from DevCounters::chunk_t0; stride in doubles per step
 void launch_ib_totals(const FluidParams& P, const IbSolidDev& S, const double* table, double* partial,
                       double* out_base, int stride, cudaStream_t st);

@@ -386,10 +386,13 @@ __global__ void __launch_bounds__(256) ghost_fill_kernel(const __grid_constant__
     }
 }
 
-// The fill program of step parity p: same enumeration as ghost_fill_kernel;
-// records are appended per warp (out == null: count only).
+// The fill program of step parity p: same enumeration as ghost_fill_kernel.
+// A warp whose 32 entries each give one record, consecutive in source and
+// destination (a y/z face row), becomes one run at out[count[0]++]; other
+// records are appended per warp at out[eoff + count[1]++] (out == null:
+// count only).
 __global__ void __launch_bounds__(256) ghost_plan_kernel(const __grid_constant__ FluidParams P, int p, FillRec* out,
-                                                         unsigned cap, unsigned* count) {
+                                                         unsigned eoff, unsigned* count) {
     const RegionGeo& g = P.g;
     unsigned e = blockIdx.x * blockDim.x + threadIdx.x;
     const unsigned FX = unsigned(g.ny) * g.nzl, FY = unsigned(g.nx) * g.nzl, FZ = g.plane;
@@ -413,27 +416,41 @@ __global__ void __launch_bounds__(256) ghost_plan_kernel(const __grid_constant__
             default: n = ghost_plan_entry<5>(P, p, q, j, rec); break;
         }
     }
-    // warp-aggregated append: the ghost records of a warp (consecutive face
-    // nodes) stay contiguous, so the copy kernel keeps their coalescing
     const unsigned lane = threadIdx.x & 31u;
-    const unsigned b0 = __ballot_sync(kFull, n > 0), b1 = __ballot_sync(kFull, n > 1);
-    const unsigned total = __popc(b0) + __popc(b1);
+    const unsigned b0 = __ballot_sync(kFull, n > 0), b1 = __ballot_sync(kFull, n == 1);
+    const unsigned b2 = __ballot_sync(kFull, n > 1);
+    // the record that fills the ghost slot is rec[n - 1]; a run needs one
+    // record per lane (no face-slot copy) at consecutive addresses
+    const FillRec last = n > 0 ? rec[n - 1] : FillRec{nullptr, nullptr};
+    const unsigned long long s0 = __shfl_sync(kFull, (unsigned long long)last.src, 0);
+    const unsigned long long d0 = __shfl_sync(kFull, (unsigned long long)last.dst, 0);
+    const bool run = b1 == kFull && __all_sync(kFull, (unsigned long long)last.src == s0 + 4ull * lane &&
+                                                       (unsigned long long)last.dst == d0 + 4ull * lane);
+    if (run) {
+        if (lane == 0) {
+            const unsigned at = atomicAdd(&count[0], 1u);
+            if (out != nullptr && at < eoff) out[at] = last;
+        }
+        return;
+    }
+    const unsigned total = __popc(b0) + __popc(b2);
     unsigned base = 0;
-    if (lane == 0 && total) base = atomicAdd(count, total);
+    if (lane == 0 && total) base = atomicAdd(&count[1], total);
     base = __shfl_sync(kFull, base, 0);
     if (out == nullptr) return;
-    // layout: all first records of the warp in lane order, then the second ones
+    out += eoff;
+    // all first records of the warp in lane order, then the second ones
     const unsigned pos0 = base + __popc(b0 & ((1u << lane) - 1u));
-    const unsigned pos1 = base + __popc(b0) + __popc(b1 & ((1u << lane) - 1u));
-    if (n > 0 && pos0 < cap) out[pos0] = rec[0];
-    if (n > 1 && pos1 < cap) out[pos1] = rec[1];
+    const unsigned pos1 = base + __popc(b0) + __popc(b2 & ((1u << lane) - 1u));
+    if (n > 0) out[pos0] = rec[0];
+    if (n > 1) out[pos1] = rec[1];
 }
 
 // Per-step ghost fill through the program of this step's parity (no decode,
-// no ownership logic; fill_copy_records).
+// no ownership logic; fill_copy_block).
 __global__ void __launch_bounds__(256) ghost_copy_kernel(const __grid_constant__ FluidParams P) {
     if (P.ctr->diverged) return;
-    fill_copy_records(P, blockIdx.x * (blockDim.x * kFillPer) + threadIdx.x, blockDim.x);
+    fill_copy_block(P, blockIdx.x, threadIdx.x, blockDim.x);
 }
 
 template <int KIND, int POLICY, bool STD, int T>
@@ -912,8 +929,8 @@ void launch_fluid_form(const FluidParams& P, int part, int write_macro, cudaStre
 void launch_ghost_fill(const FluidParams& P, cudaStream_t st, bool full) {
     const RegionGeo& g = P.g;
     if (!full && P.p.fill_plan[0] != nullptr) {
-        const unsigned n = std::max(P.p.fill_n[0], P.p.fill_n[1]);
-        if (n) ghost_copy_kernel<<<blocks_for(n, 256u * kFillPer), 256, 0, st>>>(P);
+        const unsigned nb = fill_blocks(P.p, 256u);
+        if (nb) ghost_copy_kernel<<<nb, 256, 0, st>>>(P);
         return;
     }
     const unsigned long long entries =
@@ -921,18 +938,16 @@ void launch_ghost_fill(const FluidParams& P, cudaStream_t st, bool full) {
     ghost_fill_kernel<<<blocks_for(entries, 256), 256, 0, st>>>(P, full ? 1 : 0);
 }
 
-unsigned launch_fill_plan(const FluidParams& P, int p, FillRec* out, unsigned cap, unsigned* count_dev,
-                          cudaStream_t st) {
+void launch_fill_plan(const FluidParams& P, int p, FillRec* out, unsigned eoff, unsigned* count_dev,
+                      unsigned counts[2], cudaStream_t st) {
     const RegionGeo& g = P.g;
     const unsigned long long entries =
         18ull * (unsigned long long)(unsigned(g.ny) * g.nzl + unsigned(g.nx) * g.nzl + g.plane);
-    CUDA_OK(cudaMemsetAsync(count_dev, 0, sizeof(unsigned), st));
-    ghost_plan_kernel<<<blocks_for(entries, 256), 256, 0, st>>>(P, p, out, cap, count_dev);
+    CUDA_OK(cudaMemsetAsync(count_dev, 0, 2 * sizeof(unsigned), st));
+    ghost_plan_kernel<<<blocks_for(entries, 256), 256, 0, st>>>(P, p, out, eoff, count_dev);
     CUDA_OK(cudaGetLastError());
-    unsigned n = 0;
-    CUDA_OK(cudaMemcpyAsync(&n, count_dev, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaMemcpyAsync(counts, count_dev, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));
-    return n;
 }
 
 bool launch_fluid(const FluidParams& P, int part, int write_macro, cudaStream_t st, bool fill, bool end_step) {

@@ -278,11 +278,14 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     __shared__ double red[kFusedSamples][6];
     __shared__ bool last;
     DevCounters* ctr = P.ctr;
-    if (ctr->diverged) return;
     if (B.fill_from != 0 && blockIdx.x >= B.fill_from) {  // merged launch: the ghost-fill blocks
-        fill_copy_records(P, (blockIdx.x - B.fill_from) * (blockDim.x * kFillPer) + threadIdx.x, blockDim.x);
+        if (ctr->diverged) return;
+        fill_copy_block(P, blockIdx.x - B.fill_from, threadIdx.x, blockDim.x);
         return;
     }
+    // (the divergence check waits below the sample loads: they are valid
+    // either way, and the chain of dependent loads is this kernel's latency)
+    const unsigned diverged = ctr->diverged;
     const RegionGeo& g = P.g;
     unsigned lo = 0, hi = B.n_solids;
     while (hi - lo > 1) {
@@ -291,7 +294,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
         else hi = mid;
     }
     const unsigned solid = lo;
-    const IbSolidDev S = B.solids[solid];
+    const IbSolidDev S = B.n_solids == 1 ? B.solo : B.solids[solid];  // (one solid: from parameter space)
     const double* table = B.table + size_t(solid) * B.table_stride;
     const int moving = B.moving[solid] | B.probe;
     const unsigned b0 = B.block_start[solid], nblk = B.block_start[solid + 1] - b0;
@@ -312,6 +315,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     const double pos[3] = {have ? S.pos[3 * s] : 0.0, have ? S.pos[3 * s + 1] : 0.0, have ? S.pos[3 * s + 2] : 0.0};
     const double ub[3] = {have ? S.ub[3 * s] : 0.0, have ? S.ub[3 * s + 1] : 0.0,
                           have ? S.ub[3 * s + 2] : 0.0};  // (issued early)
+    if (diverged) return;  // block-uniform (set only by the fluid kernel, which runs after)
     const Support ks = kernel_support(pos, g.nx, g.ny, g.NZ);
     if (have && corner == 0) S.flagged[s] = ks.inside ? 0 : 1;
     const int z0 = g.gz0, z1 = g.gz0 + g.nzl;
@@ -656,11 +660,9 @@ void launch_ib_fused(const FluidParams& P, IbBatch B, unsigned total_blocks, con
         for (unsigned k = 0; k < B.n_solids; ++k) launch_ib_det_reduce(P, host_solids[k], st);
 }
 void launch_ib_fused_fill(const FluidParams& P, IbBatch B, unsigned total_blocks, cudaStream_t st) {
-    const unsigned n = P.p.fill_n[0] > P.p.fill_n[1] ? P.p.fill_n[0] : P.p.fill_n[1];
-    const unsigned per = kFusedWarps * 32 * kFillPer;
     B.probe = 0;
     B.fill_from = total_blocks;
-    ib_fused_kernel<<<total_blocks + (n + per - 1) / per, kFusedWarps * 32, 0, st>>>(P, B, 0);
+    ib_fused_kernel<<<total_blocks + fill_blocks(P.p, kFusedWarps * 32), kFusedWarps * 32, 0, st>>>(P, B, 0);
 }
 int totals_blocks(size_t n) {
     size_t b = (n + kTotThreads - 1) / kTotThreads;

@@ -756,33 +756,37 @@ void Runner::build_fill_plan(Region& r) {
         return e && std::string(e) == "0";
     }();
     r.ptr.fill_plan[0] = r.ptr.fill_plan[1] = nullptr;
-    r.ptr.fill_n[0] = r.ptr.fill_n[1] = 0;
+    r.ptr.fill_n[0] = r.ptr.fill_n[1] = r.ptr.fill_runs[0] = r.ptr.fill_runs[1] = 0;
     if (off || !r.geo.ghost || r.geo.nbuf != 2) return;
     DevGuard dg(r.dev);
     cudaStream_t st = rst(r);
     if (!r.inlet_g) {
         r.inlet_g = static_cast<float*>(dalloc(sizeof(float) * 6 * 27, false, r.dev));
         CK(cudaMemcpyAsync(r.inlet_g, &faces_.inlet[0][0], sizeof(float) * 6 * 27, cudaMemcpyHostToDevice, st));
-        r.plan_count = static_cast<unsigned*>(dalloc(sizeof(unsigned), true, r.dev));
+        r.plan_count = static_cast<unsigned*>(dalloc(2 * sizeof(unsigned), true, r.dev));
     }
     r.ptr.inlet_g = r.inlet_g;
     FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
-    if (!r.plan[0]) {  // the record count depends on the face geometry only
-        const unsigned n = std::max(launch_fill_plan(P, 0, nullptr, 0, r.plan_count, st),
-                                    launch_fill_plan(P, 1, nullptr, 0, r.plan_count, st));
-        r.plan_cap = std::max(n, 1u);
+    if (!r.plan[0]) {  // the record counts depend on the face geometry only (any buffers, layout)
+        unsigned c[2][2];
+        for (int p = 0; p < 2; ++p) launch_fill_plan(P, p, nullptr, 0, r.plan_count, c[p], st);
+        r.plan_eoff = std::max(c[0][0], c[1][0]);
+        r.plan_cap = r.plan_eoff + std::max(c[0][1], c[1][1]);
         for (int p = 0; p < 2; ++p)
-            r.plan[p] = static_cast<FillRec*>(dalloc(sizeof(FillRec) * r.plan_cap, false, r.dev));
+            r.plan[p] = static_cast<FillRec*>(dalloc(sizeof(FillRec) * std::max(r.plan_cap, 1u), false, r.dev));
     }
-    unsigned n[2];
+    unsigned c[2][2];
     for (int p = 0; p < 2; ++p) {
-        n[p] = launch_fill_plan(P, p, r.plan[p], r.plan_cap, r.plan_count, st);
-        if (n[p] > r.plan_cap) throw std::runtime_error("fill plan: record count changed");
+        launch_fill_plan(P, p, r.plan[p], r.plan_eoff, r.plan_count, c[p], st);
+        if (c[p][0] > r.plan_eoff || r.plan_eoff + c[p][1] > r.plan_cap)
+            throw std::runtime_error("fill plan: record count changed");
     }
     for (int p = 0; p < 2; ++p) {
         r.ptr.fill_plan[p] = r.plan[p];
-        r.ptr.fill_n[p] = n[p];
+        r.ptr.fill_runs[p] = c[p][0];
+        r.ptr.fill_n[p] = c[p][1];
     }
+    r.ptr.fill_eoff = r.plan_eoff;
 }
 
 bool Runner::overlap_off() {
@@ -854,6 +858,7 @@ void Runner::enqueue_step_multi(bool write_macro) {
             B.block_start = r.batch_start;
             B.moving = r.batch_moving;
             B.n_solids = unsigned(ns);
+            if (ns == 1) B.solo = r.solids[0];
             B.table = motion_tab_;
             B.table_stride = size_t(cap_ + 2) * kMotionRow;
             B.partial = r.fused_partial;
@@ -927,6 +932,7 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
             B.block_start = r.batch_start;
             B.moving = r.batch_moving;
             B.n_solids = unsigned(ns);
+            if (ns == 1) B.solo = r.solids[0];
             B.table = motion_tab_;
             B.table_stride = size_t(cap_ + 2) * kMotionRow;
             B.partial = r.fused_partial;

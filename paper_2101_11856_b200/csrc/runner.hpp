@@ -147,6 +147,7 @@ private:
         RegionPtrs ptr{};
         FillRec* plan[2] = {nullptr, nullptr};  // per-step ghost fill programs (fill_ghosts_full)
         unsigned plan_cap = 0;
+        unsigned plan_eoff = 0;
         unsigned* plan_count = nullptr;
         float* inlet_g = nullptr;
         float* f[3] = {nullptr, nullptr, nullptr};
