@@ -21,6 +21,7 @@ struct IbSolidDev {
     // static set); nullptr = all n (moving solids, deterministic mode)
     unsigned* active = nullptr;
     unsigned n_active = 0;
+    double* act_pu = nullptr;  // (pos, u_b) of active[j] at 6j: one load level less for the fused kernel
     unsigned* source;
     unsigned char* flagged;
     // deterministic accumulation (ib_accumulation = deterministic): one

@@ -312,9 +312,11 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     const unsigned n_run = S.active ? S.n_active : S.n;
     const bool have = local < n_run;
     const unsigned s = have ? (S.active ? S.active[local] : local) : 0u;
-    const double pos[3] = {have ? S.pos[3 * s] : 0.0, have ? S.pos[3 * s + 1] : 0.0, have ? S.pos[3 * s + 2] : 0.0};
-    const double ub[3] = {have ? S.ub[3 * s] : 0.0, have ? S.ub[3 * s + 1] : 0.0,
-                          have ? S.ub[3 * s + 2] : 0.0};  // (issued early)
+    // static solids: (pos, u_b) stored in run order, loaded in parallel with s
+    const double* pp = S.act_pu != nullptr ? S.act_pu + 6 * size_t(local) : S.pos + 3 * size_t(s);
+    const double* up = S.act_pu != nullptr ? pp + 3 : S.ub + 3 * size_t(s);
+    const double pos[3] = {have ? pp[0] : 0.0, have ? pp[1] : 0.0, have ? pp[2] : 0.0};
+    const double ub[3] = {have ? up[0] : 0.0, have ? up[1] : 0.0, have ? up[2] : 0.0};  // (issued early)
     if (diverged) return;  // block-uniform (set only by the fluid kernel, which runs after)
     const Support ks = kernel_support(pos, g.nx, g.ny, g.NZ);
     if (have && corner == 0) S.flagged[s] = ks.inside ? 0 : 1;

@@ -596,6 +596,10 @@ void Runner::build_active_lists() {
                 dfree(d.active);
                 d.active = nullptr;
             }
+            if (d.act_pu) {
+                dfree(d.act_pu);
+                d.act_pu = nullptr;
+            }
             d.n_active = 0;
             if (!moving_[k] && !det && d.n) {
                 std::vector<double> pos(3 * size_t(d.n));
@@ -613,6 +617,7 @@ void Runner::build_active_lists() {
                 if (!act.empty())
                     CK(copy_sync(d.active, act.data(), sizeof(unsigned) * act.size(), cudaMemcpyHostToDevice));
                 d.n_active = unsigned(act.size());
+                d.act_pu = static_cast<double*>(dalloc(sizeof(double) * 6 * std::max<size_t>(act.size(), 1), false, r.dev));
             }
             // (at least one block: it writes the solid's totals row of the region)
             start[k + 1] = start[k] + unsigned(std::max(1, fused_blocks(d.active ? d.n_active : d.n)));
@@ -623,6 +628,28 @@ void Runner::build_active_lists() {
         }
         r.batch_blocks = start[ns];
     }
+    refresh_active_pu();
+}
+
+// (pos, u_b) of the static solids' active samples in run order (the fused
+// kernel's copy); after every change of the static positions (init's
+// update_rigid_motion(0), a re-sort), same buffers so captured graphs stay valid.
+void Runner::refresh_active_pu() {
+    for (auto& r : regions_)
+        for (auto& d : r.solids) {
+            if (!d.act_pu || !d.active || !d.n_active) continue;
+            std::vector<double> pos(3 * size_t(d.n)), ub(3 * size_t(d.n)), pu(6 * size_t(d.n_active));
+            std::vector<unsigned> act(d.n_active);
+            CK(copy_sync(pos.data(), d.pos, sizeof(double) * pos.size(), cudaMemcpyDeviceToHost));
+            CK(copy_sync(ub.data(), d.ub, sizeof(double) * ub.size(), cudaMemcpyDeviceToHost));
+            CK(copy_sync(act.data(), d.active, sizeof(unsigned) * act.size(), cudaMemcpyDeviceToHost));
+            for (size_t j = 0; j < act.size(); ++j)
+                for (int a = 0; a < 3; ++a) {
+                    pu[6 * j + a] = pos[3 * size_t(act[j]) + a];
+                    pu[6 * j + 3 + a] = ub[3 * size_t(act[j]) + a];
+                }
+            CK(copy_sync(d.act_pu, pu.data(), sizeof(double) * pu.size(), cudaMemcpyHostToDevice));
+        }
 }
 
 // Rigid motion row at step t (ib.cpp:456-475): centre(t) and Rodrigues R(t)
@@ -679,6 +706,7 @@ void Runner::init_fields() {
             }
         }
         dfree(row);
+        refresh_active_pu();
     }
     CK(cudaStreamSynchronize(stream()));
 }
@@ -767,19 +795,24 @@ void Runner::build_fill_plan(Region& r) {
     }
     r.ptr.inlet_g = r.inlet_g;
     FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
-    if (!r.plan[0]) {  // the record counts depend on the face geometry only (any buffers, layout)
+    {  // counts first: how many rows form runs depends on the layout (Eq. 9 block edges)
         unsigned c[2][2];
         for (int p = 0; p < 2; ++p) launch_fill_plan(P, p, nullptr, 0, r.plan_count, c[p], st);
-        r.plan_eoff = std::max(c[0][0], c[1][0]);
-        r.plan_cap = r.plan_eoff + std::max(c[0][1], c[1][1]);
-        for (int p = 0; p < 2; ++p)
-            r.plan[p] = static_cast<FillRec*>(dalloc(sizeof(FillRec) * std::max(r.plan_cap, 1u), false, r.dev));
+        const unsigned eoff = std::max(c[0][0], c[1][0]), cap = eoff + std::max(c[0][1], c[1][1]);
+        if (!r.plan[0] || cap > r.plan_cap) {  // (callers re-capture their step graphs after a full fill)
+            for (int p = 0; p < 2; ++p) {
+                if (r.plan[p]) dfree(r.plan[p]);
+                r.plan[p] = static_cast<FillRec*>(dalloc(sizeof(FillRec) * std::max(cap, 1u), false, r.dev));
+            }
+            r.plan_cap = cap;
+        }
+        r.plan_eoff = eoff;
     }
     unsigned c[2][2];
     for (int p = 0; p < 2; ++p) {
         launch_fill_plan(P, p, r.plan[p], r.plan_eoff, r.plan_count, c[p], st);
         if (c[p][0] > r.plan_eoff || r.plan_eoff + c[p][1] > r.plan_cap)
-            throw std::runtime_error("fill plan: record count changed");
+            throw std::runtime_error("fill plan: record count changed between passes");
     }
     for (int p = 0; p < 2; ++p) {
         r.ptr.fill_plan[p] = r.plan[p];

@@ -194,6 +194,7 @@ private:
     static bool overlap_off();
     void fill_ghosts_full();
     void build_fill_plan(Region& r);
+    void refresh_active_pu();
     void enqueue_fluid(bool write_macro, int part);
     void invalidate_graphs();
     void ensure_graphs();
