@@ -110,7 +110,11 @@ def main():
             md.append(f"| `{short}` | {v['time'] * 1e6:.1f} | {v['dram_read'] / 1e6:.1f} | {v['dram_write'] / 1e6:.1f} | "
                       f"{v['dram_pct']:.1f} | {int(v['regs'])} | {v['warps_active_pct']:.1f} | {v['issue_pct']:.1f} | "
                       f"{v['fma_pipe_pct']:.1f} | {st} |")
-            if ("fluid_bulk" in short or "fluid_ghost" in short) and (best is None or v["time"] > best["time"]):
+            # the steady-state step: the launch with the least DRAM traffic (a
+            # launch that also stores rho*/u* moves 16 B/node more)
+            tr = v["dram_read"] + v["dram_write"]
+            if ("fluid_bulk" in short or "fluid_ghost" in short) and (
+                    best is None or tr < best["dram_read"] + best["dram_write"]):
                 best = dict(v, kernel=short)
         md.append("")
         if best:
