@@ -1025,10 +1025,36 @@ void Runner::ensure_graphs() {
     }
 }
 
+bool Runner::lazy_macro() {
+    static const bool on = [] {
+        const char* e = std::getenv("LBMG_LAZY_MACRO");
+        return !(e && std::string(e) == "0");
+    }();
+    return on;
+}
+
+// The moments-phase rho*, u* of step macro_t_ from f(macro_t_) (the A/B
+// buffer the step read, the ghost slots and face slots it used): the same
+// values the fluid kernel computed in that step, bit for bit (scalar and
+// packed moments are identical per node).
+void Runner::ensure_macro() const {
+    if (!macro_pending_) return;
+    macro_pending_ = false;
+    for (const auto& r : regions_) {
+        DevGuard dg(r.dev);
+        FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+        launch_macro(P, macro_t_, rst(r));
+        CK(cudaStreamSynchronize(rst(r)));
+    }
+}
+
 Status Runner::advance(long steps, std::vector<Timing>* timings) {
     if (!status_.ok || steps <= 0) return status_;
     cudaStream_t st = stream();
     CK(cudaSetDevice(device_));
+    // the step graphs' last step stores rho*/u* unless they are produced on demand
+    const bool lazy = lazy_macro() && !has_tracers_ && !multi_dev_ && !timings;
+    macro_pending_ = false;  // superseded: readers see this advance's last step
     long done = 0;
     while (done < steps) {
         const long chunk = std::min(cap_, steps - done);
@@ -1078,8 +1104,9 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
                 launches_ += graph_kernels_[2];
                 j += kMultiSteps;
             } else {
-                CK(cudaGraphLaunch(graph_[last ? 1 : 0], st));
-                launches_ += graph_kernels_[last ? 1 : 0];
+                const int which = last && !lazy ? 1 : 0;
+                CK(cudaGraphLaunch(graph_[which], st));
+                launches_ += graph_kernels_[which];
                 ++j;
             }
         }
@@ -1106,6 +1133,10 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
         finish_chunk(t0, chunk);
         if (!status_.ok) break;
         done += chunk;
+    }
+    if (lazy && status_.ok && t_ > 0) {
+        macro_pending_ = true;
+        macro_t_ = t_ - 1;
     }
     return status_;
 }
@@ -1178,6 +1209,7 @@ Status Runner::step_once() {
 }
 
 void Runner::load_state(const double* f, const double* f_star, long t) {
+    ensure_macro();
     if (regions_.size() != 1 || rank_mode_ || has_solids_ || has_tracers_)
         throw StateError("load_state: a single in-process region without solids or tracers");
     if (t < 0) throw ConfigError("load_state: the step counter must be >= 0");
@@ -1216,6 +1248,7 @@ void Runner::slab(int* z0, int* z1) const {
 }
 
 void Runner::gather(int what, double* out) const {
+    if (what != 2) ensure_macro();
     const size_t beta = what == 0 ? 1 : (what == 1 ? 3 : 27);
     const unsigned chunk = 1u << 20;
     const size_t base_plane = size_t(regions_.front().z0) * regions_.front().geo.plane;
@@ -1245,6 +1278,7 @@ void Runner::gather(int what, double* out) const {
 }
 
 void Runner::snapshot_begin() {
+    ensure_macro();
     CK(cudaSetDevice(device_));
     if (snap_pending_) CK(cudaEventSynchronize(snap_done_));
     size_t n = 0;
@@ -1335,6 +1369,7 @@ void Runner::cell_flags(uint8_t* out) const {
 // Runner::set_layout (runner.cpp:252-258): permute f into the new Eq. 9
 // layout and re-sort every sample replica by the new block edge.
 void Runner::set_layout(int ell, size_t alpha) {
+    ensure_macro();
     if (ell < 1) throw ConfigError("reorder_samples: block edge must be >= 1");
     if (alpha < 1) throw ConfigError("layout: alpha and beta must be >= 1");
     CK(cudaSetDevice(device_));
@@ -1496,6 +1531,7 @@ std::unique_ptr<Runner> Runner::clone() const {
 }
 
 void Runner::copy_state_from(const Runner& o) {
+    o.ensure_macro();
     CK(cudaStreamSynchronize(o.stream()));
     for (const auto& r : o.regions_)
         if (r.st) CK(cudaStreamSynchronize(r.st));

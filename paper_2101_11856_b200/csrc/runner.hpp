@@ -240,6 +240,14 @@ private:
     char* pinned_down_ = nullptr;      // counters + totals (device -> host)
     size_t pinned_down_bytes_ = 0;
     bool downloaded_ = false;
+    // rho*/u* of the last advanced step are produced on demand: the step
+    // graphs do not store them (16 B/node less on the last step of every
+    // advance); macro_kernel recomputes them bit-identically from f(t) of
+    // that step (still resident in its A/B buffer) when something reads them
+    mutable bool macro_pending_ = false;
+    long macro_t_ = 0;
+    void ensure_macro() const;
+    static bool lazy_macro();
     cudaStream_t copy_ = nullptr;
     cudaEvent_t snap_ready_ = nullptr, snap_done_ = nullptr;
     double* snap_dev_ = nullptr;   // rho (n) then u (3n), canonical order of this runner's slabs
