@@ -179,6 +179,16 @@ struct RegionPtrs {
     unsigned fill_runs[2];  // [0, fill_runs[p]): runs of 32 consecutive records (src + k -> dst + k)
     unsigned fill_n[2];     // [fill_eoff, fill_eoff + fill_n[p]): single records
     unsigned fill_eoff;
+    // Reaction totals of the fused IB kernel of this step, summed by the
+    // fluid kernel (its CTA k, k += grid, before its first tile): solid k's
+    // block partials [ib_start[k], ib_start[k+1]) x 6 in the fixed order
+    // (thread v of 128 takes blocks v, v + 128, ..., then a tree), row
+    // (t - chunk_t0) at ib_out + row * ib_stride + 6k.  ib_solids = 0: none.
+    const double* ib_partial;
+    const unsigned* ib_start;
+    double* ib_out;
+    unsigned ib_solids;
+    int ib_stride;
 };
 
 // One record of the fill program: *dst = *src.

@@ -522,6 +522,26 @@ __global__ void __launch_bounds__(T, 512 / T)
     };
     // consumer release: the last warp to finish reading a stage refills it
     // (no CTA-wide barrier per tile: warps never wait for the slowest one)
+    // the fused IB kernel's reaction totals of this step (RegionPtrs::ib_partial):
+    // shared memory of the not yet filled stages as scratch, before the first refill
+    for (unsigned k = blockIdx.x; k < P.p.ib_solids; k += gridDim.x) {
+        double* tree = reinterpret_cast<double*>(stage0);  // [6][128]
+        const unsigned b0 = P.p.ib_start[k], nblk = P.p.ib_start[k + 1] - b0;
+        if (tid < 128) {
+            double acc[6] = {0, 0, 0, 0, 0, 0};
+            for (unsigned b = tid; b < nblk; b += 128)
+                for (int a = 0; a < 6; ++a) acc[a] += __ldcg(&P.p.ib_partial[size_t(b0 + b) * 6 + a]);
+            for (int a = 0; a < 6; ++a) tree[a * 128 + tid] = acc[a];
+        }
+        __syncthreads();
+        for (unsigned off = 64; off > 0; off >>= 1) {
+            if (tid < off)
+                for (int a = 0; a < 6; ++a) tree[a * 128 + tid] += tree[a * 128 + tid + off];
+            __syncthreads();
+        }
+        if (tid < 6) P.p.ib_out[(t - ctr->chunk_t0) * P.p.ib_stride + 6 * k + tid] = tree[tid * 128];
+        __syncthreads();
+    }
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);

@@ -390,32 +390,18 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     if (corner == 0)
         for (int a = 0; a < 6; ++a) red[slot][a] = tot[a];
     __syncthreads();
+    // this block's partial; the fixed-order sum over the solid's blocks is
+    // the fluid kernel's (RegionPtrs::ib_partial): no fence, counter or
+    // last-block pass on this kernel's dependency chain
     if (threadIdx.x < 6) {
         double acc = 0.0;
         for (int w2 = 0; w2 < kFusedSamples; ++w2) acc += red[w2][threadIdx.x];
         partial[(blockIdx.x - b0) * 6 + threadIdx.x] = acc;
-        __threadfence();
     }
-    __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == nblk - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    // fixed-order sum of the block partials: thread t takes blocks t, t+T, ...,
-    // then a shared-memory tree (independent of which block finished last)
-    __shared__ double tree[6][kFusedWarps * 32];
-    double acc[6] = {0, 0, 0, 0, 0, 0};
-    for (unsigned b = threadIdx.x; b < nblk; b += blockDim.x)
-        for (int a = 0; a < 6; ++a) acc[a] += __ldcg(&partial[b * 6 + a]);
-    for (int a = 0; a < 6; ++a) tree[a][threadIdx.x] = acc[a];
-    __syncthreads();
-    for (unsigned off = blockDim.x / 2; off > 0; off >>= 1) {
-        if (threadIdx.x < off)
-            for (int a = 0; a < 6; ++a) tree[a][threadIdx.x] += tree[a][threadIdx.x + off];
-        __syncthreads();
-    }
-    if (threadIdx.x < 6) out_base[(t - ctr->chunk_t0) * stride + threadIdx.x] = tree[threadIdx.x][0];
-    if (threadIdx.x == 0) *done = 0u;
+    (void)done;
+    (void)out_base;
+    (void)stride;
+    (void)nblk;
 }
 
 // ---------------------------------------------------------------------------

@@ -822,6 +822,19 @@ void Runner::build_fill_plan(Region& r) {
     r.ptr.fill_eoff = r.plan_eoff;
 }
 
+// The fused IB kernel leaves per-block partials; the region's fluid kernel
+// of the same step sums them into the totals row (RegionPtrs::ib_partial).
+void Runner::set_ib_totals(FluidParams& P, int ri) const {
+    if (!fused_ib()) return;
+    const Region& r = regions_[size_t(ri)];
+    const int ns = int(scene_.solids.size()), m = int(regions_.size());
+    P.p.ib_partial = r.fused_partial;
+    P.p.ib_start = r.batch_start;
+    P.p.ib_solids = unsigned(ns);
+    P.p.ib_out = totals_dev_ + size_t(ri) * ns * 6;
+    P.p.ib_stride = m * ns * 6;
+}
+
 bool Runner::overlap_off() {
     static const bool off = [] {
         const char* e = std::getenv("LBMG_IB_OVERLAP");
@@ -905,6 +918,7 @@ void Runner::enqueue_step_multi(bool write_macro) {
     for (auto& r : regions_) {
         DevGuard dg(r.dev);
         FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+        set_ib_totals(P, int(&r - regions_.data()));
         launch_fluid(P, 0, write_macro, r.st, false, false);
         CK(cudaEventRecord(r.ev_fluid, r.st));
     }
@@ -984,6 +998,7 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
     bool ended = false;
     for (auto& r : regions_) {
         FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+        set_ib_totals(P, int(&r - regions_.data()));
         ended = launch_fluid(P, 0, write_macro, st, false, regions_.size() == 1 && !has_tracers_);
     }
     if (ev) CK(cudaEventRecord((*ev)[3], st));

@@ -195,6 +195,7 @@ private:
     void fill_ghosts_full();
     void build_fill_plan(Region& r);
     void refresh_active_pu();
+    void set_ib_totals(FluidParams& P, int ri) const;
     void enqueue_fluid(bool write_macro, int part);
     void invalidate_graphs();
     void ensure_graphs();
