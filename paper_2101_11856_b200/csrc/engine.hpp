@@ -22,6 +22,7 @@ struct IbSolidDev {
     unsigned* active = nullptr;
     unsigned n_active = 0;
     double* act_pu = nullptr;  // (pos, u_b) of active[j] at 6j: one load level less for the fused kernel
+    unsigned* corner_band = nullptr;  // band path: band index of active sample j's corner c at 8j + c (~0u: none)
     unsigned* source;
     unsigned char* flagged;
     // deterministic accumulation (ib_accumulation = deterministic): one
@@ -109,10 +110,21 @@ struct IbBatch {
     int out_stride;
     int probe;
     unsigned fill_from;            // blocks >= fill_from replay the ghost-fill program (0: none)
+    const float* band_m;           // band path: (rho* - 1, j*) per band node, 4 floats (null: gathers)
     IbSolidDev solo;               // solids[0] when n_solids == 1 (read from parameter space)
 };
 void launch_ib_fused(const FluidParams& P, IbBatch B, unsigned total_blocks, const IbSolidDev* host_solids,
                      cudaStream_t st, bool deterministic = false);
+// Band path of the fused IB kernel (static solids, one region): the sorted
+// unique support-node slots of every active sample (band, sized 8 x the
+// active samples) and each (sample, corner)'s band index in corner_band;
+// returns the band size.  Per step launch_ib_band_moments writes rho* - 1 and
+// j* of every band node (the same 27 pulls and sum order as the fused
+// kernel's gather, coalesced along rows), which the fused kernel then reads
+// per corner instead of gathering 27 populations.
+unsigned build_ib_band(const FluidParams& P, IbSolidDev* solids, size_t n_solids, unsigned* band, cudaStream_t st);
+void launch_ib_band_moments(const FluidParams& P, const unsigned* band, unsigned n, float* out, cudaStream_t st);
+
 // The same launch with the ghost-fill program appended as extra blocks (one
 // launch instead of a fill || IB fork/join; only when no support node can
 // touch a ghost slot and the region has a fill program).  Atomic mode.

@@ -17,8 +17,11 @@
 #include <cuda_runtime.h>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
 
+#include <algorithm>
 #include <cstdio>
+#include <stdexcept>
 #include <cstdlib>
 #include <string>
 
@@ -267,6 +270,67 @@ __global__ void ib_motion_once_kernel(IbSolidDev S, const double* row, int nx, i
 // (Measured alternatives, slower on C2 and configs[3]: 8-warp CTAs with a
 // shared-memory pre-aggregated scatter — 2.8 vs 1.9 ms on configs[3] — and a
 // per-CTA dedup of support nodes in shared memory — 5.0 ms.)
+// rho* - 1 and j* of one node from its 27 pulled f*: the fixed sum order the
+// fused kernel's gather and the band kernel share (bit-identical results).
+__device__ __forceinline__ void band_sums(const float (&v)[27], float& r, float& jx, float& jy, float& jz) {
+    r = jx = jy = jz = 0.f;
+#pragma unroll
+    for (int i = 0; i < 27; ++i) {
+        r += v[i];
+        jx += float(cx(i)) * v[i];
+        jy += float(cy(i)) * v[i];
+        jz += float(cz(i)) * v[i];
+    }
+}
+
+// band path setup: the slot of every (active sample, corner) of a static
+// solid on a single region (~0u: sample inactive), as the fused kernel finds it
+__global__ void ib_band_keys_kernel(const FluidParams P, IbSolidDev S, unsigned* keys) {
+    const unsigned e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= 8u * S.n_active) return;
+    const unsigned j = e >> 3, c = e & 7u;
+    const double* pp = S.act_pu + 6 * size_t(j);
+    const double pos[3] = {pp[0], pp[1], pp[2]};
+    const RegionGeo& g = P.g;
+    const Support ks = kernel_support(pos, g.nx, g.ny, g.NZ);
+    const bool act = ks.inside && sample_active(pos[2], g.NZ, g.gz0, g.gz0 + g.nzl);
+    const int ox = int(c & 1u), oy = int((c >> 1) & 1u), oz = int(c >> 2);
+    keys[e] = act ? g.sidx(ks.base[0] + ox, ks.base[1] + oy, ks.base[2] + oz - g.gz0) : ~0u;
+}
+
+__global__ void ib_band_index_kernel(const unsigned* keys, unsigned n_keys, const unsigned* band, unsigned n_band,
+                                     unsigned* out) {
+    const unsigned e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n_keys) return;
+    const unsigned key = keys[e];
+    unsigned lo = 0, hi = n_band;
+    while (lo < hi) {
+        const unsigned mid = (lo + hi) >> 1;
+        if (band[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    out[e] = key != ~0u && lo < n_band && band[lo] == key ? lo : ~0u;
+}
+
+// per step: rho* - 1, j* of every band node (band sorted by slot: consecutive
+// threads pull consecutive slots of each direction array)
+__global__ void __launch_bounds__(256) ib_band_moments_kernel(const __grid_constant__ FluidParams P,
+                                                              const unsigned* __restrict__ band, unsigned n,
+                                                              float4* __restrict__ out) {
+    if (P.ctr->diverged) return;
+    const unsigned b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= n) return;
+    const RegionGeo& g = P.g;
+    const float* fin = P.p.f[fcur(g, P.ctr->t)];
+    const long long sl = band[b];
+    float v[27];
+#pragma unroll
+    for (int i = 0; i < 27; ++i) v[i] = __ldcg(&fin[g.gaddr((unsigned long long)(sl - g.soff(i)), i)]);
+    float r, jx, jy, jz;
+    band_sums(v, r, jx, jy, jz);
+    out[b] = make_float4(r, jx, jy, jz);
+}
+
 constexpr int kFusedWarps = 4;
 constexpr int kLanesPerSample = 8;
 constexpr int kFusedSamples = kFusedWarps * 32 / kLanesPerSample;
@@ -328,18 +392,23 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     const int gz = act ? ks.base[2] + oz : z0;
     const IbSlab& R = gz < z0 ? B.lo : (gz >= z1 ? B.hi : B.own);
     const int x = act ? ks.base[0] + ox : 0, y = act ? ks.base[1] + oy : 0;
-    const float* fin = R.f[fcur(R.g, t)];
-    const long long sl = R.g.sidx(x, y, gz - R.g.gz0);
-    float v[27];
-#pragma unroll
-    for (int i = 0; i < 27; ++i) v[i] = __ldcg(&fin[R.g.gaddr((unsigned long long)(sl - R.g.soff(i)), i)]);
     float r = 0.f, jx = 0.f, jy = 0.f, jz = 0.f;
+    if (B.band_m != nullptr && S.corner_band != nullptr) {  // band path: the corner's moments, one 16-B load
+        const unsigned cb = have ? S.corner_band[8u * local + corner] : ~0u;
+        if (cb != ~0u) {
+            const float4 mm = __ldcg(reinterpret_cast<const float4*>(B.band_m) + cb);
+            r = mm.x;
+            jx = mm.y;
+            jy = mm.z;
+            jz = mm.w;
+        }
+    } else {
+        const float* fin = R.f[fcur(R.g, t)];
+        const long long sl = R.g.sidx(x, y, gz - R.g.gz0);
+        float v[27];
 #pragma unroll
-    for (int i = 0; i < 27; ++i) {
-        r += v[i];
-        jx += float(cx(i)) * v[i];
-        jy += float(cy(i)) * v[i];
-        jz += float(cz(i)) * v[i];
+        for (int i = 0; i < 27; ++i) v[i] = __ldcg(&fin[R.g.gaddr((unsigned long long)(sl - R.g.soff(i)), i)]);
+        band_sums(v, r, jx, jy, jz);
     }
     const float rho = 1.0f + r;
     const float inv = 1.0f / rho;
@@ -652,6 +721,59 @@ void launch_ib_fused_fill(const FluidParams& P, IbBatch B, unsigned total_blocks
     B.fill_from = total_blocks;
     ib_fused_kernel<<<total_blocks + fill_blocks(P.p, kFusedWarps * 32), kFusedWarps * 32, 0, st>>>(P, B, 0);
 }
+unsigned build_ib_band(const FluidParams& P, IbSolidDev* solids, size_t n_solids, unsigned* band, cudaStream_t st) {
+    size_t total = 0;
+    for (size_t k = 0; k < n_solids; ++k)
+        if (solids[k].corner_band) total += 8ull * solids[k].n_active;
+    if (total == 0) return 0;
+    unsigned *keys = nullptr, *sorted = nullptr, *count = nullptr;
+    void* temp = nullptr;
+    size_t tb_sort = 0, tb_uniq = 0;
+    auto ok = [](cudaError_t e) {
+        if (e != cudaSuccess) throw std::runtime_error(std::string("ib band: ") + cudaGetErrorString(e));
+    };
+    ok(cudaMalloc(&keys, sizeof(unsigned) * total));
+    ok(cudaMalloc(&sorted, sizeof(unsigned) * total));
+    ok(cudaMalloc(&count, sizeof(unsigned)));
+    size_t off = 0;
+    for (size_t k = 0; k < n_solids; ++k) {
+        const IbSolidDev& S = solids[k];
+        if (!S.corner_band || !S.n_active) continue;
+        ib_band_keys_kernel<<<blocks_for(8ull * S.n_active, 256), 256, 0, st>>>(P, S, keys + off);
+        off += 8ull * S.n_active;
+    }
+    cub::DeviceRadixSort::SortKeys(nullptr, tb_sort, keys, sorted, int(total), 0, 32, st);
+    cub::DeviceSelect::Unique(nullptr, tb_uniq, sorted, band, count, int(total), st);
+    ok(cudaMalloc(&temp, std::max(tb_sort, tb_uniq)));
+    cub::DeviceRadixSort::SortKeys(temp, tb_sort, keys, sorted, int(total), 0, 32, st);
+    cub::DeviceSelect::Unique(temp, tb_uniq, sorted, band, count, int(total), st);
+    unsigned n = 0;
+    ok(cudaMemcpyAsync(&n, count, sizeof n, cudaMemcpyDeviceToHost, st));
+    ok(cudaStreamSynchronize(st));
+    unsigned last = 0;
+    if (n) ok(cudaMemcpy(&last, band + n - 1, sizeof last, cudaMemcpyDeviceToHost));
+    if (n && last == ~0u) --n;  // inactive corners sort last
+    off = 0;
+    for (size_t k = 0; k < n_solids; ++k) {
+        const IbSolidDev& S = solids[k];
+        if (!S.corner_band || !S.n_active) continue;
+        ib_band_index_kernel<<<blocks_for(8ull * S.n_active, 256), 256, 0, st>>>(keys + off, 8u * S.n_active, band, n,
+                                                                              S.corner_band);
+        off += 8ull * S.n_active;
+    }
+    ok(cudaStreamSynchronize(st));
+    ok(cudaGetLastError());
+    cudaFree(keys);
+    cudaFree(sorted);
+    cudaFree(count);
+    cudaFree(temp);
+    return n;
+}
+
+void launch_ib_band_moments(const FluidParams& P, const unsigned* band, unsigned n, float* out, cudaStream_t st) {
+    if (n) ib_band_moments_kernel<<<blocks_for(n, 256), 256, 0, st>>>(P, band, n, reinterpret_cast<float4*>(out));
+}
+
 int totals_blocks(size_t n) {
     size_t b = (n + kTotThreads - 1) / kTotThreads;
     return int(b < 1 ? 1 : (b > 256 ? 256 : b));

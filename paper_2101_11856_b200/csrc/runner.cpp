@@ -600,6 +600,10 @@ void Runner::build_active_lists() {
                 dfree(d.act_pu);
                 d.act_pu = nullptr;
             }
+            if (d.corner_band) {
+                dfree(d.corner_band);
+                d.corner_band = nullptr;
+            }
             d.n_active = 0;
             if (!moving_[k] && !det && d.n) {
                 std::vector<double> pos(3 * size_t(d.n));
@@ -650,6 +654,60 @@ void Runner::refresh_active_pu() {
                 }
             CK(copy_sync(d.act_pu, pu.data(), sizeof(double) * pu.size(), cudaMemcpyHostToDevice));
         }
+    build_band_lists();
+}
+
+// Band path of the fused IB kernel: one region, atomic mode, static solids
+// with at least kBandMin active samples in total (LBMG_IB_BAND=1 / 0 forces
+// it on / off).  Below that the per-corner gathers of the fused kernel are
+// cheaper than an extra launch on the step's critical path.
+bool Runner::band_path() const {
+    static const int env = [] {
+        const char* e = std::getenv("LBMG_IB_BAND");
+        return e ? std::atoi(e) : -1;
+    }();
+    constexpr size_t kBandMin = 65536;
+    if (env == 0 || regions_.size() != 1 || multi_dev_ || rank_mode_ || !has_solids_ ||
+        scene_.cfg.ib_mode == LBMG_IB_DETERMINISTIC || !regions_[0].geo.ghost)
+        return false;
+    size_t n = 0;
+    for (const auto& d : regions_[0].solids)
+        if (d.act_pu) n += d.n_active;
+    return n > 0 && (env == 1 || n >= kBandMin);
+}
+
+void Runner::build_band_lists() {
+    for (auto& r : regions_) {
+        if (r.sband) {
+            dfree(r.sband);
+            dfree(r.sband_m);
+            r.sband = nullptr;
+            r.sband_m = nullptr;
+            r.sband_n = 0;
+        }
+        for (auto& d : r.solids)
+            if (d.corner_band) {
+                dfree(d.corner_band);
+                d.corner_band = nullptr;
+            }
+    }
+    if (!band_path()) return;
+    Region& r = regions_[0];
+    DevGuard dg(r.dev);
+    size_t total = 0;
+    for (auto& d : r.solids)
+        if (d.act_pu && d.n_active) {
+            d.corner_band = static_cast<unsigned*>(dalloc(sizeof(unsigned) * 8 * size_t(d.n_active), false, r.dev));
+            total += 8 * size_t(d.n_active);
+        }
+    unsigned* band = static_cast<unsigned*>(dalloc(sizeof(unsigned) * std::max<size_t>(total, 1), false, r.dev));
+    FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
+    const unsigned n = build_ib_band(P, r.solids.data(), r.solids.size(), band, rst(r));
+    r.sband = band;
+    r.sband_n = n;
+    r.sband_m = static_cast<float*>(dalloc(sizeof(float) * 4 * std::max<size_t>(n, 1), false, r.dev));
+    if (r.batch_solids)
+        CK(copy_sync(r.batch_solids, r.solids.data(), sizeof(IbSolidDev) * r.solids.size(), cudaMemcpyHostToDevice));
 }
 
 // Rigid motion row at step t (ib.cpp:456-475): centre(t) and Rodrigues R(t)
@@ -937,7 +995,9 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
     if (ev) CK(cudaEventRecord((*ev)[0], st));
     // ghost fill || fused IB when no IB support node can touch a ghost slot
     // (a fork/join inside the captured graph); timed runs keep them serial
-    const bool overlap = !ev && fused_ib() && regions_.size() == 1 && ib_overlap_ok_ && !overlap_off();
+    // (the band path's moments kernel reads the filled f*: fill, band moments, IB in order)
+    const bool band = fused_ib() && regions_[0].sband_n > 0;
+    const bool overlap = !ev && fused_ib() && regions_.size() == 1 && ib_overlap_ok_ && !overlap_off() && !band;
     // ... and with a fill program in atomic mode, both in ONE launch (the
     // fill records as extra blocks of the IB kernel: no fork/join, one launch
     // gap less; LBMG_IB_MERGE=0 keeps the fork/join)
@@ -986,6 +1046,10 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
             B.done = r.fused_done;
             B.out_base = totals_dev_ + size_t(ri) * ns * 6;
             B.out_stride = m * ns * 6;
+            if (band) {
+                launch_ib_band_moments(P, r.sband, r.sband_n, r.sband_m, st);
+                B.band_m = r.sband_m;
+            }
             if (merged) launch_ib_fused_fill(P, B, r.batch_blocks, st);
             else launch_ib_fused(P, B, r.batch_blocks, r.solids.data(), st, scene_.cfg.ib_mode == LBMG_IB_DETERMINISTIC);
         }

@@ -150,6 +150,9 @@ private:
         unsigned plan_eoff = 0;
         unsigned* plan_count = nullptr;
         float* inlet_g = nullptr;
+        unsigned* sband = nullptr;   // IB band path: sorted unique support-node slots of the static solids
+        unsigned sband_n = 0;
+        float* sband_m = nullptr;    // 4 floats per band node, written each step
         float* f[3] = {nullptr, nullptr, nullptr};
         float* recv_lo[2] = {nullptr, nullptr};
         float* recv_hi[2] = {nullptr, nullptr};
@@ -196,6 +199,8 @@ private:
     void build_fill_plan(Region& r);
     void refresh_active_pu();
     void set_ib_totals(FluidParams& P, int ri) const;
+    void build_band_lists();
+    bool band_path() const;
     void enqueue_fluid(bool write_macro, int part);
     void invalidate_graphs();
     void ensure_graphs();

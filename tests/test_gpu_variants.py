@@ -77,3 +77,23 @@ def test_merged_ib_fill_launch_matches_fork_join(tmp_path):
         for k in ("rho", "u", "force", "totals"):
             rel = np.linalg.norm(a[k] - other[k]) / max(np.linalg.norm(other[k]), 1e-30)
             assert rel <= 1e-4, (k, rel)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scene,kw", [
+    ("city", dict(nx=64, ny=32, nz=48, n_boxes=4)),   # static boxes on the ground (supports on ghost slots)
+    ("sphere", dict(nx=64, ny=40, nz=40, center=(24, 20, 20), radius=6.0, subdiv=3, r=0.6)),
+])
+def test_ib_band_path_matches_gathers(tmp_path, scene, kw):
+    """The fused IB kernel reading per-corner moments from the band list
+    (LBMG_IB_BAND=1; default above 64 k static samples) vs gathering the 27
+    populations per corner: the same sums in the same order, so only the fp32
+    RED arrival order differs."""
+    chunks = [10, 1, 9]
+    a = _run(tmp_path, "band", {"LBMG_IB_BAND": "1"}, scene, kw, chunks)
+    b = _run(tmp_path, "gather", {"LBMG_IB_BAND": "0"}, scene, kw, chunks)
+    assert int(a["t"][0]) == int(b["t"][0]) == sum(chunks)
+    assert np.abs(a["f"] - b["f"]).max() <= 2e-5
+    for k in ("rho", "u", "force", "totals"):
+        rel = np.linalg.norm(a[k] - b[k]) / max(np.linalg.norm(b[k]), 1e-30)
+        assert rel <= 1e-4, (k, rel)
