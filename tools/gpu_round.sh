@@ -34,3 +34,8 @@ if has ncu; then
   gzip -f $OUT/*.ncu-rep
 fi
 ls -la $OUT | tail -30
+if has ibprof; then
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ib_fused|ib_band_moments" -s 2 -c 2 \
+     -o $OUT/prof_c4ib_$TAG python bench.py --config c4 --steps 1 --warmup 2 --no-cpu-baseline > /dev/null 2>&1
+  gzip -f $OUT/*.ncu-rep
+fi
