@@ -189,6 +189,12 @@ struct RegionPtrs {
     double* ib_out;
     unsigned ib_solids;
     int ib_stride;
+    // Zero-copy results (the single-region step the fluid kernel ends): the
+    // device aliases of the mapped pinned host block advance() reads after
+    // its stream sync — the counters (written by the last CTA) and the
+    // totals rows (written next to ib_out) — so no D2H copy follows the step.
+    struct DevCounters* ctr_host;
+    double* ib_out_host;
 };
 
 // One record of the fill program: *dst = *src.

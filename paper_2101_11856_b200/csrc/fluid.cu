@@ -453,6 +453,19 @@ __global__ void __launch_bounds__(256) ghost_copy_kernel(const __grid_constant__
     fill_copy_block(P, blockIdx.x, threadIdx.x, blockDim.x);
 }
 
+// The step's counters into the mapped host block (RegionPtrs::ctr_host), by
+// the last CTA of the launch that ends the step (after every CTA's updates).
+__device__ __forceinline__ void publish_counters(const FluidParams& P) {
+    DevCounters* h = P.p.ctr_host;
+    if (h == nullptr) return;
+    const DevCounters* c = P.ctr;
+    h->t = __ldcg(&c->t);
+    h->diverged = __ldcg(&c->diverged);
+    h->mach = __ldcg(&c->mach);
+    h->diverged_step = __ldcg(&c->diverged_step);
+    h->chunk_t0 = __ldcg(&c->chunk_t0);
+}
+
 template <int KIND, int POLICY, bool STD, int T>
 __global__ void __launch_bounds__(T, 512 / T)
     fluid_ghost_kernel(const __grid_constant__ FluidParams P, int z_a, int z_b, int slot, int write_macro, int dbg,
@@ -467,6 +480,7 @@ __global__ void __launch_bounds__(T, 512 / T)
         if (threadIdx.x == 0 && atomicAdd(&P.p.queue[4 + slot], 1u) == gridDim.x - 1) {
             P.p.queue[slot] = 0u;
             P.p.queue[4 + slot] = 0u;
+            if (end_step) publish_counters(P);
         }
         return;
     }
@@ -539,7 +553,11 @@ __global__ void __launch_bounds__(T, 512 / T)
                 for (int a = 0; a < 6; ++a) tree[a * 128 + tid] += tree[a * 128 + tid + off];
             __syncthreads();
         }
-        if (tid < 6) P.p.ib_out[(t - ctr->chunk_t0) * P.p.ib_stride + 6 * k + tid] = tree[tid * 128];
+        if (tid < 6) {
+            const long long at = (t - ctr->chunk_t0) * P.p.ib_stride + 6 * k + tid;
+            P.p.ib_out[at] = tree[tid * 128];
+            if (P.p.ib_out_host != nullptr) P.p.ib_out_host[at] = tree[tid * 128];  // (zero-copy row)
+        }
         __syncthreads();
     }
     if (tid == 0) {
@@ -695,7 +713,8 @@ __global__ void __launch_bounds__(T, 512 / T)
             P.p.queue[slot] = 0u;
             P.p.queue[4 + slot] = 0u;
             __threadfence();
-            if (end_step && !ctr->diverged) ctr->t += 1;  // step_end_kernel folded in
+            if (end_step && !__ldcg(&ctr->diverged)) ctr->t += 1;  // step_end_kernel folded in
+            if (end_step) publish_counters(P);
         }
     }
 }

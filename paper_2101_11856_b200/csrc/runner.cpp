@@ -298,7 +298,9 @@ Runner::Runner(const lbmg_scene& scene, int regions, int device, int world, int 
         const size_t ns = scene_.solids.size();
         CK(cudaMallocHost(&pinned_up_, sizeof(double) * (1 + (cap_ + 2) * std::max<size_t>(ns, 1) * kMotionRow)));
         pinned_down_bytes_ = kCtrBytes + sizeof(double) * cap_ * regions_.size() * std::max<size_t>(ns, 1) * 6;
-        CK(cudaMallocHost(&pinned_down_, pinned_down_bytes_));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&pinned_down_), pinned_down_bytes_,
+                         cudaHostAllocMapped | cudaHostAllocPortable));
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&pinned_down_dev_), pinned_down_, 0));
     }
     upload_solids();
     init_fields();
@@ -336,7 +338,7 @@ Runner::~Runner() {
     if (snap_ready_) cudaEventDestroy(snap_ready_);
     if (snap_done_) cudaEventDestroy(snap_done_);
     if (pinned_up_) cudaFreeHost(pinned_up_);
-    if (pinned_down_) cudaFreeHost(pinned_down_);
+    if (pinned_down_) cudaFreeHost(pinned_down_);  // (cudaHostAlloc)
     if (pinned_temit_) cudaFreeHost(pinned_temit_);
     if (pinned_tstate_) cudaFreeHost(pinned_tstate_);
     for (auto& r : regions_) {
@@ -1063,7 +1065,14 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
     for (auto& r : regions_) {
         FluidParams P{r.geo, faces_, model_, r.ptr, ctr_};
         set_ib_totals(P, int(&r - regions_.data()));
+        // one region whose fluid kernel ends the step: results zero-copy
+        const bool zc = regions_.size() == 1 && !has_tracers_ && (!has_solids_ || fused_ib());
+        if (zc) {
+            P.p.ctr_host = reinterpret_cast<DevCounters*>(pinned_down_dev_);
+            if (P.p.ib_out) P.p.ib_out_host = reinterpret_cast<double*>(pinned_down_dev_ + kCtrBytes);
+        }
         ended = launch_fluid(P, 0, write_macro, st, false, regions_.size() == 1 && !has_tracers_);
+        zc_steps_ = zc && ended;
     }
     if (ev) CK(cudaEventRecord((*ev)[3], st));
     // emit + advect after collision, before the step counter moves (runner.cpp:213-223)
@@ -1191,8 +1200,10 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
         }
         // results of the chunk (counters + reaction totals), one sync
         const size_t tot_now = has_solids_ ? sizeof(double) * size_t(chunk) * regions_.size() * scene_.solids.size() * 6 : 0;
-        CK(cudaMemcpyAsync(pinned_down_, ctr_, (has_solids_ ? kCtrBytes : sizeof(DevCounters)) + tot_now,
-                           cudaMemcpyDeviceToHost, st));
+        // (graph steps whose fluid kernel published them zero-copy need no copy)
+        if (!(zc_steps_ && !timings && !multi_dev_))
+            CK(cudaMemcpyAsync(pinned_down_, ctr_, (has_solids_ ? kCtrBytes : sizeof(DevCounters)) + tot_now,
+                               cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         CK(cudaGetLastError());
         downloaded_ = true;

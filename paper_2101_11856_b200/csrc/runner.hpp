@@ -244,6 +244,8 @@ private:
     bool ib_overlap_ok_ = false;
     double* pinned_up_ = nullptr;      // chunk_t0 + motion rows (host -> device)
     char* pinned_down_ = nullptr;      // counters + totals (device -> host)
+    char* pinned_down_dev_ = nullptr;  // its device alias (mapped): the zero-copy results
+    bool zc_steps_ = false;            // the step graphs publish the results zero-copy
     size_t pinned_down_bytes_ = 0;
     bool downloaded_ = false;
     // rho*/u* of the last advanced step are produced on demand: the step
