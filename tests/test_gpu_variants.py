@@ -27,6 +27,8 @@ import paper_2101_11856_b200 as lbm
 from tests import scenes
 cfg = getattr(scenes, {scene!r})(**{kw!r})
 r = lbm.Runner(lbm.build_scene(cfg))
+if {variant!r} is not None:
+    r.set_variant(*{variant!r})
 for n in {chunks!r}:
     st = r.advance(n)
 out = dict(rho=r.gather_rho(), u=r.gather_u(), f=r.gather_f(), t=np.array([r.step_count()]))
@@ -37,10 +39,10 @@ np.savez({out!r}, **out)
 """
 
 
-def _run(tmp_path, tag, env_extra, scene, kw, chunks):
+def _run(tmp_path, tag, env_extra, scene, kw, chunks, variant=None):
     out = tmp_path / f"{tag}.npz"
     env = dict(os.environ, **env_extra)
-    code = CHILD.format(root=str(ROOT), scene=scene, kw=kw, chunks=chunks, out=str(out))
+    code = CHILD.format(root=str(ROOT), scene=scene, kw=kw, chunks=chunks, out=str(out), variant=variant)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     return dict(np.load(out))
@@ -97,3 +99,21 @@ def test_ib_band_path_matches_gathers(tmp_path, scene, kw):
     for k in ("rho", "u", "force", "totals"):
         rel = np.linalg.norm(a[k] - b[k]) / max(np.linalg.norm(b[k]), 1e-30)
         assert rel <= 1e-4, (k, rel)
+
+
+@pytest.mark.gpu
+def test_split_pipeline_shared_memory_scatter_matches_direct(tmp_path):
+    """The split IB pipeline's spread with per-CTA shared-memory pre-aggregation
+    (LBMG_IB_SPREAD=smem: one global RED per distinct node and component) vs
+    one RED per corner, and both vs the fused kernel."""
+    kw = dict(nx=64, ny=40, nz=40, center=(24, 20, 20), radius=6.0, subdiv=3, r=0.6)
+    chunks = [10, 1, 9]
+    a = _run(tmp_path, "smem", {"LBMG_IB_SPREAD": "smem"}, "sphere", kw, chunks, variant=(0, 1))
+    b = _run(tmp_path, "direct", {}, "sphere", kw, chunks, variant=(0, 1))
+    c = _run(tmp_path, "fused", {}, "sphere", kw, chunks)
+    for other in (b, c):
+        assert int(a["t"][0]) == int(other["t"][0]) == sum(chunks)
+        assert np.abs(a["f"] - other["f"]).max() <= 2e-5
+        for k in ("rho", "u", "force", "totals"):
+            rel = np.linalg.norm(a[k] - other[k]) / max(np.linalg.norm(other[k]), 1e-30)
+            assert rel <= 1e-4, (k, rel)
