@@ -105,9 +105,6 @@ struct IbBatch {
     const double* table;           // motion rows, table_stride doubles per solid
     size_t table_stride;
     double* partial;               // 6 per block
-    unsigned* done;                // n_solids counters
-    double* out_base;
-    int out_stride;
     int probe;
     unsigned fill_from;            // blocks >= fill_from replay the ghost-fill program (0: none)
     const float* band_m;           // band path: (rho* - 1, j*) per band node, 4 floats (null: gathers)

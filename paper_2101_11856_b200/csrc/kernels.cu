@@ -263,8 +263,8 @@ __global__ void ib_motion_once_kernel(IbSolidDev S, const double* row, int nx, i
 // penalty (ib.cpp:345-365) for samples whose support touches the slab
 // (sample_active, ib.cpp:313-317), the scatter (ib.cpp:369-454, atomic mode:
 // one fp32 RED per corner, owned nodes only, ib.cpp:377), the reaction totals
-// (ib.cpp:491-501: per-block FP64 partials, the last block sums them in block
-// order -> deterministic) and, for moving solids, the rigid motion to t+1
+// (ib.cpp:491-501: per-block FP64 partials; the region's fluid kernel sums
+// them in block order -> deterministic) and, for moving solids, the rigid motion to t+1
 // (ib.cpp:456-489).  Static solids run over the region's active samples only
 // (IbSolidDev::active, partitioned once by slab); moving ones over all.
 // (Measured alternatives, slower on C2 and configs[3]: 8-warp CTAs with a
@@ -340,7 +340,6 @@ constexpr int kFusedSamples = kFusedWarps * 32 / kLanesPerSample;
 __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     ib_fused_kernel(const __grid_constant__ FluidParams P, const __grid_constant__ IbBatch B, int det) {
     __shared__ double red[kFusedSamples][6];
-    __shared__ bool last;
     DevCounters* ctr = P.ctr;
     if (B.fill_from != 0 && blockIdx.x >= B.fill_from) {  // merged launch: the ghost-fill blocks
         if (ctr->diverged) return;
@@ -363,9 +362,6 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     const int moving = B.moving[solid] | B.probe;
     const unsigned b0 = B.block_start[solid], nblk = B.block_start[solid + 1] - b0;
     double* partial = B.partial + size_t(b0) * 6;
-    unsigned* done = B.done + solid;
-    double* out_base = B.out_base + 6 * solid;
-    const int stride = B.out_stride;
     const unsigned lane = threadIdx.x & 31u;
     const unsigned slot = threadIdx.x / kLanesPerSample;  // sample slot in the block
     const unsigned local = (blockIdx.x - b0) * kFusedSamples + slot;
@@ -467,9 +463,6 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
         for (int w2 = 0; w2 < kFusedSamples; ++w2) acc += red[w2][threadIdx.x];
         partial[(blockIdx.x - b0) * 6 + threadIdx.x] = acc;
     }
-    (void)done;
-    (void)out_base;
-    (void)stride;
     (void)nblk;
 }
 

@@ -466,7 +466,6 @@ void Runner::build_regions(int) {
             size_t blocks = 1;
             for (const auto& so : scene_.solids) blocks += size_t(std::max(1, fused_blocks(so.samples.size())));
             r.fused_partial = static_cast<double*>(dalloc(sizeof(double) * 6 * blocks, true, r.dev));
-            r.fused_done = static_cast<unsigned*>(dalloc(sizeof(unsigned) * scene_.solids.size(), true, r.dev));
         }
         for (int f = 0; f < 6; ++f) {
             const int a = face_axis(f);
@@ -968,9 +967,6 @@ void Runner::enqueue_step_multi(bool write_macro) {
             B.table = motion_tab_;
             B.table_stride = size_t(cap_ + 2) * kMotionRow;
             B.partial = r.fused_partial;
-            B.done = r.fused_done;
-            B.out_base = totals_dev_ + size_t(ri) * ns * 6;
-            B.out_stride = m * ns * 6;
             launch_ib_fused(P, B, r.batch_blocks, r.solids.data(), r.st,
                             scene_.cfg.ib_mode == LBMG_IB_DETERMINISTIC);
         }
@@ -1045,9 +1041,6 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
             B.table = motion_tab_;
             B.table_stride = size_t(cap_ + 2) * kMotionRow;
             B.partial = r.fused_partial;
-            B.done = r.fused_done;
-            B.out_base = totals_dev_ + size_t(ri) * ns * 6;
-            B.out_stride = m * ns * 6;
             if (band) {
                 launch_ib_band_moments(P, r.sband, r.sband_n, r.sband_m, st);
                 B.band_m = r.sband_m;

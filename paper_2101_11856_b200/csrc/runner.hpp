@@ -166,7 +166,6 @@ private:
         unsigned* band = nullptr;
         double* partial = nullptr;
         double* fused_partial = nullptr;  // fused IB: per-block totals
-        unsigned* fused_done = nullptr;   // one counter per solid
         IbSolidDev* batch_solids = nullptr;  // device copy of `solids` (the fused kernel's batch)
         unsigned* batch_start = nullptr;
         int* batch_moving = nullptr;
