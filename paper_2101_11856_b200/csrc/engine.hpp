@@ -100,6 +100,7 @@ struct IbBatch {
     IbSlab own, lo, hi;            // the region and its z neighbours (own where absent)
     const IbSolidDev* solids;      // device copy, n_solids
     const unsigned* block_start;   // n_solids + 1 prefix of fused_blocks(samples run)
+    const unsigned* block_solid;   // solid of each block (one load instead of a binary search)
     const int* moving;             // n_solids
     unsigned n_solids;
     const double* table;           // motion rows, table_stride doubles per solid

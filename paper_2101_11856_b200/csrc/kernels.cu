@@ -351,10 +351,14 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     const unsigned diverged = ctr->diverged;
     const RegionGeo& g = P.g;
     unsigned lo = 0, hi = B.n_solids;
-    while (hi - lo > 1) {
-        const unsigned mid = (lo + hi) >> 1;
-        if (B.block_start[mid] <= blockIdx.x) lo = mid;
-        else hi = mid;
+    if (B.block_solid != nullptr && B.n_solids > 1) {
+        lo = B.block_solid[blockIdx.x];
+    } else {
+        while (hi - lo > 1) {
+            const unsigned mid = (lo + hi) >> 1;
+            if (B.block_start[mid] <= blockIdx.x) lo = mid;
+            else hi = mid;
+        }
     }
     const unsigned solid = lo;
     const IbSolidDev S = B.n_solids == 1 ? B.solo : B.solids[solid];  // (one solid: from parameter space)
@@ -372,6 +376,10 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     const unsigned n_run = S.active ? S.n_active : S.n;
     const bool have = local < n_run;
     const unsigned s = have ? (S.active ? S.active[local] : local) : 0u;
+    // band path: the corner's band index, issued with the sample loads (it
+    // does not depend on the position)
+    const bool band = B.band_m != nullptr && S.corner_band != nullptr;
+    const unsigned cb = band && have ? S.corner_band[8u * local + corner] : ~0u;
     // static solids: (pos, u_b) stored in run order, loaded in parallel with s
     const double* pp = S.act_pu != nullptr ? S.act_pu + 6 * size_t(local) : S.pos + 3 * size_t(s);
     const double* up = S.act_pu != nullptr ? pp + 3 : S.ub + 3 * size_t(s);
@@ -389,8 +397,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 8)
     const IbSlab& R = gz < z0 ? B.lo : (gz >= z1 ? B.hi : B.own);
     const int x = act ? ks.base[0] + ox : 0, y = act ? ks.base[1] + oy : 0;
     float r = 0.f, jx = 0.f, jy = 0.f, jz = 0.f;
-    if (B.band_m != nullptr && S.corner_band != nullptr) {  // band path: the corner's moments, one 16-B load
-        const unsigned cb = have ? S.corner_band[8u * local + corner] : ~0u;
+    if (band) {  // band path: the corner's moments, one 16-B load
         if (cb != ~0u) {
             const float4 mm = __ldcg(reinterpret_cast<const float4*>(B.band_m) + cb);
             r = mm.x;

@@ -630,6 +630,12 @@ void Runner::build_active_lists() {
         if (ns) {
             CK(copy_sync(r.batch_solids, r.solids.data(), sizeof(IbSolidDev) * ns, cudaMemcpyHostToDevice));
             CK(copy_sync(r.batch_start, start.data(), sizeof(unsigned) * (ns + 1), cudaMemcpyHostToDevice));
+            std::vector<unsigned> bs(std::max<unsigned>(start[ns], 1u), 0u);
+            for (size_t k = 0; k < ns; ++k)
+                for (unsigned b = start[k]; b < start[k + 1]; ++b) bs[b] = unsigned(k);
+            if (r.batch_block_solid) dfree(r.batch_block_solid);
+            r.batch_block_solid = static_cast<unsigned*>(dalloc(sizeof(unsigned) * bs.size(), false, r.dev));
+            CK(copy_sync(r.batch_block_solid, bs.data(), sizeof(unsigned) * bs.size(), cudaMemcpyHostToDevice));
         }
         r.batch_blocks = start[ns];
     }
@@ -961,6 +967,7 @@ void Runner::enqueue_step_multi(bool write_macro) {
             B.hi = ri + 1 < m ? slab(regions_[ri + 1]) : B.own;
             B.solids = r.batch_solids;
             B.block_start = r.batch_start;
+            B.block_solid = r.batch_block_solid;
             B.moving = r.batch_moving;
             B.n_solids = unsigned(ns);
             if (ns == 1) B.solo = r.solids[0];
@@ -1035,6 +1042,7 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
             B.hi = ri + 1 < m ? slab(regions_[ri + 1]) : B.own;
             B.solids = r.batch_solids;
             B.block_start = r.batch_start;
+            B.block_solid = r.batch_block_solid;
             B.moving = r.batch_moving;
             B.n_solids = unsigned(ns);
             if (ns == 1) B.solo = r.solids[0];

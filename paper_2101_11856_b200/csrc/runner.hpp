@@ -168,6 +168,7 @@ private:
         double* fused_partial = nullptr;  // fused IB: per-block totals
         IbSolidDev* batch_solids = nullptr;  // device copy of `solids` (the fused kernel's batch)
         unsigned* batch_start = nullptr;
+        unsigned* batch_block_solid = nullptr;  // solid index per fused-IB block
         int* batch_moving = nullptr;
         unsigned batch_blocks = 0;
         std::vector<IbSolidDev> solids;
