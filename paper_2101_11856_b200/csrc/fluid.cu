@@ -568,8 +568,12 @@ __global__ void __launch_bounds__(T, 512 / T)
         fence_mbar_init();
     }
     __syncthreads();
-    if (tid == 0)
+    if (tid == 0) {
+        // the totals scratch above was written through the generic proxy:
+        // order it before the bulk copies (async proxy) into the same stage
+        if (blockIdx.x < P.p.ib_solids) fence_proxy_async_smem();
         for (int s = 0; s < kStages; ++s) refill(s, 0u);
+    }
 
     for (unsigned it = 0;; ++it) {
         const int s = int(it % kStages);

@@ -990,7 +990,7 @@ void Runner::enqueue_step_multi(bool write_macro) {
     launch_step_end(ctr_, hs);
 }
 
-void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
+void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev, bool publish) {
     if (multi_dev_) {
         enqueue_step_multi(write_macro);
         return;
@@ -1069,7 +1069,10 @@ void Runner::enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev) {
         // one region whose fluid kernel ends the step: results zero-copy
         const bool zc = regions_.size() == 1 && !has_tracers_ && (!has_solids_ || fused_ib());
         if (zc) {
-            P.p.ctr_host = reinterpret_cast<DevCounters*>(pinned_down_dev_);
+            // the counters only from the last step of an advance (a kernel that
+            // writes host memory last waits for that write before it completes);
+            // the totals rows every step (written early in the kernel)
+            if (publish) P.p.ctr_host = reinterpret_cast<DevCounters*>(pinned_down_dev_);
             if (P.p.ib_out) P.p.ib_out_host = reinterpret_cast<double*>(pinned_down_dev_ + kCtrBytes);
         }
         ended = launch_fluid(P, 0, write_macro, st, false, regions_.size() == 1 && !has_tracers_);
@@ -1093,7 +1096,9 @@ void Runner::ensure_graphs() {
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         const int n = which == 2 ? kMultiSteps : 1;
-        for (int q = 0; q < n; ++q) enqueue_step(which == 1, nullptr);
+        // [1] = the last step of an advance: publishes the counters, stores
+        // rho*/u* unless they are produced on demand
+        for (int q = 0; q < n; ++q) enqueue_step(which == 1 && !lazy_macro(), nullptr, which == 1);
         CK(cudaStreamEndCapture(st, &graph));
         size_t nn = 0;
         CK(cudaGraphGetNodes(graph, nullptr, &nn));
@@ -1193,7 +1198,9 @@ Status Runner::advance(long steps, std::vector<Timing>* timings) {
                 launches_ += graph_kernels_[2];
                 j += kMultiSteps;
             } else {
-                const int which = last && !lazy ? 1 : 0;
+                // the last step of every chunk publishes the counters its
+                // results are read from (zero-copy); [2] never ends a chunk
+                const int which = last || j == chunk - 1 ? 1 : 0;
                 CK(cudaGraphLaunch(graph_[which], st));
                 launches_ += graph_kernels_[which];
                 ++j;

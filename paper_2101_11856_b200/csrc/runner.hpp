@@ -190,7 +190,7 @@ private:
     void build_active_lists();
     void fill_motion_table(long t0, long rows, bool sync);
     void motion_row(int solid, long t, double* row) const;
-    void enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev);
+    void enqueue_step(bool write_macro, std::vector<cudaEvent_t>* ev, bool publish = true);
     void enqueue_ib_pre();
     void enqueue_ib_mid();
     bool fused_ib() const;
